@@ -1,0 +1,231 @@
+/*
+ * ridgepath_b200.h -- C ABI of the B200-native IHS-BIN ridge-path engine.
+ *
+ * Drop-in boundary for the reference's proj/core solver API (namespace
+ * ridgepath::, /root/reference/proj/core/include/ridgepath/).  Every entry point
+ * below names the reference interface it replaces.  Plain pointers and sizes
+ * only: dense matrices are column-major (Eigen::MatrixXd's layout,
+ * matrix.hpp:10), CSR uses the reference's int64 offsets/columns
+ * (matrix.hpp:16-50).  `where` says whether a buffer lives in host memory
+ * (RP_HOST, copied in/out inside the call) or in device memory on the
+ * context's GPU (RP_DEVICE, used in place; results are ready when the call
+ * returns unless stated otherwise).
+ *
+ * Errors: every function returns rp_status; the message of the last failure on
+ * a context is available from rp_last_error().  Status codes map the
+ * reference's exceptions 1:1:
+ *   std::invalid_argument          -> RP_EINVAL
+ *   BasisDivergedError             -> RP_EDIVERGED (path_solver.hpp:18-21)
+ *   SolverError                    -> RP_ESOLVER   (path_solver.hpp:23-27)
+ *   thin_svd non-convergence       -> RP_ESVD      (matrix.cpp:227-228); here:
+ *                                     shifted sketched Gram not SPD
+ * plus RP_ECUDA / RP_ENCCL / RP_ENOMEM for device-side failures.
+ *
+ * Threading: a context is single-owner (like SeededRng); calls on
+ * one context must come from one host thread.  Distinct contexts are
+ * independent.
+ */
+#ifndef RIDGEPATH_B200_H
+#define RIDGEPATH_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RP_API __attribute__((visibility("default")))
+#else
+#define RP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rp_ctx rp_ctx;
+typedef struct rp_precond rp_precond;
+
+typedef enum {
+  RP_OK = 0,
+  RP_EINVAL = 1,
+  RP_EDIVERGED = 2,
+  RP_ESOLVER = 3,
+  RP_ESVD = 4,
+  RP_ECUDA = 5,
+  RP_ENCCL = 6,
+  RP_ENOMEM = 7
+} rp_status;
+
+enum { RP_HOST = 0, RP_DEVICE = 1 };
+
+/* SketchKind, sketch.hpp:10 (same order). */
+typedef enum {
+  RP_SKETCH_GAUSSIAN = 0,
+  RP_SKETCH_COUNTSKETCH = 1,
+  RP_SKETCH_SJLT = 2,
+  RP_SKETCH_SRHT = 3,
+  RP_SKETCH_IDENTITY = 4
+} rp_sketch_kind;
+
+/* SketchSpec, sketch.hpp:17-29. */
+typedef struct {
+  int32_t kind; /* rp_sketch_kind */
+  int32_t s;    /* SJLT column sparsity */
+  int64_t m;    /* sketch rows */
+  int64_t n;    /* input rows (rows of the operator) */
+  uint64_t seed;
+} rp_sketch_spec;
+
+/* PathConfig, spectrum.hpp:14-22.  num_intervals <= 0 selects the automatic
+ * split (std::nullopt). */
+typedef struct {
+  double lambda_min;
+  double lambda_max;
+  const double* lambdas; /* host */
+  int64_t num_lambdas;
+  double epsilon;
+  int32_t num_intervals;
+} rp_path_config;
+
+/* RhoBounds, spectrum.hpp:32-40; provenance follows RhoProvenance
+ * (0 Gaussian, 1 Sjlt, 2 Srht, 3 Identity, 4 Manual). */
+typedef struct {
+  double rho1;
+  double rho2;
+  int32_t provenance;
+} rp_rho_bounds;
+
+/* RateParams, spectrum.hpp:43-49. */
+typedef struct {
+  double lambda0;
+  double alpha;
+  double kappa;
+  double contraction;
+  int32_t k;
+} rp_rate_params;
+
+/* Timings of the last path call (RegPathResult setup/total seconds,
+ * path_solver.hpp:58-62, split per phase; device-timed with CUDA events). */
+typedef struct {
+  double setup_seconds;   /* sketch + factor + all interval bases */
+  double eval_seconds;    /* compose (+ dual recovery) */
+  double total_seconds;   /* setup + eval (excludes host<->device copies) */
+  double sketch_seconds;
+  double factor_seconds;  /* c = M^T b, Gram matrix, shifted inverses */
+  double basis_seconds;
+  double copy_seconds;    /* host<->device copies inside the call */
+  int32_t retries;        /* intervals rebuilt at tau/2 */
+  int32_t gram_mode;      /* 0 = pass over the operator, 1 = Gram matrix */
+  int64_t launches;       /* kernels launched by the call */
+  /* With rp_set_option(ctx, "profile", 1): every FP64 DMMA GEMM of the call
+   * bracketed by CUDA events on the call's stream. */
+  double gemm_seconds;    /* summed GEMM kernel time */
+  double gemm_flops;      /* algorithmic flops of those GEMMs */
+  int64_t gemm_calls;
+} rp_timings;
+
+/* ---- context -------------------------------------------------------------- */
+RP_API const char* rp_version(void);
+RP_API rp_status rp_create(rp_ctx** out, int device);
+RP_API void rp_destroy(rp_ctx* ctx);
+RP_API const char* rp_last_error(const rp_ctx* ctx);
+/* Run the context's work on an external CUDA stream (cudaStream_t), or NULL
+ * for the context's own stream. */
+RP_API rp_status rp_set_stream(rp_ctx* ctx, void* stream);
+RP_API rp_status rp_synchronize(rp_ctx* ctx);
+/* Options: "gram_mode" (-1 auto, 0 pass, 1 matrix); "profile" (0/1). */
+RP_API rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value);
+RP_API int64_t rp_launch_count(void);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) -------------------- */
+RP_API rp_status rp_comm_unique_id(void* id128);
+RP_API rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128);
+
+/* ---- data operator ----------------------------------------------------------
+ * Matrix, matrix.hpp:54-73.  The context keeps one operator A (n x d).  With
+ * several ranks each passes its shard: rows [row0, row0 + n_local) of the
+ * n_global x d matrix (primal route, row-sharded).  The dual route column-
+ * shards A: pass the local column block with rp_set_dense_cols. */
+RP_API rp_status rp_set_dense(rp_ctx* ctx, int64_t n, int64_t d, const double* a, int64_t lda, int where);
+RP_API rp_status rp_set_dense_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t d,
+                            const double* a, int64_t lda, int where);
+RP_API rp_status rp_set_dense_cols(rp_ctx* ctx, int64_t n, int64_t d_global, int64_t col0, int64_t d_local,
+                            const double* a, int64_t lda, int where);
+RP_API rp_status rp_set_csr(rp_ctx* ctx, int64_t n, int64_t d, const int64_t* offsets, const int64_t* cols,
+                     const double* vals, int where);
+RP_API rp_status rp_set_csr_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t d,
+                          const int64_t* offsets, const int64_t* cols, const double* vals, int where);
+
+/* ---- building blocks -------------------------------------------------------
+ * apply / apply_transpose / gram_apply (matrix.hpp:81-92): y = A x,
+ * x = A^T y, out = A^T (A x) for `ncols` column-major right-hand sides. */
+RP_API rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int where);
+RP_API rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double* x, int where);
+RP_API rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out, int where);
+
+/* sketch_apply (sketch.hpp:43): SA (m x d) of the context's operator;
+ * `transpose_op` = 1 sketches A^T instead (the dual route's operator). */
+RP_API rp_status rp_sketch_apply(rp_ctx* ctx, const rp_sketch_spec* spec, int transpose_op, double* sa, int where);
+
+/* Preconditioner::build / reshift / apply (preconditioner.hpp:24-34).
+ * P = (SA^T SA + lambda0 I)^{-1}, explicit for m >= d, Woodbury for m < d. */
+RP_API rp_status rp_precond_build(rp_ctx* ctx, const double* sa, int64_t m, int64_t d, double lambda0, int where,
+                           rp_precond** out);
+RP_API rp_status rp_precond_reshift(rp_ctx* ctx, const rp_precond* p, double lambda0, rp_precond** out);
+RP_API rp_status rp_precond_apply(rp_ctx* ctx, const rp_precond* p, const double* v, int64_t ncols, double* out,
+                           int where);
+RP_API void rp_precond_destroy(rp_precond* p);
+
+/* ihs_basis / ihs_basis_matrix (path_solver.hpp:89-96): c = A^T b, then the
+ * recursion; terms_out is k blocks of d x K (column-major, block j at
+ * j*d*K).  ihs_basis_core takes c directly (path_solver.cpp:27-53). */
+RP_API rp_status rp_ihs_basis(rp_ctx* ctx, const rp_precond* p, const double* b, int64_t K, double tau, int32_t k,
+                       double* terms_out, int where);
+RP_API rp_status rp_ihs_basis_core(rp_ctx* ctx, const rp_precond* p, const double* c, int64_t K, double tau, int32_t k,
+                            int transpose_op, double* terms_out, int where);
+/* ihs_compose / ihs_compose_matrix (path_solver.hpp:98-101): tau * sum_j (tau lambda)^j u_j. */
+RP_API rp_status rp_ihs_compose(rp_ctx* ctx, const double* terms, int64_t dim, int64_t K, int32_t k, double tau,
+                         double lambda, double* x_out, int where);
+
+/* ---- end-to-end paths ------------------------------------------------------
+ * ihs_bin_path / ihs_bin_path_matrix (path_solver.hpp:109-121) for K = 1 / K > 1:
+ * b is n x K; x_out receives the d x K solution for every grid lambda, point t
+ * at x_out + t*d*K.  dual_path (path_solver.hpp:134-139), matrix B handled as
+ * K independent dual paths: x_out is d x K per lambda (the local column block
+ * when A is column-sharded).  sigma_d may be NULL (std::nullopt). */
+RP_API rp_status rp_ihs_bin_path(rp_ctx* ctx, const double* b, int64_t K, const rp_path_config* cfg,
+                          const rp_sketch_spec* spec, const rp_rho_bounds* rho, const double* sigma_d,
+                          double* x_out, int where, rp_timings* timings);
+RP_API rp_status rp_dual_path(rp_ctx* ctx, const double* b, int64_t K, const rp_path_config* cfg, const rp_sketch_spec* spec,
+                       const rp_rho_bounds* rho, const double* sigma_d, double* x_out, int where,
+                       rp_timings* timings);
+
+/* ---- host scalar tuning (spectrum.hpp; bit-identical to the reference) ---- */
+RP_API rp_status rp_log_grid(double lambda_min, double lambda_max, int32_t count, double* out);
+RP_API rp_status rp_tune_interval(double lambda_lo, double lambda_hi, const rp_rho_bounds* rho, const double* sigma_d,
+                           double eps, rp_rate_params* out);
+RP_API int32_t rp_auto_interval_count(double lambda_min, double lambda_max);
+RP_API rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_intervals, double* edges_out,
+                            int32_t* count_out);
+
+/* ---- draw contract (rng.hpp / sketch.cpp draw loops), device-generated ---- */
+RP_API rp_status rp_draw_u64(rp_ctx* ctx, uint64_t seed, uint64_t skip, int64_t count, uint64_t* out, int where);
+RP_API rp_status rp_draw_uniform01(rp_ctx* ctx, uint64_t seed, int64_t count, double* out, int where);
+RP_API rp_status rp_draw_sign(rp_ctx* ctx, uint64_t seed, int64_t count, double* out, int where);
+RP_API rp_status rp_draw_uniform_index(rp_ctx* ctx, uint64_t seed, uint64_t bound, int64_t count, uint64_t* out,
+                                int where);
+/* normals #first .. #first+count-1 of SeededRng(seed).normal(), times scale */
+RP_API rp_status rp_draw_normals(rp_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double scale, double* out,
+                          int where);
+/* Gaussian sketch window S[r0:r0+rc, j0:j0+jc] (row-major rc x jc). */
+RP_API rp_status rp_gaussian_window(rp_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64_t r0, int64_t rc, int64_t j0,
+                             int64_t jc, double* out, int where);
+RP_API rp_status rp_count_draws(rp_ctx* ctx, const rp_sketch_spec* spec, int64_t* h_out, double* sign_out, int where);
+RP_API rp_status rp_srht_draws(rp_ctx* ctx, const rp_sketch_spec* spec, double* signs_out, int64_t* rows_out, int where);
+
+/* Host-only self-check of the jump-ahead engine: 0 on success. */
+RP_API int rp_mt_selfcheck(uint64_t seed, uint64_t offset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RIDGEPATH_B200_H */

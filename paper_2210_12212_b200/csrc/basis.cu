@@ -1,0 +1,191 @@
+// Recursion epilogues, Horner composition and sparse Gram helpers.
+#include <algorithm>
+
+#include "basis.h"
+#include "common.h"
+
+namespace rpb {
+namespace {
+
+unsigned grid_for(int64_t work, int threads = 256) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), 148 * 32)));
+}
+
+__global__ void build_args_kernel(BasisDims d, int64_t g, const double* __restrict__ y,
+                                  const double* __restrict__ gen, const double* __restrict__ tau,
+                                  double* __restrict__ args) {
+  const int64_t nb = d.L * d.K;
+  const int64_t total = d.dim * (g + 1) * nb;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % d.dim;
+    const int64_t col = idx / d.dim;  // = j*NB + b
+    const int64_t j = col / nb, b = col % nb;
+    const int64_t l = b / d.K, r = b % d.K;
+    double v;
+    if (j < g) {
+      v = __dmul_rn(tau[l], y[i + (j * nb + b) * d.dim]);
+      if (j >= 1) v = __dadd_rn(v, gen[i + ((j - 1) * nb + b) * d.dim]);
+    } else {
+      v = gen[i + ((g - 1) * nb + b) * d.dim];
+    }
+    args[i + (l * d.kmax * d.K + j * d.K + r) * d.dim] = v;
+  }
+}
+
+__global__ void update_kernel(BasisDims d, int64_t g, const double* __restrict__ applied, const int* __restrict__ kb,
+                              double* __restrict__ gen, double* __restrict__ tilde, int* __restrict__ flags) {
+  const int64_t nb = d.L * d.K;
+  const int64_t total = d.dim * (g + 1) * nb;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % d.dim;
+    const int64_t col = idx / d.dim;
+    const int64_t j = col / nb, b = col % nb;
+    const int64_t l = b / d.K, r = b % d.K;
+    if (g >= kb[l]) continue;  // this interval's loop has ended (path_solver.cpp:39)
+    const double a = applied[i + (l * d.kmax * d.K + j * d.K + r) * d.dim];
+    double* gp = gen + i + col * d.dim;
+    const double v = (j < g) ? __dsub_rn(*gp, a) : -a;
+    *gp = v;
+    if (!isfinite(v)) flags[l] = 1;
+    double* tp = tilde + i + col * d.dim;
+    *tp = __dadd_rn(*tp, v);
+  }
+}
+
+__global__ void compose_kernel(BasisDims d, const double* __restrict__ tilde, const double* __restrict__ tau,
+                               const int* __restrict__ kb, const double* __restrict__ lambda,
+                               const int* __restrict__ interval, int64_t T, double* __restrict__ x) {
+  const int64_t nb = d.L * d.K;
+  const int64_t total = d.dim * d.K * T;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % d.dim;
+    const int64_t col = idx / d.dim;  // t*K + r
+    const int64_t t = col / d.K, r = col % d.K;
+    const int l = interval[t];
+    const int64_t b = l * d.K + r;
+    const double ta = tau[l];
+    const double tt = __dmul_rn(ta, lambda[t]);
+    const int k = kb[l];
+    double v = tilde[i + ((k - 1) * nb + b) * d.dim];
+    for (int j = k - 2; j >= 0; --j) v = __dadd_rn(tilde[i + (j * nb + b) * d.dim], __dmul_rn(tt, v));
+    x[i + col * d.dim] = __dmul_rn(v, ta);
+  }
+}
+
+__global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, int64_t stride,
+                                     const double* __restrict__ args, const double* __restrict__ t3,
+                                     const double* __restrict__ lambda0, double* __restrict__ out) {
+  const int64_t per = dim * cols;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < per * L;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t l = idx / per, e = idx % per;
+    const int64_t o = l * stride + e;
+    out[o] = __ddiv_rn(__dsub_rn(args[o], t3[o]), lambda0[l]);
+  }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
+                                 double* __restrict__ out, int64_t ldo) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r + c * ldi];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + k;
+    if (r < rows && c < cols) out[c + r * ldo] = tile[threadIdx.x][k];
+  }
+}
+
+// One warp per row; lanes stride over the c right-hand sides.
+__global__ void spmm_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, int64_t n, int64_t c, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t row = warp; row < n; row += nwarps) {
+    const int64_t p0 = off[row], p1 = off[row + 1];
+    for (int64_t cc = lane; cc < c; cc += 32) {
+      double acc = 0.0;
+      for (int64_t p = p0; p < p1; ++p) acc = __dadd_rn(acc, __dmul_rn(val[p], x[static_cast<int64_t>(col[p]) * c + cc]));
+      y[row * c + cc] = acc;
+    }
+  }
+}
+
+__global__ void copy_cols_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                 double* __restrict__ dst, int64_t ldd) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rows * cols;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    dst[i + j * ldd] = src[i + j * lds];
+  }
+}
+
+__global__ void fill_kernel(double* __restrict__ dst, int64_t count, double v) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < count;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[idx] = v;
+}
+
+}  // namespace
+
+void build_args(const BasisDims& d, int64_t g, const double* y, const double* gen, const double* d_tau,
+                double* args_im, cudaStream_t stream) {
+  build_args_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, y, gen, d_tau, args_im);
+  RP_LAUNCH_CHECK();
+}
+
+void update_gen(const BasisDims& d, int64_t g, const double* applied_im, const int* d_k, double* gen, double* tilde,
+                int* d_flags, cudaStream_t stream) {
+  update_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, applied_im, d_k, gen, tilde, d_flags);
+  RP_LAUNCH_CHECK();
+}
+
+void compose(const BasisDims& d, const double* tilde, const double* d_tau, const int* d_k, const double* d_lambda,
+             const int* d_interval, int64_t T, double* x, cudaStream_t stream) {
+  if (T <= 0) return;
+  compose_kernel<<<grid_for(d.dim * d.K * T), 256, 0, stream>>>(d, tilde, d_tau, d_k, d_lambda, d_interval, T, x);
+  RP_LAUNCH_CHECK();
+}
+
+void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,
+                   const double* d_lambda0, double* out, cudaStream_t stream) {
+  woodbury_tail_kernel<<<grid_for(dim * cols * L), 256, 0, stream>>>(dim, cols, L, stride, args, t3, d_lambda0, out);
+  RP_LAUNCH_CHECK();
+}
+
+void transpose(const double* in, int64_t rows, int64_t cols, int64_t ldi, double* out, int64_t ldo,
+               cudaStream_t stream) {
+  dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(cols, 32)));
+  transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(in, rows, cols, ldi, out, ldo);
+  RP_LAUNCH_CHECK();
+}
+
+void spmm_csr_rm(const int64_t* off, const int32_t* col, const double* val, int64_t n, int64_t c, const double* x_rm,
+                 double* y_rm, cudaStream_t stream) {
+  if (n <= 0 || c <= 0) return;
+  spmm_kernel<<<grid_for(n * 32, 256), 256, 0, stream>>>(off, col, val, n, c, x_rm, y_rm);
+  RP_LAUNCH_CHECK();
+}
+
+void copy_cols(const double* src, int64_t rows, int64_t cols, int64_t lds, double* dst, int64_t ldd,
+               cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  copy_cols_kernel<<<grid_for(rows * cols), 256, 0, stream>>>(src, rows, cols, lds, dst, ldd);
+  RP_LAUNCH_CHECK();
+}
+
+void fill(double* dst, int64_t count, double v, cudaStream_t stream) {
+  if (count <= 0) return;
+  fill_kernel<<<grid_for(count), 256, 0, stream>>>(dst, count, v);
+  RP_LAUNCH_CHECK();
+}
+
+}  // namespace rpb

@@ -1,0 +1,59 @@
+// Elementwise / gather kernels of the binomial-basis recursion
+// (path_solver.cpp:27-53), the Horner composition (path_solver.cpp:64-74) and
+// the sparse Gram pieces (matrix.cpp:140-166).
+//
+// Layouts.  NB = L*K independent recursions ("problems") b = l*K + r for
+// interval l and right-hand side r.  gen / tilde are dim x (kmax*NB)
+// column-major with column j*NB + b = basis term j of problem b, so that the
+// first g*NB columns are exactly the block W = gen[:, :g] of every problem and
+// one Gram product serves all of them.  The preconditioner works on the
+// interval-major layout im[l] = dim x (kmax*K) with column j*K + r.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rpb {
+
+struct BasisDims {
+  int64_t dim = 0;
+  int64_t L = 0;     // intervals in this batch
+  int64_t K = 0;     // right-hand sides
+  int64_t kmax = 0;  // max budget over the intervals
+  int64_t nb() const { return L * K; }
+};
+
+// args_im[l][:, j*K + r] = tau_l * Y[:, j*NB + b] + (j >= 1 ? gen[:, (j-1)*NB + b] : 0) for j < g
+// args_im[l][:, g*K + r] = gen[:, (g-1)*NB + b]
+void build_args(const BasisDims& d, int64_t g, const double* y, const double* gen, const double* d_tau,
+                double* args_im, cudaStream_t stream);
+
+// gen[:, j*NB+b] -= applied[l][:, j*K+r] (j < g); gen[:, g*NB+b] = -applied[l][:, g*K+r];
+// flags[l] |= any non-finite in gen[:, 0..g]; tilde[:, j*NB+b] += gen[:, j*NB+b] (j <= g).
+// Problems whose interval has k_l <= g are left untouched.
+void update_gen(const BasisDims& d, int64_t g, const double* applied_im, const int* d_k, double* gen, double* tilde,
+                int* d_flags, cudaStream_t stream);
+
+// x[:, t*K + r] = tau_l * Horner(tilde of problem l*K + r, tau_l * lambda_t) for t < T,
+// where l = d_interval[t].  Reference: compose_horner, path_solver.cpp:64-74.
+void compose(const BasisDims& d, const double* tilde, const double* d_tau, const int* d_k, const double* d_lambda,
+             const int* d_interval, int64_t T, double* x, cudaStream_t stream);
+
+// out = (args - t3) / lambda0_l, interval-major (Woodbury preconditioner tail).
+void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,
+                   const double* d_lambda0, double* out, cudaStream_t stream);
+
+// Row-major helpers for the CSR Gram.
+void transpose(const double* in, int64_t rows, int64_t cols, int64_t ldi, double* out, int64_t ldo,
+               cudaStream_t stream);  // out (cols x rows, col-major) = in^T (in: rows x cols col-major)
+// y_rm (n x c, row-major) = CSR(M) * x_rm (D x c, row-major): per row, entries in stored order.
+void spmm_csr_rm(const int64_t* off, const int32_t* col, const double* val, int64_t n, int64_t c, const double* x_rm,
+                 double* y_rm, cudaStream_t stream);
+
+// Scale-and-copy helpers.
+void copy_cols(const double* src, int64_t rows, int64_t cols, int64_t lds, double* dst, int64_t ldd,
+               cudaStream_t stream);
+void fill(double* dst, int64_t count, double v, cudaStream_t stream);
+
+}  // namespace rpb

@@ -1,0 +1,299 @@
+// Batched SPD inverse: potrf (right-looking, 64-wide panels) -> trtri
+// (recursive doubling) -> P = L^{-T} L^{-1}; the O(n^3) parts run as DMMA GEMMs.
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "factor.h"
+#include "gemm_f64.h"
+
+namespace rpb {
+namespace {
+
+constexpr int NB = 64;
+
+// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix.
+__global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
+                                                  int* info) {
+  __shared__ double T[NB][NB + 1];
+  double* A = h + blockIdx.x * stride + k0 + k0 * ld;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    T[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = T[j][j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        if (info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + j + 1);
+        T[j][j] = 1.0;  // keep going; the caller reports the failure
+      } else {
+        T[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    const double piv = T[j][j];
+    for (int i = j + 1 + threadIdx.x; i < kb; i += blockDim.x) T[i][j] /= piv;
+    __syncthreads();
+    const int rem = kb - j - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int i = j + 1 + e % rem, c = j + 1 + e / rem;
+      if (i >= c) T[i][c] -= T[i][j] * T[c][j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    if (i >= j) A[i + j * ld] = T[i][j];
+  }
+}
+
+// Panel solve X * L11^T = B for the rows below the diagonal block.
+__global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
+                                                  int64_t rows) {
+  extern __shared__ double dsm[];
+  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
+  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+  double* base = h + blockIdx.y * stride;
+  const double* L11 = base + k0 + k0 * ld;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    L[i][j] = L11[i + j * ld];
+  }
+  const int64_t r0 = k0 + kb + static_cast<int64_t>(blockIdx.x) * 128;
+  const int nr = static_cast<int>((k0 + kb + rows - r0) < 128 ? (k0 + kb + rows - r0) : 128);
+  double* B = base + k0 * ld;  // column k0 of the matrix
+  for (int e = threadIdx.x; e < nr * kb; e += blockDim.x) {
+    const int i = e % nr, j = e / nr;
+    X[i][j] = B[r0 + i + j * ld];
+  }
+  __syncthreads();
+  const int r = threadIdx.x;
+  if (r < nr) {
+    for (int j = 0; j < kb; ++j) {
+      double s = X[r][j];
+      for (int i = 0; i < j; ++i) s -= X[r][i] * L[j][i];
+      X[r][j] = s / L[j][j];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * kb; e += blockDim.x) {
+    const int i = e % nr, j = e / nr;
+    B[r0 + i + j * ld] = X[i][j];
+  }
+}
+
+// In-place inverse of each nb x nb lower-triangular diagonal block; zeroes the
+// strict upper triangle of the whole matrix on the way.
+__global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t ld, int64_t stride) {
+  extern __shared__ double dsm[];
+  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
+  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * NB;
+  const int kb = static_cast<int>((n - k0) < NB ? (n - k0) : NB);
+  double* A = h + blockIdx.y * stride + k0 + k0 * ld;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < kb) {
+    X[c][c] = 1.0 / L[c][c];
+    for (int i = 0; i < c; ++i) X[i][c] = 0.0;
+    for (int i = c + 1; i < kb; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s += L[i][k] * X[k][c];
+      X[i][c] = -s / L[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    A[i + j * ld] = X[i][j];
+  }
+}
+
+__global__ void zero_upper(double* h, int64_t n, int64_t ld, int64_t stride) {
+  double* A = h + blockIdx.y * stride;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n * n;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    if (i < j) A[i + j * ld] = 0.0;
+  }
+}
+
+__global__ void shifted_copy_kernel(const double* __restrict__ g, int64_t n, const double* __restrict__ shifts,
+                                    double* __restrict__ h) {
+  const int64_t b = blockIdx.y;
+  const double s = shifts[b];
+  double* H = h + b * n * n;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n * n;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    H[idx] = (i == j) ? g[idx] + s : g[idx];
+  }
+}
+
+unsigned grid1(int64_t work) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 8)));
+}
+
+}  // namespace
+
+void shifted_copies(const double* g, int64_t n, const double* d_shifts, int64_t batch, double* h, cudaStream_t stream) {
+  dim3 grid(grid1(n * n), static_cast<unsigned>(batch));
+  shifted_copy_kernel<<<grid, 256, 0, stream>>>(g, n, d_shifts, h);
+  RP_LAUNCH_CHECK();
+}
+
+void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64_t batch, double* out, int64_t ldo,
+                         int64_t stride_o, cudaStream_t stream) {
+  require(n >= 1 && batch >= 1, "spd_inverse: empty problem");
+  DBuf<int> info(static_cast<size_t>(batch), stream);
+  RP_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int) * batch, stream));
+  // 1) Cholesky, lower.
+  for (int64_t k0 = 0; k0 < n; k0 += NB) {
+    const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
+    potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
+    RP_LAUNCH_CHECK();
+    const int64_t rows = n - k0 - kb;
+    if (rows <= 0) break;
+    dim3 tg(static_cast<unsigned>(ceil_div(rows, 128)), static_cast<unsigned>(batch));
+    constexpr int kTrsmSmem = (NB + 128) * (NB + 1) * 8;
+    static bool attr = false;
+    if (!attr) {
+      RP_CUDA(cudaFuncSetAttribute(potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
+      attr = true;
+    }
+    potrf_trsm<<<tg, 128, kTrsmSmem, stream>>>(h, ld, stride, k0, kb, rows);
+    RP_LAUNCH_CHECK();
+    GemmArgs g;  // A22 -= A21 A21^T (lower)
+    g.opa = Op::N;
+    g.opb = Op::T;
+    g.m = rows;
+    g.n = rows;
+    g.k = kb;
+    g.alpha = -1.0;
+    g.beta = 1.0;
+    g.a = h + (k0 + kb) + k0 * ld;
+    g.lda = ld;
+    g.stride_a = stride;
+    g.b = g.a;
+    g.ldb = ld;
+    g.stride_b = stride;
+    g.c = h + (k0 + kb) + (k0 + kb) * ld;
+    g.ldc = ld;
+    g.stride_c = stride;
+    g.batch = batch;
+    g.lower_only = true;
+    g.split_k = 1;
+    dgemm(g, stream);
+  }
+  // 2) Triangular inverse in place.
+  {
+    dim3 zg(grid1(n * n), static_cast<unsigned>(batch));
+    zero_upper<<<zg, 256, 0, stream>>>(h, n, ld, stride);
+    RP_LAUNCH_CHECK();
+    dim3 dg(static_cast<unsigned>(ceil_div(n, NB)), static_cast<unsigned>(batch));
+    constexpr int kDiagSmem = 2 * NB * (NB + 1) * 8;
+    static bool attr = false;
+    if (!attr) {
+      RP_CUDA(cudaFuncSetAttribute(trtri_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem));
+      attr = true;
+    }
+    trtri_diag<<<dg, 64, kDiagSmem, stream>>>(h, n, ld, stride);
+    RP_LAUNCH_CHECK();
+    DBuf<double> tmp;
+    for (int64_t s = NB; s < n; s *= 2) {
+      const int64_t pairs_full = n / (2 * s);
+      // full pairs: blocks [i*2s, i*2s+s) and [i*2s+s, i*2s+2s)
+      auto combine = [&](int64_t first, int64_t npairs, int64_t s2) {
+        if (npairs <= 0 || s2 <= 0) return;
+        const size_t need = static_cast<size_t>(npairs * batch * s2 * s);
+        if (tmp.size() < need) tmp.alloc(need, stream);
+        const int64_t pstride = 2 * s * (ld + 1);
+        double* base = h + first * 2 * s * (ld + 1);
+        // T = L21 * L11^{-1}   (s2 x s)
+        GemmArgs g1;
+        g1.m = s2;
+        g1.n = s;
+        g1.k = s;
+        g1.a = base + s;  // L21 at (i*2s + s, i*2s)
+        g1.lda = ld;
+        g1.stride_a = pstride;
+        g1.stride_a2 = stride;
+        g1.b = base;  // L11^{-1}
+        g1.ldb = ld;
+        g1.stride_b = pstride;
+        g1.stride_b2 = stride;
+        g1.c = tmp.get();
+        g1.ldc = s2;
+        g1.stride_c = s2 * s;
+        g1.stride_c2 = s2 * s * npairs;
+        g1.batch = npairs;
+        g1.batch2 = batch;
+        g1.split_k = 1;
+        dgemm(g1, stream);
+        // X21 = -L22^{-1} * T  -> written over L21
+        GemmArgs g2;
+        g2.m = s2;
+        g2.n = s;
+        g2.k = s2;
+        g2.alpha = -1.0;
+        g2.a = base + s + s * ld;  // L22^{-1}
+        g2.lda = ld;
+        g2.stride_a = pstride;
+        g2.stride_a2 = stride;
+        g2.b = tmp.get();
+        g2.ldb = s2;
+        g2.stride_b = s2 * s;
+        g2.stride_b2 = s2 * s * npairs;
+        g2.c = base + s;
+        g2.ldc = ld;
+        g2.stride_c = pstride;
+        g2.stride_c2 = stride;
+        g2.batch = npairs;
+        g2.batch2 = batch;
+        g2.split_k = 1;
+        dgemm(g2, stream);
+      };
+      combine(0, pairs_full, s);
+      const int64_t tail0 = pairs_full * 2 * s;
+      if (tail0 + s < n) combine(pairs_full, 1, n - tail0 - s);
+    }
+  }
+  // 3) out = L^{-T} L^{-1} (symmetric).
+  {
+    GemmArgs g;
+    g.opa = Op::T;
+    g.opb = Op::N;
+    g.m = n;
+    g.n = n;
+    g.k = n;
+    g.a = h;
+    g.lda = ld;
+    g.stride_a = stride;
+    g.b = h;
+    g.ldb = ld;
+    g.stride_b = stride;
+    g.c = out;
+    g.ldc = ldo;
+    g.stride_c = stride_o;
+    g.batch = batch;
+    g.lower_only = true;
+    g.mirror = true;
+    dgemm(g, stream);
+  }
+  std::vector<int> hinfo(static_cast<size_t>(batch));
+  RP_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), sizeof(int) * batch, cudaMemcpyDeviceToHost, stream));
+  RP_CUDA(cudaStreamSynchronize(stream));
+  for (int64_t b = 0; b < batch; ++b)
+    if (hinfo[b])
+      throw FactorFailure("factorization: shifted sketched Gram is not positive definite (matrix " +
+                          std::to_string(b) + ", column " + std::to_string(hinfo[b]) + ")");
+}
+
+}  // namespace rpb

@@ -1,0 +1,452 @@
+// FP64 DMMA GEMM for sm_100a (see gemm_f64.h for the contract).
+//
+// Layout of one CTA: BM x BN output tile, WM x WN warps, each warp owning a
+// (BM/WM) x (BN/WN) register tile built from m8n8k4 DMMA fragments.  Operands
+// move global -> shared through a STAGES-deep cp.async ring; every operand has
+// two shared layouts so the 16-byte copies stay contiguous in global memory:
+//   MN-major  (op(A) = A, op(B) = B^T):  smem[k][mn], row stride MN + 4 doubles
+//   K-major   (op(A) = A^T, op(B) = B):  smem[mn][k], row stride BK + 4 doubles
+// Strides = 4 (mod 16) doubles keep the DMMA fragment loads (8 rows x 4 k)
+// free of shared-memory bank conflicts within each half-warp.
+#include "common.h"
+#include "gemm_f64.h"
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+namespace rpb {
+namespace {
+
+thread_local int g_last_launches = 0;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct KParams {
+  int64_t m, n, k;
+  double alpha, beta;
+  const double* a;
+  int64_t lda, stride_a;
+  const double* b;
+  int64_t ldb, stride_b;
+  double* c;
+  int64_t ldc, stride_c;
+  int64_t batch;
+  int64_t batch2;
+  int64_t stride_a2, stride_b2, stride_c2;
+  int split;        // number of K splits
+  int64_t k_chunk;  // K per split (multiple of the tile K)
+  double* ws;       // split partials: [batch][split][n][m]
+  bool lower_only;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+struct Cfg {
+  static constexpr int THREADS = WM * WN * 32;
+  static constexpr int TM = BM / WM;
+  static constexpr int TN = BN / WN;
+  static constexpr int FM = TM / 8;
+  static constexpr int FN = TN / 8;
+  static constexpr int A_LD = AK ? (BK + 4) : (BM + 4);
+  static constexpr int A_ROWS = AK ? BM : BK;
+  static constexpr int B_LD = BKM ? (BK + 4) : (BN + 4);
+  static constexpr int B_ROWS = BKM ? BN : BK;
+  static constexpr int A_STAGE = A_ROWS * A_LD;
+  static constexpr int B_STAGE = B_ROWS * B_LD;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+  static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile must be a multiple of 8");
+  static_assert(BK % 4 == 0, "BK must be a multiple of 4");
+};
+
+// Load an MN x BK operand tile (op(X) is MN x K) into shared memory.
+// KMAJ: the operand is contiguous along k in global memory.
+template <int MN_T, int BK, int LD, int THREADS, bool KMAJ, int VEC>
+__device__ __forceinline__ void load_tile(double* sm, const double* g, int64_t ld, int64_t mn0,
+                                          int64_t mn_lim, int64_t k0, int64_t k_lim, int tid) {
+  if (!KMAJ) {
+    constexpr int CPR = MN_T / VEC;
+    constexpr int TOTAL = BK * CPR;
+#pragma unroll
+    for (int c = tid; c < TOTAL; c += THREADS) {
+      const int kk = c / CPR;
+      const int mm = (c % CPR) * VEC;
+      const int64_t gm = mn0 + mm, gk = k0 + kk;
+      int bytes = 0;
+      const double* src = g;
+      if (gk < k_lim && gm < mn_lim) {
+        bytes = static_cast<int>(mn_lim - gm < VEC ? mn_lim - gm : VEC) * 8;
+        src = g + gm + gk * ld;
+      }
+      double* dst = sm + kk * LD + mm;
+      if (VEC == 2)
+        cp_async16(dst, src, bytes);
+      else
+        cp_async8(dst, src, bytes);
+    }
+  } else {
+    constexpr int CPR = BK / VEC;
+    constexpr int TOTAL = MN_T * CPR;
+#pragma unroll
+    for (int c = tid; c < TOTAL; c += THREADS) {
+      const int mm = c / CPR;
+      const int kk = (c % CPR) * VEC;
+      const int64_t gm = mn0 + mm, gk = k0 + kk;
+      int bytes = 0;
+      const double* src = g;
+      if (gm < mn_lim && gk < k_lim) {
+        bytes = static_cast<int>(k_lim - gk < VEC ? k_lim - gk : VEC) * 8;
+        src = g + gk + gm * ld;
+      }
+      double* dst = sm + mm * LD + kk;
+      if (VEC == 2)
+        cp_async16(dst, src, bytes);
+      else
+        cp_async8(dst, src, bytes);
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+__global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * C::A_STAGE;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm = warp % WM;
+  const int wn = warp / WM;
+
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
+  if (p.lower_only && m0 + BM <= n0) return;  // tile strictly above the diagonal
+  const int64_t z = blockIdx.z;
+  const int64_t bidx = z / p.split;
+  const int sidx = static_cast<int>(z % p.split);
+  const int64_t b1 = bidx % p.batch, b2 = bidx / p.batch;
+  const double* A = p.a + b1 * p.stride_a + b2 * p.stride_a2;
+  const double* B = p.b + b1 * p.stride_b + b2 * p.stride_b2;
+  const int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
+  const int64_t kend = min(p.k, kbeg + p.k_chunk);
+  const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int kt, int stage) {
+    const int64_t k0 = kbeg + static_cast<int64_t>(kt) * BK;
+    load_tile<BM, BK, C::A_LD, C::THREADS, AK, VEC>(As + stage * C::A_STAGE, A, p.lda, m0, p.m, k0,
+                                                      kend, tid);
+    load_tile<BN, BK, C::B_LD, C::THREADS, BKM, VEC>(Bs + stage * C::B_STAGE, B, p.ldb, n0, p.n, k0,
+                                                       kend, tid);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) issue(s, s);
+    cp_async_commit();
+  }
+
+  const int r8 = lane >> 2;  // fragment row / column within the 8-wide tile
+  const int k4 = lane & 3;   // fragment k index
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) issue(nk, nk % STAGES);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * C::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * C::B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::FM], bf[C::FN];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i) {
+        const int row = wm * C::TM + i * 8 + r8;
+        af[i] = AK ? as[row * C::A_LD + kk + k4] : as[(kk + k4) * C::A_LD + row];
+      }
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int col = wn * C::TN + j * 8 + r8;
+        bf[j] = BKM ? bs[col * C::B_LD + kk + k4] : bs[(kk + k4) * C::B_LD + col];
+      }
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue.
+  const bool split = p.split > 1;
+  double* Cb = p.c + b1 * p.stride_c + b2 * p.stride_c2;
+  double* W = split ? p.ws + (bidx * p.split + sidx) * p.m * p.n : nullptr;
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int64_t row = m0 + wm * C::TM + i * 8 + r8;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col = n0 + wn * C::TN + j * 8 + 2 * k4 + e;
+        if (col >= p.n) continue;
+        if (p.lower_only && row < col) continue;
+        const double v = acc[i][j][e];
+        if (split) {
+          W[row + col * p.m] = v;
+        } else {
+          double* dst = Cb + row + col * p.ldc;
+          *dst = (p.beta == 0.0) ? p.alpha * v : p.alpha * v + p.beta * (*dst);
+        }
+      }
+    }
+  }
+}
+
+// Deterministic split-K reduction: partials summed in split order 0..S-1.
+__global__ void splitk_reduce(KParams p) {
+  const int64_t total = p.m * p.n;
+  const int64_t bidx = blockIdx.y;
+  const double* W = p.ws + bidx * p.split * total;
+  double* Cb = p.c + (bidx % p.batch) * p.stride_c + (bidx / p.batch) * p.stride_c2;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx % p.m, col = idx / p.m;
+    if (p.lower_only && row < col) continue;
+    double s = W[idx];
+    for (int t = 1; t < p.split; ++t) s += W[t * total + idx];
+    double* dst = Cb + row + col * p.ldc;
+    *dst = (p.beta == 0.0) ? p.alpha * s : p.alpha * s + p.beta * (*dst);
+  }
+}
+
+__global__ void mirror_lower(double* c, int64_t n, int64_t ldc, int64_t stride_c, int64_t batch,
+                             int64_t stride_c2) {
+  double* Cb = c + (blockIdx.z % batch) * stride_c + (blockIdx.z / batch) * stride_c2;
+  __shared__ double tile[32][33];
+  const int64_t bi = blockIdx.x, bj = blockIdx.y;  // source tile (bi >= bj) in the lower triangle
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int64_t row = bi * 32 + tx, col = bj * 32 + r;
+    if (row < n && col < n) tile[r][tx] = Cb[row + col * ldc];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int64_t row = bj * 32 + tx, col = bi * 32 + r;  // upper element (row < col)
+    if (row < n && col < n && row < col) Cb[row + col * ldc] = tile[tx][r];
+  }
+}
+
+struct Workspace {
+  std::mutex mu;
+  double* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+};
+Workspace g_ws;
+
+double* workspace(size_t bytes, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lock(g_ws.mu);
+  int dev = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  if (g_ws.bytes < bytes || g_ws.device != dev) {
+    if (g_ws.ptr) {
+      RP_CUDA(cudaStreamSynchronize(stream));
+      RP_CUDA(cudaFree(g_ws.ptr));
+    }
+    g_ws.ptr = nullptr;
+    RP_CUDA(cudaMalloc(&g_ws.ptr, bytes));
+    g_ws.bytes = bytes;
+    g_ws.device = dev;
+  }
+  return g_ws.ptr;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+void launch_cfg(const KParams& kp, cudaStream_t stream) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
+            static_cast<unsigned>(kp.batch * kp.batch2 * kp.split));
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(kp);
+  RP_LAUNCH_CHECK();
+}
+
+template <bool AK, bool BKM, int VEC>
+void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
+  if (tile == 128)
+    launch_cfg<128, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream);
+  else
+    launch_cfg<64, 64, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream);
+}
+
+}  // namespace
+
+int dgemm_last_launches() { return g_last_launches; }
+
+namespace {
+thread_local GemmProfiler* g_prof = nullptr;
+void dgemm_impl(const GemmArgs& g, cudaStream_t stream);
+}  // namespace
+
+void set_gemm_profiler(GemmProfiler* p) { g_prof = p; }
+
+GemmProfiler::~GemmProfiler() {
+  for (auto& r : recs) {
+    cudaEventDestroy(r.start);
+    cudaEventDestroy(r.stop);
+  }
+}
+
+void GemmProfiler::resolve(double* seconds, double* flops, int64_t* calls) {
+  double s = 0.0, f = 0.0;
+  if (!recs.empty()) RP_CUDA(cudaEventSynchronize(recs.back().stop));
+  for (auto& r : recs) {
+    float ms = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+    s += ms * 1e-3;
+    f += r.flops;
+  }
+  *seconds = s;
+  *flops = f;
+  *calls = static_cast<int64_t>(recs.size());
+}
+
+void dgemm(const GemmArgs& g, cudaStream_t stream) {
+  if (!g_prof || g.m == 0 || g.n == 0) {
+    dgemm_impl(g, stream);
+    return;
+  }
+  GemmProfiler::Rec r{};
+  RP_CUDA(cudaEventCreate(&r.start));
+  RP_CUDA(cudaEventCreate(&r.stop));
+  const double batch = static_cast<double>(g.batch * g.batch2);
+  const double mn = g.lower_only ? 0.5 * static_cast<double>(g.m) * static_cast<double>(g.n + 1)
+                                 : static_cast<double>(g.m) * static_cast<double>(g.n);
+  r.flops = 2.0 * mn * static_cast<double>(g.k) * batch;
+  RP_CUDA(cudaEventRecord(r.start, stream));
+  dgemm_impl(g, stream);
+  RP_CUDA(cudaEventRecord(r.stop, stream));
+  g_prof->recs.push_back(r);
+}
+
+namespace {
+void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
+  g_last_launches = 0;
+  require(g.m >= 0 && g.n >= 0 && g.k >= 0 && g.batch >= 1 && g.batch2 >= 1, "dgemm: negative dimensions");
+  if (g.m == 0 || g.n == 0) return;
+  const int64_t nb = g.batch * g.batch2;
+  KParams kp{};
+  kp.m = g.m;
+  kp.n = g.n;
+  kp.k = g.k;
+  kp.alpha = g.alpha;
+  kp.beta = g.beta;
+  kp.a = g.a;
+  kp.lda = g.lda;
+  kp.stride_a = g.stride_a;
+  kp.b = g.b;
+  kp.ldb = g.ldb;
+  kp.stride_b = g.stride_b;
+  kp.c = g.c;
+  kp.ldc = g.ldc;
+  kp.stride_c = g.stride_c;
+  kp.batch = g.batch;
+  kp.batch2 = g.batch2;
+  kp.stride_a2 = g.stride_a2;
+  kp.stride_b2 = g.stride_b2;
+  kp.stride_c2 = g.stride_c2;
+  kp.lower_only = g.lower_only;
+
+  const bool ak = g.opa == Op::T;  // A contiguous along k
+  const bool bk = g.opb == Op::N;  // B contiguous along k
+  const bool aligned = (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(g.b) % 16 == 0) && g.lda % 2 == 0 &&
+                       g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
+                       g.stride_b2 % 2 == 0;
+
+  // Split-K depends on (m, k) only, never on n (column determinism).
+  int split = g.split_k;
+  if (split <= 0) {
+    int64_t tiles = ceil_div(g.m, 128) * nb;
+    if (!g.col_stable) tiles *= ceil_div(g.n, 128);
+    const int64_t want = ceil_div(2 * 148, std::max<int64_t>(tiles, 1));
+    const int64_t cap = std::max<int64_t>(1, g.k / 512);
+    split = static_cast<int>(std::min<int64_t>(want, cap));
+    split = std::max(1, std::min(split, 64));
+  }
+  int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
+  if (k_chunk == 0) k_chunk = 16;
+  split = static_cast<int>(std::max<int64_t>(1, ceil_div(g.k, k_chunk)));
+  kp.split = split;
+  kp.k_chunk = k_chunk;
+  if (split > 1)
+    kp.ws = workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, stream);
+
+  const int tile = (g.m >= 128 && g.n >= 128) ? 128 : 64;
+  if (ak && bk) {
+    aligned ? launch_layout<true, true, 2>(kp, tile, stream) : launch_layout<true, true, 1>(kp, tile, stream);
+  } else if (ak && !bk) {
+    aligned ? launch_layout<true, false, 2>(kp, tile, stream) : launch_layout<true, false, 1>(kp, tile, stream);
+  } else if (!ak && bk) {
+    aligned ? launch_layout<false, true, 2>(kp, tile, stream) : launch_layout<false, true, 1>(kp, tile, stream);
+  } else {
+    aligned ? launch_layout<false, false, 2>(kp, tile, stream) : launch_layout<false, false, 1>(kp, tile, stream);
+  }
+  g_last_launches = 1;
+  if (split > 1) {
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(ceil_div(g.m * g.n, 256), 148 * 8)),
+              static_cast<unsigned>(nb));
+    splitk_reduce<<<grid, 256, 0, stream>>>(kp);
+    RP_LAUNCH_CHECK();
+    ++g_last_launches;
+  }
+  if (g.mirror) {
+    require(g.m == g.n, "dgemm: mirror needs a square output");
+    dim3 grid(static_cast<unsigned>(ceil_div(g.m, 32)), static_cast<unsigned>(ceil_div(g.m, 32)),
+              static_cast<unsigned>(nb));
+    mirror_lower<<<grid, dim3(32, 8), 0, stream>>>(g.c, g.m, g.ldc, g.stride_c, g.batch, g.stride_c2);
+    RP_LAUNCH_CHECK();
+    ++g_last_launches;
+  }
+}
+
+}  // namespace
+
+}  // namespace rpb

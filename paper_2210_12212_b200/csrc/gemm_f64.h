@@ -1,0 +1,69 @@
+// FP64 tensor-core GEMM (DMMA via mma.sync.m8n8k4.f64) for sm_100a.
+//
+// tcgen05/UMMA has no f64 kind, so FP64 tensor work on Blackwell is the
+// warp-level DMMA path; this kernel stages operands global->shared with a
+// multi-stage cp.async pipeline and keeps accumulators in registers.
+//
+// C = alpha * op(A) * op(B) + beta * C, column-major, optional strided batch.
+// Every output element is reduced over k in a fixed order that depends only on
+// (K, split) -- never on N -- so a column of C is bit-identical whether it is
+// computed alone or inside a wider batch (the property the reference pins in
+// test_path_solver.cpp "matrix basis equals independent vector runs").
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace rpb {
+
+enum class Op { N, T };
+
+struct GemmArgs {
+  Op opa = Op::N, opb = Op::N;
+  int64_t m = 0, n = 0, k = 0;
+  double alpha = 1.0, beta = 0.0;
+  const double* a = nullptr;
+  int64_t lda = 0, stride_a = 0;
+  const double* b = nullptr;
+  int64_t ldb = 0, stride_b = 0;
+  double* c = nullptr;
+  int64_t ldc = 0, stride_c = 0;
+  int64_t batch = 1;
+  // Optional second batch dimension (batch index = b1 + batch * b2).
+  int64_t batch2 = 1;
+  int64_t stride_a2 = 0, stride_b2 = 0, stride_c2 = 0;
+  // Only the lower triangle (row >= col) of each output tile is meaningful and
+  // tiles strictly above the diagonal are skipped (SYRK: C = A^T A).  The upper
+  // triangle is filled by a mirror pass when `mirror` is set.
+  bool lower_only = false;
+  bool mirror = false;
+  // Deterministic split-K factor; 0 = heuristic.  With col_stable the
+  // heuristic looks at (m, k) only, so column j of C does not depend on n.
+  int split_k = 0;
+  bool col_stable = false;
+};
+
+// Launches on `stream`.  `workspace` (may be null) is used for split-K partials;
+// when null and a split is wanted, an internal cached buffer is used.
+void dgemm(const GemmArgs& g, cudaStream_t stream);
+
+// Number of kernel launches issued by the last dgemm() call on this thread.
+int dgemm_last_launches();
+
+// Optional per-thread GEMM profiler: while installed, every dgemm() call is
+// bracketed by CUDA events on its stream and its algorithmic flops recorded.
+struct GemmProfiler {
+  struct Rec {
+    cudaEvent_t start, stop;
+    double flops;
+  };
+  std::vector<Rec> recs;
+  ~GemmProfiler();
+  // Synchronizes on the last event and returns (seconds, flops, calls).
+  void resolve(double* seconds, double* flops, int64_t* calls);
+};
+void set_gemm_profiler(GemmProfiler* p);
+
+}  // namespace rpb

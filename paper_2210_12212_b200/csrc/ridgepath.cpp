@@ -1,0 +1,1600 @@
+// Host orchestration of the IHS-BIN path on the device, and the C ABI
+// (include/ridgepath_b200.h).
+//
+// Mirrors path_solver.cpp: run_path (:147-190), plan_intervals (:85-108),
+// build_interval_basis_matrix with the tau/2 retry (:110-141), ihs_basis_core
+// (:27-53), compose_horner (:64-74) and the ihs_bin_path / ihs_bin_path_matrix
+// / dual_path wrappers (:289-351); spectrum.cpp's scalar tuning is restated
+// verbatim on the host (same glibc libm), so the plans are bit-identical.
+//
+// Device design (B200): every interval and right-hand side of the path runs
+// its recursion in lockstep -- one Gram product and one batched preconditioner
+// GEMM per generation for the whole path (L*K problems) instead of L*K*(k-1)
+// sequential products.  The Gram operator is either a pass over the data
+// (M^T (M W), two DMMA GEMMs or two sparse products) or, when cheaper, the
+// precomputed Gram matrix G = M^T M (one DMMA SYRK) applied as G W.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "basis.h"
+#include "common.h"
+#include "draws.h"
+#include "factor.h"
+#include "gemm_f64.h"
+#include "mt19937.h"
+#include "operator.h"
+#include "ridgepath_b200.h"
+#include "sketch.h"
+
+namespace rpb {
+
+// ---------------------------------------------------------------------------
+// Scalar tuning, restated from spectrum.cpp (host, bit-identical).
+// ---------------------------------------------------------------------------
+
+struct Rho {
+  double rho1 = 1.0, rho2 = 1.0;
+  int provenance = 3;
+};
+
+void rho_validate(const Rho& r) {  // spectrum.cpp:71-76
+  require(r.rho2 > 0.0, "rho bounds: rho2 must be positive");
+  require(r.rho1 >= r.rho2, "rho bounds: rho1 must be >= rho2");
+  if (r.provenance == 3) require(r.rho1 == 1.0 && r.rho2 == 1.0, "identity rho bounds must be (1,1)");
+}
+
+std::vector<double> log_grid(double lo, double hi, int count) {  // spectrum.cpp:38-53
+  require(count >= 1, "log_grid: count must be >= 1");
+  require(lo > 0.0 && hi >= lo, "log_grid: bad range");
+  std::vector<double> g(static_cast<size_t>(count));
+  if (count == 1) {
+    g[0] = lo;
+    return g;
+  }
+  const double lr = std::log(hi / lo);
+  for (int i = 0; i < count; ++i) g[i] = lo * std::exp(lr * static_cast<double>(i) / (count - 1));
+  g.front() = lo;
+  g.back() = hi;
+  return g;
+}
+
+rp_rate_params tune_interval(double lambda_lo, double lambda_hi, const Rho& rho, std::optional<double> sigma_d,
+                             double eps) {  // spectrum.cpp:171-203
+  require(lambda_lo > 0.0, "tune_interval: lambda_lo must be positive");
+  require(lambda_lo <= lambda_hi, "tune_interval: interval ordering violated");
+  require(eps > 0.0 && eps < 1.0, "tune_interval: eps not in (0,1)");
+  rho_validate(rho);
+  const double shift = sigma_d ? (*sigma_d) * (*sigma_d) : 0.0;
+  require(shift >= 0.0, "tune_interval: sigma_d must be nonnegative");
+  const double lo = lambda_lo + shift;
+  const double hi = lambda_hi + shift;
+  rp_rate_params out{};
+  out.lambda0 = std::sqrt(lo * hi) - shift;
+  out.kappa = rho.rho1 * hi / (rho.rho2 * lo);
+  out.alpha = 2.0 * std::sqrt(lo * hi) / (lo / rho.rho1 + hi / rho.rho2);
+  const double rate = (out.kappa - 1.0) / (out.kappa + 1.0);
+  out.contraction = rate * rate;
+  if (out.contraction <= 0.0) {
+    out.k = 2;
+  } else {
+    const double per_step = -std::log(rate);
+    const double raw = std::ceil(std::log(1.0 / eps) / per_step);
+    out.k = static_cast<int>(std::clamp(raw, 2.0, 64.0));
+  }
+  return out;
+}
+
+int auto_interval_count(double lo, double hi) {  // spectrum.cpp:205-211
+  require(lo > 0.0 && lo < hi, "interval_split: need 0 < lambda_min < lambda_max");
+  return std::max(1, static_cast<int>(std::floor(2.0 * std::log(hi / lo))));
+}
+
+std::vector<std::pair<double, double>> interval_split(double lo, double hi, std::optional<int> num) {
+  require(lo > 0.0 && lo < hi, "interval_split: need 0 < lambda_min < lambda_max");  // spectrum.cpp:213-233
+  const int count = num ? *num : auto_interval_count(lo, hi);
+  require(count >= 1, "interval_split: L must be >= 1");
+  const double log_beta = std::log(hi / lo);
+  std::vector<double> edges(static_cast<size_t>(count) + 1);
+  for (int i = 0; i <= count; ++i) edges[i] = lo * std::exp(log_beta * static_cast<double>(i) / count);
+  edges.front() = lo;
+  edges.back() = hi;
+  std::vector<std::pair<double, double>> out;
+  for (int i = 0; i < count; ++i) out.emplace_back(edges[i], edges[i + 1]);
+  return out;
+}
+
+struct PathCfg {
+  double lambda_min = 0, lambda_max = 0;
+  std::vector<double> lambdas;
+  double epsilon = 1e-6;
+  std::optional<int> num_intervals;
+  void validate() const {  // spectrum.cpp:20-36
+    require(lambda_min > 0.0 && lambda_max > 0.0, "path config: lambda bounds must be positive");
+    require(lambda_min < lambda_max, "path config: lambda_min must be below lambda_max");
+    require(!lambdas.empty(), "path config: empty evaluation grid");
+    require(epsilon > 0.0 && epsilon < 1.0, "path config: epsilon not in (0,1)");
+    double prev = lambda_min;
+    for (double l : lambdas) {
+      require(l >= prev, "path config: grid must be sorted ascending");
+      prev = l;
+    }
+    require(lambdas.front() >= lambda_min && lambdas.back() <= lambda_max,
+            "path config: grid must lie within [lambda_min, lambda_max]");
+    if (num_intervals) require(*num_intervals >= 1, "path config: L must be >= 1");
+  }
+};
+
+struct IntervalPlan {
+  double lo = 0, hi = 0;
+  rp_rate_params params{};
+  std::vector<int64_t> grid;  // indices into cfg.lambdas
+};
+
+std::vector<IntervalPlan> plan_intervals(const PathCfg& cfg, const Rho& rho, std::optional<double> sigma_d) {
+  const auto splits = interval_split(cfg.lambda_min, cfg.lambda_max, cfg.num_intervals);  // path_solver.cpp:85-108
+  std::vector<IntervalPlan> plans;
+  size_t cursor = 0;
+  for (size_t i = 0; i < splits.size(); ++i) {
+    IntervalPlan p;
+    p.lo = splits[i].first;
+    p.hi = splits[i].second;
+    p.params = tune_interval(p.lo, p.hi, rho, sigma_d, cfg.epsilon);
+    const bool last = (i + 1 == splits.size());
+    while (cursor < cfg.lambdas.size() && (last || cfg.lambdas[cursor] <= p.hi)) {
+      p.grid.push_back(static_cast<int64_t>(cursor));
+      ++cursor;
+    }
+    plans.push_back(std::move(p));
+  }
+  return plans;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (the library does not link a specific NCCL; in a
+// PyTorch process the already-loaded libnccl.so.2 is reused).
+// ---------------------------------------------------------------------------
+
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (api.handle) break;
+    }
+    if (api.handle) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
+    }
+  }
+  if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce)
+    throw NcclFailure("NCCL (libnccl.so.2) could not be loaded");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw NcclFailure(std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+}
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+
+struct OperatorStore {
+  bool set = false;
+  bool sparse = false;
+  int shard = 0;  // 0 none, 1 rows, 2 cols
+  int64_t n = 0, d = 0;          // global shape of A
+  int64_t off0 = 0, n_local = 0; // shard offset / extent (rows or cols)
+  // dense
+  const double* a = nullptr;
+  int64_t lda = 0;
+  DBuf<double> owned;
+  // csr (+csc) of the local block
+  DBuf<int64_t> csr_off, csc_off;
+  DBuf<int32_t> csr_col, csc_row;
+  DBuf<double> csr_val, csc_val;
+  int64_t nnz = 0;
+
+  // Primal operator M = A (rows local).
+  OpView primal() const {
+    OpView v;
+    require(set, "no operator set");
+    require(shard != 2, "this operator is column-sharded: use the dual route");
+    v.n_global = n;
+    v.row0 = shard == 1 ? off0 : 0;
+    v.n_loc = shard == 1 ? n_local : n;
+    v.d = d;
+    v.sparse = sparse;
+    if (!sparse) {
+      v.a = a;
+      v.ld = lda;
+      v.trans = false;
+    } else {
+      v.csr_off = csr_off.get();
+      v.csr_col = csr_col.get();
+      v.csr_val = csr_val.get();
+      v.csc_off = csc_off.get();
+      v.csc_row = csc_row.get();
+      v.csc_val = csc_val.get();
+      v.nnz = nnz;
+    }
+    return v;
+  }
+  // Dual operator M = A^T (rows of M = columns of A).
+  OpView dual() const {
+    OpView v;
+    require(set, "no operator set");
+    require(shard != 1, "this operator is row-sharded: use the primal route");
+    v.n_global = d;
+    v.row0 = shard == 2 ? off0 : 0;
+    v.n_loc = shard == 2 ? n_local : d;
+    v.d = n;
+    v.sparse = sparse;
+    if (!sparse) {
+      v.a = a;
+      v.ld = lda;
+      v.trans = true;
+    } else {
+      v.csr_off = csc_off.get();
+      v.csr_col = csc_row.get();
+      v.csr_val = csc_val.get();
+      v.csc_off = csr_off.get();
+      v.csc_row = csr_col.get();
+      v.csc_val = csr_val.get();
+      v.nnz = nnz;
+    }
+    return v;
+  }
+};
+
+}  // namespace rpb
+
+struct rp_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  rpb::OperatorStore op;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int gram_mode = -1;
+  bool profile = false;
+  std::string err;
+};
+
+struct rp_precond {
+  int device = 0;
+  int64_t m = 0, d = 0;
+  bool woodbury = false;
+  double lambda0 = 0;
+  std::shared_ptr<rpb::DBuf<double>> sa;    // m x d
+  std::shared_ptr<rpb::DBuf<double>> gram;  // d x d or m x m
+  std::shared_ptr<rpb::DBuf<double>> inv;  // P (d x d) or (l0 I + SA SA^T)^{-1} (m x m)
+};
+
+namespace rpb {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    RP_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) RP_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void allreduce(rp_ctx* ctx, double* buf, int64_t count) {
+  if (ctx->world <= 1 || count <= 0) return;
+  nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm, ctx->stream),
+             "ncclAllReduce");
+}
+
+// ---- operator products -------------------------------------------------------
+
+// y (n_loc x cols) = M_local x (D x cols)
+void op_apply(rp_ctx* ctx, const OpView& op, const double* x, int64_t cols, double* y) {
+  cudaStream_t s = ctx->stream;
+  if (!op.sparse) {
+    GemmArgs g;
+    g.opa = op.op_m();
+    g.m = op.n_loc;
+    g.n = cols;
+    g.k = op.d;
+    g.a = op.a;
+    g.lda = op.ld;
+    g.b = x;
+    g.ldb = op.d;
+    g.c = y;
+    g.ldc = op.n_loc;
+    g.col_stable = true;
+    dgemm(g, s);
+  } else {
+    DBuf<double> xr(static_cast<size_t>(op.d * cols), s), yr(static_cast<size_t>(op.n_loc * cols), s);
+    transpose(x, op.d, cols, op.d, xr.get(), cols, s);
+    spmm_csr_rm(op.csr_off, op.csr_col, op.csr_val, op.n_loc, cols, xr.get(), yr.get(), s);
+    transpose(yr.get(), cols, op.n_loc, cols, y, op.n_loc, s);
+  }
+}
+
+// x (D x cols) = M_local^T y (n_loc x cols), summed over ranks
+void op_apply_t(rp_ctx* ctx, const OpView& op, const double* y, int64_t cols, double* x, bool reduce = true) {
+  cudaStream_t s = ctx->stream;
+  if (!op.sparse) {
+    GemmArgs g;
+    g.opa = op.op_mt();
+    g.m = op.d;
+    g.n = cols;
+    g.k = op.n_loc;
+    g.a = op.a;
+    g.lda = op.ld;
+    g.b = y;
+    g.ldb = op.n_loc;
+    g.c = x;
+    g.ldc = op.d;
+    g.col_stable = true;
+    dgemm(g, s);
+  } else {
+    DBuf<double> yr(static_cast<size_t>(op.n_loc * cols), s), xr(static_cast<size_t>(op.d * cols), s);
+    transpose(y, op.n_loc, cols, op.n_loc, yr.get(), cols, s);
+    spmm_csr_rm(op.csc_off, op.csc_row, op.csc_val, op.d, cols, yr.get(), xr.get(), s);
+    transpose(xr.get(), cols, op.d, cols, x, op.d, s);
+  }
+  if (reduce) allreduce(ctx, x, op.d * cols);
+}
+
+struct GramOp {
+  rp_ctx* ctx = nullptr;
+  OpView op;
+  bool matrix = false;
+  DBuf<double> G;  // D x D when matrix
+  DBuf<double> tmp;
+
+  // Y (D x cols) = M^T (M W)  (matrix.cpp:168-172) or G W.
+  void apply(const double* W, int64_t cols, double* Y) {
+    cudaStream_t s = ctx->stream;
+    if (cols <= 0) return;
+    if (matrix) {
+      GemmArgs g;
+      g.m = op.d;
+      g.n = cols;
+      g.k = op.d;
+      g.a = G.get();
+      g.lda = op.d;
+      g.b = W;
+      g.ldb = op.d;
+      g.c = Y;
+      g.ldc = op.d;
+      g.col_stable = true;
+      dgemm(g, s);
+      return;
+    }
+    const size_t need = static_cast<size_t>(op.n_loc * cols);
+    if (tmp.size() < need) tmp.alloc(need, s);
+    op_apply(ctx, op, W, cols, tmp.get());
+    op_apply_t(ctx, op, tmp.get(), cols, Y, true);
+  }
+
+  void build_matrix() {
+    cudaStream_t s = ctx->stream;
+    require(!op.sparse, "gram matrix mode needs a dense operator");
+    G.alloc(static_cast<size_t>(op.d * op.d), s);
+    GemmArgs g;  // G = M^T M (lower + mirror)
+    g.opa = op.op_mt();
+    g.opb = op.op_m();
+    g.m = op.d;
+    g.n = op.d;
+    g.k = op.n_loc;
+    g.a = op.a;
+    g.lda = op.ld;
+    g.b = op.a;
+    g.ldb = op.ld;
+    g.c = G.get();
+    g.ldc = op.d;
+    g.lower_only = true;
+    g.mirror = true;
+    dgemm(g, s);
+    allreduce(ctx, G.get(), op.d * op.d);
+    matrix = true;
+  }
+};
+
+// ---- preconditioner ------------------------------------------------------------
+
+// P_l for a batch of shifts.  m >= d: P_l = (SA^T SA + l0 I)^{-1} explicitly;
+// m < d: Woodbury with W_l = (l0 I + SA SA^T)^{-1}: P v = (v - SA^T W_l SA v) / l0.
+// Same operator as preconditioner.cpp:12-65 (projection or shift form).
+struct PrecondBatch {
+  int64_t m = 0, d = 0, L = 0;
+  bool woodbury = false;
+  const double* sa = nullptr;  // m x d
+  std::vector<double> lambda0;
+  DBuf<double> d_lambda0;
+  DBuf<double> inv_owned;
+  const double* inv = nullptr;  // L x (n x n), n = d or m
+  int64_t n() const { return woodbury ? m : d; }
+
+  void build(rp_ctx* ctx, const double* sa_, const double* gram /* n x n, may be null */, int64_t m_, int64_t d_,
+             const std::vector<double>& l0) {
+    cudaStream_t s = ctx->stream;
+    m = m_;
+    d = d_;
+    sa = sa_;
+    woodbury = m < d;
+    L = static_cast<int64_t>(l0.size());
+    lambda0 = l0;
+    for (double v : l0) require(v > 0.0, "preconditioner: shift must be positive");
+    const int64_t nn = n();
+    DBuf<double> gbuf;
+    if (!gram) {
+      gbuf.alloc(static_cast<size_t>(nn * nn), s);
+      GemmArgs g;
+      g.opa = woodbury ? Op::N : Op::T;
+      g.opb = woodbury ? Op::T : Op::N;
+      g.m = nn;
+      g.n = nn;
+      g.k = woodbury ? d : m;
+      g.a = sa;
+      g.lda = m;
+      g.b = sa;
+      g.ldb = m;
+      g.c = gbuf.get();
+      g.ldc = nn;
+      g.lower_only = true;
+      g.mirror = true;
+      dgemm(g, s);
+      gram = gbuf.get();
+    }
+    d_lambda0.alloc(static_cast<size_t>(L), s);
+    RP_CUDA(cudaMemcpyAsync(d_lambda0.get(), lambda0.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+    DBuf<double> h(static_cast<size_t>(L * nn * nn), s);
+    shifted_copies(gram, nn, d_lambda0.get(), L, h.get(), s);
+    inv_owned.alloc(static_cast<size_t>(L * nn * nn), s);
+    inv = inv_owned.get();
+    spd_inverse_batched(h.get(), nn, nn, nn * nn, L, inv_owned.get(), nn, nn * nn, s);
+  }
+
+  // out_l (d x cols) = P_l in_l for l < L; in/out strided by `sin`/`sout`
+  // (sin = 0 broadcasts one input to every interval).
+  void apply(rp_ctx* ctx, const double* in, int64_t sin, int64_t cols, double* out, int64_t sout) const {
+    cudaStream_t s = ctx->stream;
+    if (cols <= 0) return;
+    if (!woodbury) {
+      GemmArgs g;
+      g.m = d;
+      g.n = cols;
+      g.k = d;
+      g.a = inv;
+      g.lda = d;
+      g.stride_a = d * d;
+      g.b = in;
+      g.ldb = d;
+      g.stride_b = sin;
+      g.c = out;
+      g.ldc = d;
+      g.stride_c = sout;
+      g.batch = L;
+      g.col_stable = true;
+      dgemm(g, s);
+      return;
+    }
+    DBuf<double> t1(static_cast<size_t>(L * m * cols), s), t2(static_cast<size_t>(L * m * cols), s);
+    DBuf<double> t3(static_cast<size_t>(L * d * cols), s);
+    GemmArgs g1;  // t1_l = SA in_l
+    g1.m = m;
+    g1.n = cols;
+    g1.k = d;
+    g1.a = sa;
+    g1.lda = m;
+    g1.b = in;
+    g1.ldb = d;
+    g1.stride_b = sin;
+    g1.c = t1.get();
+    g1.ldc = m;
+    g1.stride_c = m * cols;
+    g1.batch = L;
+    g1.col_stable = true;
+    dgemm(g1, s);
+    GemmArgs g2;  // t2_l = W_l t1_l
+    g2.m = m;
+    g2.n = cols;
+    g2.k = m;
+    g2.a = inv;
+    g2.lda = m;
+    g2.stride_a = m * m;
+    g2.b = t1.get();
+    g2.ldb = m;
+    g2.stride_b = m * cols;
+    g2.c = t2.get();
+    g2.ldc = m;
+    g2.stride_c = m * cols;
+    g2.batch = L;
+    g2.col_stable = true;
+    dgemm(g2, s);
+    GemmArgs g3;  // t3_l = SA^T t2_l
+    g3.opa = Op::T;
+    g3.m = d;
+    g3.n = cols;
+    g3.k = m;
+    g3.a = sa;
+    g3.lda = m;
+    g3.b = t2.get();
+    g3.ldb = m;
+    g3.stride_b = m * cols;
+    g3.c = t3.get();
+    g3.ldc = d;
+    g3.stride_c = d * cols;
+    g3.batch = L;
+    g3.col_stable = true;
+    dgemm(g3, s);
+    // out_l = (in_l - t3_l) / l0_l   (in may be broadcast: materialize per l)
+    if (sin == 0) {
+      DBuf<double> inb(static_cast<size_t>(L * d * cols), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(in, d, cols, d, inb.get() + l * d * cols, d, s);
+      DBuf<double> o(static_cast<size_t>(L * d * cols), s);
+      woodbury_tail(d, cols, L, d * cols, inb.get(), t3.get(), d_lambda0.get(), o.get(), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(o.get() + l * d * cols, d, cols, d, out + l * sout, d, s);
+    } else if (sin == d * cols && sout == d * cols) {
+      woodbury_tail(d, cols, L, d * cols, in, t3.get(), d_lambda0.get(), out, s);
+    } else {
+      DBuf<double> o(static_cast<size_t>(L * d * cols), s);
+      DBuf<double> inb(static_cast<size_t>(L * d * cols), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(in + l * sin, d, cols, d, inb.get() + l * d * cols, d, s);
+      woodbury_tail(d, cols, L, d * cols, inb.get(), t3.get(), d_lambda0.get(), o.get(), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(o.get() + l * d * cols, d, cols, d, out + l * sout, d, s);
+    }
+  }
+};
+
+// ---- basis recursion (path_solver.cpp:27-53), batched over intervals x RHS ----
+
+struct BasisRun {
+  BasisDims dims;
+  DBuf<double> gen, tilde;
+  std::vector<double> tau;
+  std::vector<int> k;
+  DBuf<double> d_tau;
+  DBuf<int> d_k;
+  std::vector<int> diverged;  // per interval
+};
+
+void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c, int64_t K,
+               const std::vector<double>& tau, const std::vector<int>& ks, BasisRun& out) {
+  cudaStream_t s = ctx->stream;
+  const int64_t L = P.L;
+  const int64_t dim = P.d;
+  int kmax = 1;
+  for (int kv : ks) {
+    require(kv >= 1, "ihs_basis: k must be >= 1");
+    kmax = std::max(kmax, kv);
+  }
+  for (double t : tau) require(t > 0.0, "ihs_basis: tau must be positive");
+  BasisDims d{dim, L, K, kmax};
+  out.dims = d;
+  out.tau = tau;
+  out.k = ks;
+  const int64_t NB = d.nb();
+  out.gen.alloc(static_cast<size_t>(dim * kmax * NB), s);
+  out.tilde.alloc(static_cast<size_t>(dim * kmax * NB), s);
+  out.d_tau.alloc(static_cast<size_t>(L), s);
+  out.d_k.alloc(static_cast<size_t>(L), s);
+  RP_CUDA(cudaMemcpyAsync(out.d_tau.get(), tau.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(out.d_k.get(), ks.data(), sizeof(int) * L, cudaMemcpyHostToDevice, s));
+  DBuf<int> flags(static_cast<size_t>(L), s);
+  RP_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * L, s));
+  // gen_0 = P c (every interval, every RHS), tilde_0 = gen_0.
+  P.apply(ctx, c, 0, K, out.gen.get(), K * dim);
+  fill(out.tilde.get(), dim * kmax * NB, 0.0, s);
+  copy_cols(out.gen.get(), dim, NB, dim, out.tilde.get(), dim, s);
+  if (kmax > 1) {
+    const int64_t stride_im = dim * kmax * K;
+    DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);
+    DBuf<double> args(static_cast<size_t>(L * stride_im), s), applied(static_cast<size_t>(L * stride_im), s);
+    for (int64_t g = 1; g < kmax; ++g) {
+      gram.apply(out.gen.get(), g * NB, y.get());
+      build_args(d, g, y.get(), out.gen.get(), out.d_tau.get(), args.get(), s);
+      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im);
+      update_gen(d, g, applied.get(), out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+    }
+  }
+  out.diverged.assign(static_cast<size_t>(L), 0);
+  RP_CUDA(cudaMemcpyAsync(out.diverged.data(), flags.get(), sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---- helpers for host/device buffers -------------------------------------------
+
+struct InBuf {
+  const double* ptr = nullptr;
+  DBuf<double> owned;
+  InBuf(const double* p, size_t count, int where, cudaStream_t s) {
+    if (where == RP_DEVICE || count == 0) {
+      ptr = p;
+    } else {
+      owned.alloc(count, s);
+      RP_CUDA(cudaMemcpyAsync(owned.get(), p, count * sizeof(double), cudaMemcpyHostToDevice, s));
+      ptr = owned.get();
+    }
+  }
+};
+
+struct OutBuf {
+  double* dev = nullptr;
+  double* host = nullptr;
+  size_t count = 0;
+  DBuf<double> owned;
+  cudaStream_t s;
+  OutBuf(double* p, size_t n, int where, cudaStream_t st) : count(n), s(st) {
+    if (where == RP_DEVICE) {
+      dev = p;
+    } else {
+      host = p;
+      owned.alloc(n ? n : 1, st);
+      dev = owned.get();
+    }
+  }
+  void finish() {
+    if (host && count) RP_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+};
+
+Rho to_rho(const rp_rho_bounds* r) {
+  require(r != nullptr, "rho bounds: null");
+  Rho o;
+  o.rho1 = r->rho1;
+  o.rho2 = r->rho2;
+  o.provenance = r->provenance;
+  return o;
+}
+
+SketchSpecC to_spec(const rp_sketch_spec* s) {
+  require(s != nullptr, "sketch spec: null");
+  SketchSpecC o;
+  o.kind = s->kind;
+  o.m = s->m;
+  o.n = s->n;
+  o.s = s->s;
+  o.seed = s->seed;
+  return o;
+}
+
+PathCfg to_cfg(const rp_path_config* c) {
+  require(c != nullptr, "path config: null");
+  PathCfg o;
+  o.lambda_min = c->lambda_min;
+  o.lambda_max = c->lambda_max;
+  require(c->num_lambdas >= 0, "path config: negative grid size");
+  if (c->num_lambdas > 0) {
+    require(c->lambdas != nullptr, "path config: null grid");
+    o.lambdas.assign(c->lambdas, c->lambdas + c->num_lambdas);
+  }
+  o.epsilon = c->epsilon;
+  if (c->num_intervals > 0) o.num_intervals = c->num_intervals;
+  return o;
+}
+
+// ---- run_path (path_solver.cpp:147-190) ------------------------------------------
+
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  explicit Events(int n) : ev(static_cast<size_t>(n)) {
+    for (auto& e : ev) RP_CUDA(cudaEventCreate(&e));
+  }
+  ~Events() {
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  double secs(int a, int b) const {
+    float ms = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    return ms * 1e-3;
+  }
+};
+
+void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathCfg& cfg, const SketchSpecC& spec,
+              const Rho& rho, std::optional<double> sigma_d, double* x_out, int where, rp_timings* tm) {
+  cudaStream_t s = ctx->stream;
+  const int64_t launches0 = launch_counter().load();
+  std::unique_ptr<GemmProfiler> prof;
+  if (ctx->profile) {
+    prof = std::make_unique<GemmProfiler>();
+    set_gemm_profiler(prof.get());
+  }
+  struct ProfReset {
+    ~ProfReset() { set_gemm_profiler(nullptr); }
+  } prof_reset;
+  const auto host_t0 = std::chrono::steady_clock::now();
+  cfg.validate();
+  rho_validate(rho);
+  require(K >= 1, "path: empty right-hand side");
+  const OpView op = dual ? ctx->op.dual() : ctx->op.primal();
+  // ihs_bin_path: spec.n == A.rows; dual_path: spec.n == A.cols (path_solver.cpp:294, 333-334)
+  require(spec.n == op.n_global, dual ? "dual_path: spec.n must equal A.cols (the dual operator is A^T)"
+                                      : "ihs_bin_path: spec.n must equal A.rows");
+  const int64_t dim = op.d;
+  const int64_t b_rows = dual ? op.d : op.n_loc;  // dual: b has A.rows = op.d entries per column
+  // Host -> device copy of b (timed as copy).
+  double copy_secs = 0.0;
+  auto tc0 = std::chrono::steady_clock::now();
+  InBuf b(b_in, static_cast<size_t>(b_rows * K), where, s);
+  if (where == RP_HOST) RP_CUDA(cudaStreamSynchronize(s));
+  copy_secs += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count();
+
+  Events ev(6);
+  RP_CUDA(cudaEventRecord(ev.ev[0], s));
+  // 1) Sketch (once), summed over ranks.
+  DBuf<double> sa(static_cast<size_t>(spec.m * dim), s);
+  sketch_apply(spec, op, sa.get(), s);
+  allreduce(ctx, sa.get(), spec.m * dim);
+  RP_CUDA(cudaEventRecord(ev.ev[1], s));
+  // 2) Plans (host, bit-identical to the reference).
+  const auto plans = plan_intervals(cfg, rho, sigma_d);
+  const int64_t L = static_cast<int64_t>(plans.size());
+  // 3) Linear term: c = M^T b (primal) or c = b (dual).
+  DBuf<double> cbuf(static_cast<size_t>(dim * K), s);
+  if (!dual) {
+    op_apply_t(ctx, op, b.ptr, K, cbuf.get(), true);
+  } else {
+    copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
+  }
+  // Gram operator: pass over M, or G = M^T M when cheaper.
+  GramOp gram;
+  gram.ctx = ctx;
+  gram.op = op;
+  int kmax = 2;
+  for (const auto& p : plans) kmax = std::max(kmax, p.params.k);
+  {
+    const double cols_total = static_cast<double>(L * K) * (static_cast<double>(kmax) * (kmax - 1) / 2.0);
+    const double nnz = op.sparse ? static_cast<double>(op.nnz) : static_cast<double>(op.n_loc) * op.d;
+    const double pass = 4.0 * nnz * cols_total;
+    const double matrix = static_cast<double>(op.n_loc) * op.d * op.d + 2.0 * op.d * op.d * cols_total;
+    bool use_matrix = !op.sparse && matrix < pass && static_cast<double>(op.d) * op.d * 8.0 <= 16.0 * (1 << 30);
+    if (ctx->gram_mode == 0) use_matrix = false;
+    if (ctx->gram_mode == 1) {
+      require(!op.sparse, "gram_mode=1 needs a dense operator");
+      use_matrix = true;
+    }
+    if (use_matrix) gram.build_matrix();
+  }
+  // 4) Preconditioners for every interval shift (shared sketch, reshift per
+  //    interval: path_solver.cpp:164-170).
+  PrecondBatch P;
+  std::vector<double> l0s, taus;
+  std::vector<int> ks;
+  for (const auto& p : plans) {
+    l0s.push_back(p.params.lambda0);
+    taus.push_back(p.params.alpha);
+    ks.push_back(p.params.k);
+  }
+  P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
+  RP_CUDA(cudaEventRecord(ev.ev[2], s));
+  // 5) Bases for all intervals at once; diverged intervals retried at tau/2
+  //    (path_solver.cpp:132-140).
+  BasisRun run;
+  run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, run);
+  std::vector<int64_t> retry;
+  for (int64_t l = 0; l < L; ++l)
+    if (run.diverged[l]) retry.push_back(l);
+  BasisRun run2;
+  std::vector<int> retry_slot(static_cast<size_t>(L), -1);
+  if (!retry.empty()) {
+    PrecondBatch P2;
+    std::vector<double> l0r, taur;
+    std::vector<int> kr;
+    for (size_t i = 0; i < retry.size(); ++i) {
+      l0r.push_back(l0s[retry[i]]);
+      taur.push_back(taus[retry[i]] / 2.0);
+      kr.push_back(ks[retry[i]]);
+      retry_slot[retry[i]] = static_cast<int>(i);
+    }
+    P2.build(ctx, sa.get(), nullptr, spec.m, dim, l0r);
+    run_basis(ctx, gram, P2, cbuf.get(), K, taur, kr, run2);
+    for (int v : run2.diverged)
+      if (v) throw SolverFailure("interval basis diverged twice, even at tau/2");
+  }
+  RP_CUDA(cudaEventRecord(ev.ev[3], s));
+  // 6) Compose x(lambda) for every grid point (Horner, path_solver.cpp:64-74).
+  const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
+  DBuf<double> xs(static_cast<size_t>(dim * K * T), s);
+  for (int pass = 0; pass < 2; ++pass) {
+    BasisRun& R = pass == 0 ? run : run2;
+    if (pass == 1 && retry.empty()) break;
+    std::vector<double> lam;
+    std::vector<int> itv;
+    std::vector<int64_t> tidx;
+    for (int64_t l = 0; l < L; ++l) {
+      const bool mine = (pass == 0) ? retry_slot[l] < 0 : retry_slot[l] >= 0;
+      if (!mine) continue;
+      for (int64_t t : plans[l].grid) {
+        lam.push_back(cfg.lambdas[t]);
+        itv.push_back(pass == 0 ? static_cast<int>(l) : retry_slot[l]);
+        tidx.push_back(t);
+      }
+    }
+    if (lam.empty()) continue;
+    const int64_t Tn = static_cast<int64_t>(lam.size());
+    DBuf<double> d_lam(static_cast<size_t>(Tn), s);
+    DBuf<int> d_itv(static_cast<size_t>(Tn), s);
+    RP_CUDA(cudaMemcpyAsync(d_lam.get(), lam.data(), sizeof(double) * Tn, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(d_itv.get(), itv.data(), sizeof(int) * Tn, cudaMemcpyHostToDevice, s));
+    // grid points of one batch are contiguous in t (intervals partition the grid in order)
+    const bool contiguous = tidx.back() - tidx.front() + 1 == Tn;
+    if (contiguous) {
+      compose(R.dims, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam.get(), d_itv.get(), Tn,
+              xs.get() + tidx.front() * dim * K, s);
+    } else {
+      DBuf<double> tmp(static_cast<size_t>(dim * K * Tn), s);
+      compose(R.dims, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam.get(), d_itv.get(), Tn, tmp.get(), s);
+      for (int64_t i = 0; i < Tn; ++i)
+        copy_cols(tmp.get() + i * dim * K, dim, K, dim, xs.get() + tidx[i] * dim * K, dim, s);
+    }
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+  // 7) Dual recovery v = A^T z = M_local z (path_solver.cpp:342).
+  const int64_t out_rows = dual ? op.n_loc : dim;
+  OutBuf xo(x_out, static_cast<size_t>(out_rows * K * T), where, s);
+  if (dual) {
+    op_apply(ctx, op, xs.get(), K * T, xo.dev);
+  } else {
+    RP_CUDA(cudaMemcpyAsync(xo.dev, xs.get(), sizeof(double) * dim * K * T, cudaMemcpyDeviceToDevice, s));
+  }
+  RP_CUDA(cudaEventRecord(ev.ev[4], s));
+  RP_CUDA(cudaEventSynchronize(ev.ev[4]));
+  tc0 = std::chrono::steady_clock::now();
+  xo.finish();
+  copy_secs += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count();
+  if (tm) {
+    std::memset(tm, 0, sizeof(*tm));
+    tm->sketch_seconds = ev.secs(0, 1);
+    tm->factor_seconds = ev.secs(1, 2);
+    tm->basis_seconds = ev.secs(2, 3);
+    tm->eval_seconds = ev.secs(3, 4);
+    tm->setup_seconds = ev.secs(0, 3);
+    tm->total_seconds = ev.secs(0, 4);
+    tm->copy_seconds = copy_secs;
+    tm->retries = static_cast<int32_t>(retry.size());
+    tm->gram_mode = gram.matrix ? 1 : 0;
+    tm->launches = launch_counter().load() - launches0;
+    if (prof) prof->resolve(&tm->gemm_seconds, &tm->gemm_flops, &tm->gemm_calls);
+  }
+  (void)host_t0;
+}
+
+rp_status status_of(rp_ctx* ctx, const std::exception& e, rp_status code) {
+  if (ctx) ctx->err = e.what();
+  return code;
+}
+
+}  // namespace rpb
+
+// ============================================================================
+// C ABI
+// ============================================================================
+
+using namespace rpb;
+
+namespace {
+
+thread_local std::string g_err_noctx;
+
+template <class F>
+rp_status guarded(rp_ctx* ctx, F&& f) {
+  try {
+    std::optional<DeviceGuard> guard;
+    if (ctx) guard.emplace(ctx->device);
+    f();
+    return RP_OK;
+  } catch (const InvalidArgument& e) {
+    if (!ctx) g_err_noctx = e.what();
+    return status_of(ctx, e, RP_EINVAL);
+  } catch (const BasisDiverged& e) {
+    return status_of(ctx, e, RP_EDIVERGED);
+  } catch (const SolverFailure& e) {
+    return status_of(ctx, e, RP_ESOLVER);
+  } catch (const FactorFailure& e) {
+    return status_of(ctx, e, RP_ESVD);
+  } catch (const NcclFailure& e) {
+    if (!ctx) g_err_noctx = e.what();
+    return status_of(ctx, e, RP_ENCCL);
+  } catch (const CudaFailure& e) {
+    if (!ctx) g_err_noctx = e.what();
+    const bool oom = std::string(e.what()).find("allocation") != std::string::npos;
+    return status_of(ctx, e, oom ? RP_ENOMEM : RP_ECUDA);
+  } catch (const std::invalid_argument& e) {
+    return status_of(ctx, e, RP_EINVAL);
+  } catch (const std::exception& e) {
+    if (!ctx) g_err_noctx = e.what();
+    return status_of(ctx, e, RP_ECUDA);
+  }
+}
+
+void copy_out_i64(int64_t* dst, const int32_t* src_dev, int64_t n, int where, cudaStream_t s) {
+  std::vector<int32_t> tmp(static_cast<size_t>(n));
+  RP_CUDA(cudaMemcpyAsync(tmp.data(), src_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> wide(tmp.begin(), tmp.end());
+  if (where == RP_DEVICE)
+    RP_CUDA(cudaMemcpyAsync(dst, wide.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+  else
+    std::memcpy(dst, wide.data(), sizeof(int64_t) * n);
+  RP_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+void copy_out(T* dst, const T* src_dev, int64_t n, int where, cudaStream_t s) {
+  if (n <= 0) return;
+  RP_CUDA(cudaMemcpyAsync(dst, src_dev, sizeof(T) * n, where == RP_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                          : cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+}
+
+void set_csr_impl(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t d, const int64_t* offsets,
+                  const int64_t* cols, const double* vals, int where, int shard) {
+  require(n_local >= 0 && d >= 0 && n_global >= n_local, "csr: negative dimensions");
+  require(d < (int64_t{1} << 31) && n_local < (int64_t{1} << 31), "csr: dimensions exceed int32 indices");
+  cudaStream_t s = ctx->stream;
+  // Bring the arrays to the host for validation and the CSC build.
+  std::vector<int64_t> off(static_cast<size_t>(n_local + 1));
+  if (where == RP_DEVICE) {
+    RP_CUDA(cudaMemcpy(off.data(), offsets, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(off.data(), offsets, sizeof(int64_t) * (n_local + 1));
+  }
+  require(off.front() == 0, "csr: row_offsets must start at 0");
+  const int64_t nnz = off.back();
+  std::vector<int64_t> c64(static_cast<size_t>(nnz));
+  std::vector<double> v(static_cast<size_t>(nnz));
+  if (where == RP_DEVICE) {
+    RP_CUDA(cudaMemcpy(c64.data(), cols, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+    RP_CUDA(cudaMemcpy(v.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(c64.data(), cols, sizeof(int64_t) * nnz);
+    std::memcpy(v.data(), vals, sizeof(double) * nnz);
+  }
+  // CsrMatrix invariants (matrix.cpp:22-50).
+  std::vector<int32_t> c32(static_cast<size_t>(nnz));
+  std::vector<int64_t> ccount(static_cast<size_t>(d) + 1, 0);
+  for (int64_t i = 0; i < n_local; ++i) {
+    require(off[i] <= off[i + 1], "csr: row_offsets must be monotone");
+    for (int64_t p = off[i]; p < off[i + 1]; ++p) {
+      require(c64[p] >= 0 && c64[p] < d, "csr: column index out of range");
+      if (p > off[i]) require(c64[p - 1] < c64[p], "csr: column indices must be strictly increasing within a row");
+      require(std::isfinite(v[p]), "csr: non-finite value");
+      c32[p] = static_cast<int32_t>(c64[p]);
+      ccount[c64[p] + 1]++;
+    }
+  }
+  std::partial_sum(ccount.begin(), ccount.end(), ccount.begin());
+  std::vector<int32_t> crow(static_cast<size_t>(nnz));
+  std::vector<double> cval(static_cast<size_t>(nnz));
+  {
+    std::vector<int64_t> pos(ccount.begin(), ccount.end() - 1);
+    for (int64_t i = 0; i < n_local; ++i)
+      for (int64_t p = off[i]; p < off[i + 1]; ++p) {
+        const int64_t q = pos[c64[p]]++;
+        crow[q] = static_cast<int32_t>(i);
+        cval[q] = v[p];
+      }
+  }
+  OperatorStore& o = ctx->op;
+  o = OperatorStore();
+  o.sparse = true;
+  o.n = shard == 2 ? n_global : n_global;
+  o.d = d;
+  o.shard = shard;
+  o.off0 = row0;
+  o.n_local = n_local;
+  o.nnz = nnz;
+  o.csr_off.alloc(off.size(), s);
+  o.csr_col.alloc(std::max<size_t>(c32.size(), 1), s);
+  o.csr_val.alloc(std::max<size_t>(v.size(), 1), s);
+  o.csc_off.alloc(ccount.size(), s);
+  o.csc_row.alloc(std::max<size_t>(crow.size(), 1), s);
+  o.csc_val.alloc(std::max<size_t>(cval.size(), 1), s);
+  RP_CUDA(cudaMemcpyAsync(o.csr_off.get(), off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(o.csr_col.get(), c32.data(), sizeof(int32_t) * c32.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(o.csr_val.get(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(o.csc_off.get(), ccount.data(), sizeof(int64_t) * ccount.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(o.csc_row.get(), crow.data(), sizeof(int32_t) * crow.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(o.csc_val.get(), cval.data(), sizeof(double) * cval.size(), cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  o.set = true;
+}
+
+void set_dense_impl(rp_ctx* ctx, int64_t n, int64_t d, int shard, int64_t off0, int64_t n_local, const double* a,
+                    int64_t lda, int where) {
+  require(n >= 0 && d >= 0 && n_local >= 0, "dense: negative dimensions");
+  const int64_t rows = shard == 1 ? n_local : n;
+  const int64_t cols = shard == 2 ? n_local : d;
+  require(lda >= std::max<int64_t>(rows, 1), "dense: leading dimension too small");
+  cudaStream_t s = ctx->stream;
+  OperatorStore& o = ctx->op;
+  o = OperatorStore();
+  o.sparse = false;
+  o.n = n;
+  o.d = d;
+  o.shard = shard;
+  o.off0 = off0;
+  o.n_local = n_local;
+  if (where == RP_DEVICE) {
+    o.a = a;
+    o.lda = lda;
+  } else {
+    o.owned.alloc(static_cast<size_t>(std::max<int64_t>(rows * cols, 1)), s);
+    RP_CUDA(cudaMemcpy2DAsync(o.owned.get(), sizeof(double) * rows, a, sizeof(double) * lda, sizeof(double) * rows,
+                              static_cast<size_t>(cols), cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    o.a = o.owned.get();
+    o.lda = std::max<int64_t>(rows, 1);
+  }
+  o.set = true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rp_version(void) { return "ridgepath-b200 0.1 (sm_100a)"; }
+
+int64_t rp_launch_count(void) { return launch_counter().load(); }
+
+rp_status rp_create(rp_ctx** out, int device) {
+  if (!out) return RP_EINVAL;
+  *out = nullptr;
+  rp_ctx* ctx = new rp_ctx();
+  ctx->device = device;
+  const rp_status st = guarded(nullptr, [&] {
+    int count = 0;
+    RP_CUDA(cudaGetDeviceCount(&count));
+    require(device >= 0 && device < count, "rp_create: no such CUDA device");
+    DeviceGuard g(device);
+    RP_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    ctx->stream = ctx->own;
+    mt::init_tables();
+  });
+  if (st != RP_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return RP_OK;
+}
+
+void rp_destroy(rp_ctx* ctx) {
+  if (!ctx) return;
+  {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->op = OperatorStore();
+    if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    cudaSetDevice(prev);
+  }
+  delete ctx;
+}
+
+const char* rp_last_error(const rp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err_noctx.c_str(); }
+
+rp_status rp_set_stream(rp_ctx* ctx, void* stream) {
+  if (!ctx) return RP_EINVAL;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return RP_OK;
+}
+
+rp_status rp_synchronize(rp_ctx* ctx) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] { RP_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const std::string k(key);
+    if (k == "gram_mode") {
+      require(value >= -1 && value <= 1, "gram_mode must be -1, 0 or 1");
+      ctx->gram_mode = static_cast<int>(value);
+    } else if (k == "profile") {
+      ctx->profile = value != 0;
+    } else {
+      throw InvalidArgument("unknown option: " + k);
+    }
+  });
+}
+
+rp_status rp_comm_unique_id(void* id128) {
+  return guarded(nullptr, [&] {
+    require(id128 != nullptr, "unique id: null buffer");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, 128);
+  });
+}
+
+rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(world >= 1 && rank >= 0 && rank < world, "comm: bad rank/world");
+    ctx->rank = rank;
+    ctx->world = world;
+    if (world == 1) return;
+    require(id128 != nullptr, "comm: null unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    nccl_check(nccl().CommInitRank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+  });
+}
+
+rp_status rp_set_dense(rp_ctx* ctx, int64_t n, int64_t d, const double* a, int64_t lda, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] { set_dense_impl(ctx, n, d, 0, 0, n, a, lda, where); });
+}
+
+rp_status rp_set_dense_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t d, const double* a,
+                            int64_t lda, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(row0 >= 0 && row0 + n_local <= n_global, "dense rows: shard out of range");
+    set_dense_impl(ctx, n_global, d, 1, row0, n_local, a, lda, where);
+  });
+}
+
+rp_status rp_set_dense_cols(rp_ctx* ctx, int64_t n, int64_t d_global, int64_t col0, int64_t d_local, const double* a,
+                            int64_t lda, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(col0 >= 0 && col0 + d_local <= d_global, "dense cols: shard out of range");
+    set_dense_impl(ctx, n, d_global, 2, col0, d_local, a, lda, where);
+  });
+}
+
+rp_status rp_set_csr(rp_ctx* ctx, int64_t n, int64_t d, const int64_t* offsets, const int64_t* cols,
+                     const double* vals, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] { set_csr_impl(ctx, n, 0, n, d, offsets, cols, vals, where, 0); });
+}
+
+rp_status rp_set_csr_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t d,
+                          const int64_t* offsets, const int64_t* cols, const double* vals, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(row0 >= 0 && row0 + n_local <= n_global, "csr rows: shard out of range");
+    set_csr_impl(ctx, n_global, row0, n_local, d, offsets, cols, vals, where, 1);
+  });
+}
+
+rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const OpView op = ctx->op.primal();
+    require(ncols >= 0, "apply: dimension mismatch");
+    InBuf in(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
+    OutBuf out(y, static_cast<size_t>(op.n_loc * ncols), where, ctx->stream);
+    if (ncols > 0) op_apply(ctx, op, in.ptr, ncols, out.dev);
+    out.finish();
+  });
+}
+
+rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double* x, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const OpView op = ctx->op.primal();
+    require(ncols >= 0, "apply_transpose: dimension mismatch");
+    InBuf in(y, static_cast<size_t>(op.n_loc * ncols), where, ctx->stream);
+    OutBuf out(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
+    if (ncols > 0) op_apply_t(ctx, op, in.ptr, ncols, out.dev, true);
+    out.finish();
+  });
+}
+
+rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* outp, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const OpView op = ctx->op.primal();
+    require(ncols >= 0, "gram_apply: dimension mismatch");
+    InBuf in(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
+    OutBuf out(outp, static_cast<size_t>(op.d * ncols), where, ctx->stream);
+    GramOp g;
+    g.ctx = ctx;
+    g.op = op;
+    if (ncols > 0) g.apply(in.ptr, ncols, out.dev);
+    out.finish();
+  });
+}
+
+rp_status rp_sketch_apply(rp_ctx* ctx, const rp_sketch_spec* specp, int transpose_op, double* sa, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const SketchSpecC spec = to_spec(specp);
+    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    validate_spec(spec);
+    require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
+    OutBuf out(sa, static_cast<size_t>(spec.m * op.d), where, ctx->stream);
+    sketch_apply(spec, op, out.dev, ctx->stream);
+    allreduce(ctx, out.dev, spec.m * op.d);
+    out.finish();
+  });
+}
+
+rp_status rp_precond_build(rp_ctx* ctx, const double* sa, int64_t m, int64_t d, double lambda0, int where,
+                           rp_precond** outp) {
+  if (!ctx || !outp) return RP_EINVAL;
+  *outp = nullptr;
+  return guarded(ctx, [&] {
+    if (lambda0 <= 0.0) throw InvalidArgument("preconditioner: shift must be positive");
+    require(m >= 1 && d >= 1, "preconditioner: empty sketch");
+    cudaStream_t s = ctx->stream;
+    auto p = std::make_unique<rp_precond>();
+    p->device = ctx->device;
+    p->m = m;
+    p->d = d;
+    p->lambda0 = lambda0;
+    p->woodbury = m < d;
+    p->sa = std::make_shared<DBuf<double>>(static_cast<size_t>(m * d), s);
+    if (where == RP_DEVICE)
+      RP_CUDA(cudaMemcpyAsync(p->sa->get(), sa, sizeof(double) * m * d, cudaMemcpyDeviceToDevice, s));
+    else
+      RP_CUDA(cudaMemcpyAsync(p->sa->get(), sa, sizeof(double) * m * d, cudaMemcpyHostToDevice, s));
+    PrecondBatch P;
+    P.build(ctx, p->sa->get(), nullptr, m, d, {lambda0});
+    p->inv = std::make_shared<DBuf<double>>(std::move(P.inv_owned));
+    RP_CUDA(cudaStreamSynchronize(s));
+    *outp = p.release();
+  });
+}
+
+rp_status rp_precond_reshift(rp_ctx* ctx, const rp_precond* p, double lambda0, rp_precond** outp) {
+  if (!ctx || !p || !outp) return RP_EINVAL;
+  *outp = nullptr;
+  return guarded(ctx, [&] {
+    if (lambda0 <= 0.0) throw InvalidArgument("preconditioner: shift must be positive");
+    auto q = std::make_unique<rp_precond>();
+    q->device = p->device;
+    q->m = p->m;
+    q->d = p->d;
+    q->lambda0 = lambda0;
+    q->woodbury = p->woodbury;
+    q->sa = p->sa;
+    PrecondBatch P;
+    P.build(ctx, q->sa->get(), nullptr, q->m, q->d, {lambda0});
+    q->inv = std::make_shared<DBuf<double>>(std::move(P.inv_owned));
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    *outp = q.release();
+  });
+}
+
+void rp_precond_destroy(rp_precond* p) {
+  if (!p) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  p->inv.reset();
+  p->sa.reset();
+  cudaDeviceSynchronize();
+  cudaSetDevice(prev);
+  delete p;
+}
+
+namespace {
+
+PrecondBatch view_of(rp_ctx* ctx, const rp_precond* p) {
+  PrecondBatch P;
+  P.m = p->m;
+  P.d = p->d;
+  P.L = 1;
+  P.woodbury = p->woodbury;
+  P.sa = p->sa->get();
+  P.inv = p->inv->get();
+  P.lambda0 = {p->lambda0};
+  P.d_lambda0.alloc(1, ctx->stream);
+  RP_CUDA(cudaMemcpyAsync(P.d_lambda0.get(), &p->lambda0, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  return P;
+}
+
+void precond_apply_borrowed(rp_ctx* ctx, const rp_precond* p, const double* in, int64_t cols, double* out) {
+  const PrecondBatch P = view_of(ctx, p);
+  P.apply(ctx, in, p->d * cols, cols, out, p->d * cols);
+}
+
+void basis_core(rp_ctx* ctx, const rp_precond* p, const OpView& op, const double* c_dev, int64_t K, double tau, int k,
+                double* terms_out, int where) {
+  require(op.d == p->d, "ihs_basis: preconditioner dimension mismatch");
+  GramOp gram;
+  gram.ctx = ctx;
+  gram.op = op;
+  if (ctx->gram_mode == 1) gram.build_matrix();
+  const PrecondBatch P = view_of(ctx, p);
+  BasisRun run;
+  run_basis(ctx, gram, P, c_dev, K, {tau}, {k}, run);
+  if (run.diverged[0]) throw BasisDiverged("basis recursion diverged (step too large)");
+  // terms_out block j = tilde[:, j*K : (j+1)*K]  (NB = K for one interval)
+  const int64_t dim = op.d;
+  OutBuf out(terms_out, static_cast<size_t>(dim * K * k), where, ctx->stream);
+  copy_cols(run.tilde.get(), dim, K * k, dim, out.dev, dim, ctx->stream);
+  out.finish();
+}
+
+}  // namespace
+
+rp_status rp_precond_apply(rp_ctx* ctx, const rp_precond* p, const double* v, int64_t ncols, double* outp,
+                           int where) {
+  if (!ctx || !p) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(ncols >= 0, "preconditioner apply: dimension mismatch");
+    InBuf in(v, static_cast<size_t>(p->d * ncols), where, ctx->stream);
+    OutBuf out(outp, static_cast<size_t>(p->d * ncols), where, ctx->stream);
+    if (ncols > 0) precond_apply_borrowed(ctx, p, in.ptr, ncols, out.dev);
+    out.finish();
+  });
+}
+
+rp_status rp_ihs_basis(rp_ctx* ctx, const rp_precond* p, const double* b, int64_t K, double tau, int32_t k,
+                       double* terms_out, int where) {
+  if (!ctx || !p) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(K >= 1, "ihs_basis_matrix: empty right-hand side");
+    require(k >= 1, "ihs_basis: k must be >= 1");
+    require(tau > 0.0, "ihs_basis: tau must be positive");
+    const OpView op = ctx->op.primal();
+    InBuf bb(b, static_cast<size_t>(op.n_loc * K), where, ctx->stream);
+    DBuf<double> c(static_cast<size_t>(op.d * K), ctx->stream);
+    op_apply_t(ctx, op, bb.ptr, K, c.get(), true);
+    basis_core(ctx, p, op, c.get(), K, tau, k, terms_out, where);
+  });
+}
+
+rp_status rp_ihs_basis_core(rp_ctx* ctx, const rp_precond* p, const double* c, int64_t K, double tau, int32_t k,
+                            int transpose_op, double* terms_out, int where) {
+  if (!ctx || !p) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(K >= 1, "ihs_basis_matrix: empty right-hand side");
+    require(k >= 1, "ihs_basis: k must be >= 1");
+    require(tau > 0.0, "ihs_basis: tau must be positive");
+    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    require(op.d == p->d, "ihs_basis: operator/right-hand-side mismatch");
+    InBuf cc(c, static_cast<size_t>(op.d * K), where, ctx->stream);
+    basis_core(ctx, p, op, cc.ptr, K, tau, k, terms_out, where);
+  });
+}
+
+rp_status rp_ihs_compose(rp_ctx* ctx, const double* terms, int64_t dim, int64_t K, int32_t k, double tau, double lambda,
+                         double* x_out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(k >= 1 && dim >= 0 && K >= 1, "ihs_compose: bad basis shape");
+    cudaStream_t s = ctx->stream;
+    InBuf tb(terms, static_cast<size_t>(dim * K * k), where, s);
+    OutBuf out(x_out, static_cast<size_t>(dim * K), where, s);
+    BasisDims d{dim, 1, K, k};
+    DBuf<double> dt(1, s), dl(1, s);
+    DBuf<int> dk(1, s), di(1, s);
+    const int kk = k, zero = 0;
+    RP_CUDA(cudaMemcpyAsync(dt.get(), &tau, sizeof(double), cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(dl.get(), &lambda, sizeof(double), cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(dk.get(), &kk, sizeof(int), cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(di.get(), &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    if (dim > 0) compose(d, tb.ptr, dt.get(), dk.get(), dl.get(), di.get(), 1, out.dev, s);
+    out.finish();
+  });
+}
+
+rp_status rp_ihs_bin_path(rp_ctx* ctx, const double* b, int64_t K, const rp_path_config* cfg,
+                          const rp_sketch_spec* spec, const rp_rho_bounds* rho, const double* sigma_d, double* x_out,
+                          int where, rp_timings* timings) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    std::optional<double> sd;
+    if (sigma_d) sd = *sigma_d;
+    run_path(ctx, false, b, K, to_cfg(cfg), to_spec(spec), to_rho(rho), sd, x_out, where, timings);
+  });
+}
+
+rp_status rp_dual_path(rp_ctx* ctx, const double* b, int64_t K, const rp_path_config* cfg, const rp_sketch_spec* spec,
+                       const rp_rho_bounds* rho, const double* sigma_d, double* x_out, int where,
+                       rp_timings* timings) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    std::optional<double> sd;
+    if (sigma_d) sd = *sigma_d;
+    run_path(ctx, true, b, K, to_cfg(cfg), to_spec(spec), to_rho(rho), sd, x_out, where, timings);
+  });
+}
+
+rp_status rp_log_grid(double lambda_min, double lambda_max, int32_t count, double* out) {
+  return guarded(nullptr, [&] {
+    const auto g = log_grid(lambda_min, lambda_max, count);
+    std::copy(g.begin(), g.end(), out);
+  });
+}
+
+rp_status rp_tune_interval(double lambda_lo, double lambda_hi, const rp_rho_bounds* rho, const double* sigma_d,
+                           double eps, rp_rate_params* out) {
+  return guarded(nullptr, [&] {
+    std::optional<double> sd;
+    if (sigma_d) sd = *sigma_d;
+    *out = tune_interval(lambda_lo, lambda_hi, to_rho(rho), sd, eps);
+  });
+}
+
+int32_t rp_auto_interval_count(double lambda_min, double lambda_max) {
+  int32_t v = -1;
+  guarded(nullptr, [&] { v = auto_interval_count(lambda_min, lambda_max); });
+  return v;
+}
+
+rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_intervals, double* edges_out,
+                            int32_t* count_out) {
+  return guarded(nullptr, [&] {
+    std::optional<int> num;
+    if (num_intervals > 0) num = num_intervals;
+    const auto sp = interval_split(lambda_min, lambda_max, num);
+    *count_out = static_cast<int32_t>(sp.size());
+    if (edges_out)
+      for (size_t i = 0; i < sp.size(); ++i) {
+        edges_out[2 * i] = sp[i].first;
+        edges_out[2 * i + 1] = sp[i].second;
+      }
+  });
+}
+
+rp_status rp_draw_u64(rp_ctx* ctx, uint64_t seed, uint64_t skip, int64_t count, uint64_t* out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(count >= 0, "draw: negative count");
+    DBuf<uint64_t> d(static_cast<size_t>(std::max<int64_t>(count, 1)), ctx->stream);
+    draw_words(seed, skip, count, WordMode::Raw, d.get(), ctx->stream);
+    copy_out(out, d.get(), count, where, ctx->stream);
+  });
+}
+
+rp_status rp_draw_uniform01(rp_ctx* ctx, uint64_t seed, int64_t count, double* out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(count >= 0, "draw: negative count");
+    DBuf<double> d(static_cast<size_t>(std::max<int64_t>(count, 1)), ctx->stream);
+    draw_words(seed, 0, count, WordMode::Uniform01, d.get(), ctx->stream);
+    copy_out(out, d.get(), count, where, ctx->stream);
+  });
+}
+
+rp_status rp_draw_sign(rp_ctx* ctx, uint64_t seed, int64_t count, double* out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(count >= 0, "draw: negative count");
+    DBuf<double> d(static_cast<size_t>(std::max<int64_t>(count, 1)), ctx->stream);
+    draw_words(seed, 0, count, WordMode::Sign, d.get(), ctx->stream);
+    copy_out(out, d.get(), count, where, ctx->stream);
+  });
+}
+
+rp_status rp_draw_uniform_index(rp_ctx* ctx, uint64_t seed, uint64_t bound, int64_t count, uint64_t* out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(count >= 0, "draw: negative count");
+    DBuf<uint64_t> d(static_cast<size_t>(std::max<int64_t>(count, 1)), ctx->stream);
+    draw_uniform_index(seed, bound, count, d.get(), ctx->stream);
+    copy_out(out, d.get(), count, where, ctx->stream);
+  });
+}
+
+rp_status rp_draw_normals(rp_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double scale, double* out,
+                          int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(count >= 0 && first >= 0, "draw: negative count");
+    if (count == 0) return;
+    DBuf<uint64_t> st(312, ctx->stream);
+    DBuf<int64_t> cur(1, ctx->stream);
+    DBuf<double> d(static_cast<size_t>(count), ctx->stream);
+    GaussRows g;
+    g.d_states = st.get();
+    g.d_cursor = cur.get();
+    gauss_rows_init(seed, 1, first, 0, g, ctx->stream);
+    gauss_rows_next(g, count, scale, d.get(), count, ctx->stream);
+    copy_out(out, d.get(), count, where, ctx->stream);
+  });
+}
+
+rp_status rp_gaussian_window(rp_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64_t r0, int64_t rc, int64_t j0,
+                             int64_t jc, double* out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(m >= 1 && n >= 1 && r0 >= 0 && rc >= 0 && j0 >= 0 && jc >= 0 && r0 + rc <= m && j0 + jc <= n,
+            "gaussian window: out of range");
+    if (rc == 0 || jc == 0) return;
+    DBuf<uint64_t> st(static_cast<size_t>(rc) * 312, ctx->stream);
+    DBuf<int64_t> cur(static_cast<size_t>(rc), ctx->stream);
+    DBuf<double> d(static_cast<size_t>(rc * jc), ctx->stream);
+    GaussRows g;
+    g.d_states = st.get();
+    g.d_cursor = cur.get();
+    gauss_rows_init(seed, rc, r0 * n + j0, n, g, ctx->stream);
+    gauss_rows_next(g, jc, 1.0 / std::sqrt(static_cast<double>(m)), d.get(), jc, ctx->stream);
+    copy_out(out, d.get(), rc * jc, where, ctx->stream);
+  });
+}
+
+rp_status rp_count_draws(rp_ctx* ctx, const rp_sketch_spec* specp, int64_t* h_out, double* sign_out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const SketchSpecC spec = to_spec(specp);
+    validate_spec(spec);
+    require(spec.kind == kCountSketch || spec.kind == kSjlt, "count draws: not a CountSketch/SJLT spec");
+    const int blocks = spec.kind == kSjlt ? spec.s : 1;
+    const double entry = spec.kind == kSjlt ? 1.0 / std::sqrt(static_cast<double>(spec.s)) : 1.0;
+    const int64_t total = spec.n * blocks;
+    DBuf<int32_t> h(static_cast<size_t>(total), ctx->stream);
+    DBuf<double> sg(static_cast<size_t>(total), ctx->stream);
+    draw_count(spec.seed, spec.n, spec.m / blocks, blocks, entry, h.get(), sg.get(), ctx->stream);
+    copy_out_i64(h_out, h.get(), total, where, ctx->stream);
+    copy_out(sign_out, sg.get(), total, where, ctx->stream);
+  });
+}
+
+rp_status rp_srht_draws(rp_ctx* ctx, const rp_sketch_spec* specp, double* signs_out, int64_t* rows_out, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const SketchSpecC spec = to_spec(specp);
+    validate_spec(spec);
+    require(spec.kind == kSrht, "srht draws: not an SRHT spec");
+    DBuf<double> sg(static_cast<size_t>(spec.n), ctx->stream);
+    DBuf<int64_t> rows(static_cast<size_t>(spec.m), ctx->stream);
+    draw_srht(spec.seed, spec.n, spec.m, sg.get(), rows.get(), ctx->stream);
+    copy_out(signs_out, sg.get(), spec.n, where, ctx->stream);
+    copy_out(rows_out, rows.get(), spec.m, where, ctx->stream);
+  });
+}
+
+int rp_mt_selfcheck(uint64_t seed, uint64_t offset) {
+  try {
+    mt::init_tables();
+    uint64_t w0[mt::kN], w1[mt::kN];
+    mt::seed_window(seed, w0);
+    mt::host_jump(w0, mt::xpow(offset), w1);
+    std::vector<uint64_t> direct(4);
+    mt::host_outputs(seed, offset, 4, direct.data());
+    uint64_t win[2 * mt::kN];
+    std::memcpy(win, w1, sizeof(w1));
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t y = (win[k] & mt::kUpper) | (win[k + 1] & mt::kLower);
+      win[mt::kN + k] = win[k + mt::kM] ^ (y >> 1) ^ ((y & 1ULL) ? mt::kMatrixA : 0ULL);
+      uint64_t x = win[mt::kN + k];
+      x ^= (x >> 29) & 0x5555555555555555ULL;
+      x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+      x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+      x ^= (x >> 43);
+      if (x != direct[k]) return 1;
+    }
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// Sketch families on the device.
+//
+//   Gaussian     sketch.cpp:83-109   S generated slab by slab from the MT
+//                                    stream (draws.cu) and multiplied on the
+//                                    FP64 tensor cores (gemm_f64.cu).
+//   CountSketch  sketch.cpp:114-136  per output column, rows accumulated in
+//   / SJLT                           ascending order -- the reference's own
+//                                    summation order, so SA is bit-exact.
+//   SRHT         sketch.cpp:25-48,   Walsh-Hadamard butterflies in shared
+//                138-173             memory, stride n_pad/2 first (descending),
+//                                    the reference's order: SA is bit-exact.
+//   Identity     sketch.cpp:229-231  densifying copy.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.h"
+#include "draws.h"
+#include "gemm_f64.h"
+#include "sketch.h"
+
+namespace rpb {
+
+void validate_spec(const SketchSpecC& spec) {
+  require(spec.kind >= 0 && spec.kind <= 4, "unknown sketch kind");
+  require(spec.n >= 1, "sketch: n must be positive");
+  require(spec.m >= 1, "sketch: m must be positive");
+  if (spec.kind == kSjlt) {
+    require(spec.s >= 1, "sjlt: sparsity must be >= 1");
+    require(spec.m % spec.s == 0, "sjlt: sparsity must divide m");
+  }
+  if (spec.kind == kIdentity) require(spec.m == spec.n, "identity sketch: m must equal n");
+}
+
+namespace {
+
+// ---- densify / identity ------------------------------------------------------
+
+__global__ void densify_dense(const double* __restrict__ a, int64_t ld, bool trans, int64_t n, int64_t d,
+                              double* __restrict__ out, int64_t ldo) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n * d;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    out[i + j * ldo] = trans ? a[j + i * ld] : a[i + j * ld];
+  }
+}
+
+__global__ void zero_fill(double* __restrict__ out, int64_t rows, int64_t cols, int64_t ld) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rows * cols;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    out[i + j * ld] = 0.0;
+  }
+}
+
+__global__ void densify_csr(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, int64_t n, double* __restrict__ out, int64_t ldo) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (int64_t p = off[r]; p < off[r + 1]; ++p) out[r + static_cast<int64_t>(col[p]) * ldo] = val[p];
+}
+
+unsigned grid_for(int64_t work, int threads = 256) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), 148 * 16)));
+}
+
+// ---- CountSketch / SJLT -------------------------------------------------------
+
+// One thread per (output column c, block b).  Rows are visited in ascending
+// order, so every SA entry receives its terms in the reference's order
+// (sketch.cpp:125-134); the product sgn * value is rounded before the add,
+// exactly as `out(...) += sgn * value`.
+__global__ void count_dense(const double* __restrict__ a, int64_t ld, bool trans, int64_t n_loc, int64_t row0,
+                            int64_t n_glob, int64_t d, int blocks, int64_t rpb, const int32_t* __restrict__ h,
+                            const double* __restrict__ sgn, double* __restrict__ sa, int64_t m) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= d * blocks) return;
+  const int64_t c = t % d;
+  const int b = static_cast<int>(t / d);
+  double* col = sa + c * m + static_cast<int64_t>(b) * rpb;
+  const int32_t* hb = h + static_cast<int64_t>(b) * n_glob + row0;
+  const double* sb = sgn + static_cast<int64_t>(b) * n_glob + row0;
+  for (int64_t j = 0; j < n_loc; ++j) {
+    const double v = trans ? a[c + j * ld] : a[j + c * ld];
+    double* dst = col + hb[j];
+    *dst = __dadd_rn(*dst, __dmul_rn(sb[j], v));
+  }
+}
+
+__global__ void count_csc(const int64_t* __restrict__ coff, const int32_t* __restrict__ crow,
+                          const double* __restrict__ cval, int64_t row0, int64_t n_glob, int64_t d, int blocks,
+                          int64_t rpb, const int32_t* __restrict__ h, const double* __restrict__ sgn,
+                          double* __restrict__ sa, int64_t m) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= d * blocks) return;
+  const int64_t c = t % d;
+  const int b = static_cast<int>(t / d);
+  double* col = sa + c * m + static_cast<int64_t>(b) * rpb;
+  const int32_t* hb = h + static_cast<int64_t>(b) * n_glob + row0;
+  const double* sb = sgn + static_cast<int64_t>(b) * n_glob + row0;
+  for (int64_t p = coff[c]; p < coff[c + 1]; ++p) {
+    const int32_t j = crow[p];
+    double* dst = col + hb[j];
+    *dst = __dadd_rn(*dst, __dmul_rn(sb[j], cval[p]));
+  }
+}
+
+// ---- SRHT ------------------------------------------------------------------------
+
+// x[i, c] = sign[row0 + i] * M(i, c) at global position row0 + i; zero elsewhere.
+__global__ void srht_load_dense(const double* __restrict__ a, int64_t ld, bool trans, int64_t n_loc, int64_t row0,
+                                int64_t d, const double* __restrict__ signs, double* __restrict__ x, int64_t npad) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < npad * d;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % npad, c = idx / npad;
+    const int64_t li = i - row0;
+    double v = 0.0;
+    if (li >= 0 && li < n_loc) v = signs[i] * (trans ? a[c + li * ld] : a[li + c * ld]);
+    x[idx] = v;
+  }
+}
+
+__global__ void srht_scatter_csc(const int64_t* __restrict__ coff, const int32_t* __restrict__ crow,
+                                 const double* __restrict__ cval, int64_t row0, int64_t d,
+                                 const double* __restrict__ signs, double* __restrict__ x, int64_t npad) {
+  const int64_t c = blockIdx.x;
+  if (c >= d) return;
+  for (int64_t p = coff[c] + threadIdx.x; p < coff[c + 1]; p += blockDim.x) {
+    const int64_t i = row0 + crow[p];
+    x[i + c * npad] = signs[i] * cval[p];
+  }
+}
+
+// One pass of butterflies over index bits [lo, lo + B): for every column and
+// every fixed value of the other bits, an S = 2^B point transform with the
+// largest stride first (the reference's descending recursion).
+template <int B>
+__global__ void __launch_bounds__(256) fwht_pass(double* __restrict__ x, int64_t npad, int lo, int W) {
+  constexpr int S = 1 << B;
+  extern __shared__ double tile[];  // [S][W]
+  const int64_t groups_per_col = npad / (static_cast<int64_t>(S) * W);
+  const int64_t c = blockIdx.x / groups_per_col;
+  const int64_t gidx = blockIdx.x % groups_per_col;
+  const int64_t low_span = int64_t{1} << lo;
+  const int64_t wblocks = low_span / W;  // groups of W consecutive low values
+  const int64_t hi_part = gidx / wblocks;
+  const int64_t l0 = (gidx % wblocks) * W;
+  double* col = x + c * npad;
+  const int64_t base = hi_part * (static_cast<int64_t>(S) << lo) + l0;
+  const int total = S * W;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int t = e / W, l = e % W;
+    tile[e] = col[base + (static_cast<int64_t>(t) << lo) + l];
+  }
+  __syncthreads();
+  for (int h = S / 2; h >= 1; h >>= 1) {
+    for (int e = threadIdx.x; e < total / 2; e += blockDim.x) {
+      const int pair = e / W, l = e % W;
+      const int t = (pair / h) * 2 * h + (pair % h);
+      double* pa = tile + t * W + l;
+      double* pb = tile + (t + h) * W + l;
+      const double a = *pa, b = *pb;
+      *pa = a + b;
+      *pb = a - b;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int t = e / W, l = e % W;
+    col[base + (static_cast<int64_t>(t) << lo) + l] = tile[e];
+  }
+}
+
+__global__ void srht_gather(const double* __restrict__ x, int64_t npad, const int64_t* __restrict__ rows, int64_t m,
+                            int64_t d, double scale, double* __restrict__ sa) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < m * d;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx % m, c = idx / m;
+    sa[idx] = x[rows[r] + c * npad] * scale;
+  }
+}
+
+void launch_fwht(double* x, int64_t npad, int64_t d, int lo, int bits, cudaStream_t stream) {
+  const int S = 1 << bits;
+  const int W = static_cast<int>(std::min<int64_t>(int64_t{1} << lo, std::max(1, 4096 / S)));
+  const int64_t blocks = d * (npad / (static_cast<int64_t>(S) * W));
+  const int smem = S * W * 8;
+  auto go = [&](auto kern) {
+    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(x, npad, lo, W);
+    RP_LAUNCH_CHECK();
+  };
+  switch (bits) {
+    case 1: go(fwht_pass<1>); break;
+    case 2: go(fwht_pass<2>); break;
+    case 3: go(fwht_pass<3>); break;
+    case 4: go(fwht_pass<4>); break;
+    case 5: go(fwht_pass<5>); break;
+    case 6: go(fwht_pass<6>); break;
+    case 7: go(fwht_pass<7>); break;
+    case 8: go(fwht_pass<8>); break;
+    case 9: go(fwht_pass<9>); break;
+    case 10: go(fwht_pass<10>); break;
+    case 11: go(fwht_pass<11>); break;
+    case 12: go(fwht_pass<12>); break;
+    default: throw InvalidArgument("fwht: pass width out of range");
+  }
+}
+
+__global__ void transpose_rm_to_cm(const double* __restrict__ in, int64_t rows, int64_t cols,
+                                   double* __restrict__ out) {
+  // in: rows x cols row-major; out: rows x cols column-major
+  __shared__ double tile[32][33];
+  const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[r + c * rows] = tile[threadIdx.x][i];
+  }
+}
+
+// SA[:, c] += S_slab[:, j] * v over the CSC entries (j in the slab) of column c.
+__global__ void gauss_csc_accum(const int64_t* __restrict__ coff, const int32_t* __restrict__ crow,
+                                const double* __restrict__ cval, int64_t j0, int64_t J,
+                                const double* __restrict__ s_cm, int64_t m, double* __restrict__ sa) {
+  const int64_t c = blockIdx.y;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = sa[r + c * m];
+    for (int64_t p = coff[c]; p < coff[c + 1]; ++p) {
+      const int64_t j = crow[p] - j0;
+      if (j < 0 || j >= J) continue;
+      acc = __dadd_rn(acc, __dmul_rn(s_cm[r + j * m], cval[p]));
+    }
+    sa[r + c * m] = acc;
+  }
+}
+
+}  // namespace
+
+void densify(const OpView& op, double* d_out, int64_t ld_out, cudaStream_t stream) {
+  if (!op.sparse) {
+    densify_dense<<<grid_for(op.n_loc * op.d), 256, 0, stream>>>(op.a, op.ld, op.trans, op.n_loc, op.d, d_out,
+                                                                  ld_out);
+    RP_LAUNCH_CHECK();
+  } else {
+    zero_fill<<<grid_for(op.n_loc * op.d), 256, 0, stream>>>(d_out, op.n_loc, op.d, ld_out);
+    RP_LAUNCH_CHECK();
+    densify_csr<<<grid_for(op.n_loc), 256, 0, stream>>>(op.csr_off, op.csr_col, op.csr_val, op.n_loc, d_out,
+                                                         ld_out);
+    RP_LAUNCH_CHECK();
+  }
+}
+
+void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaStream_t stream) {
+  validate_spec(spec);
+  require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
+  const int64_t m = spec.m, d = op.d;
+  switch (spec.kind) {
+    case kIdentity: {
+      zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
+      RP_LAUNCH_CHECK();
+      densify(op, d_sa + op.row0, m, stream);
+      return;
+    }
+    case kGaussian: {
+      const double scale = 1.0 / std::sqrt(static_cast<double>(m));
+      // S slab budget: 1 GiB of doubles.
+      const int64_t J = std::max<int64_t>(
+          2, std::min<int64_t>(op.n_loc, ((int64_t{1} << 27) / std::max<int64_t>(m, 1)) & ~int64_t{1}));
+      DBuf<uint64_t> states(static_cast<size_t>(m) * 312, stream);
+      DBuf<int64_t> cursor(static_cast<size_t>(m), stream);
+      GaussRows g;
+      g.d_states = states.get();
+      g.d_cursor = cursor.get();
+      gauss_rows_init(spec.seed, m, op.row0, spec.n, g, stream);
+      DBuf<double> slab(static_cast<size_t>(m * J), stream);
+      DBuf<double> slab_cm;
+      if (op.sparse) {
+        slab_cm.alloc(static_cast<size_t>(m * J), stream);
+        zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
+        RP_LAUNCH_CHECK();
+      }
+      for (int64_t j0 = 0; j0 < op.n_loc; j0 += J) {
+        const int64_t Jc = std::min(J, op.n_loc - j0);
+        gauss_rows_next(g, Jc, scale, slab.get(), Jc, stream);
+        if (!op.sparse) {
+          GemmArgs ga;
+          ga.opa = Op::T;  // slab is row-major m x Jc == column-major Jc x m
+          ga.opb = op.trans ? Op::T : Op::N;
+          ga.m = m;
+          ga.n = d;
+          ga.k = Jc;
+          ga.a = slab.get();
+          ga.lda = Jc;
+          ga.b = op.trans ? op.a + j0 * op.ld : op.a + j0;
+          ga.ldb = op.ld;
+          ga.c = d_sa;
+          ga.ldc = m;
+          ga.beta = j0 == 0 ? 0.0 : 1.0;
+          dgemm(ga, stream);
+        } else {
+          dim3 tg(static_cast<unsigned>(ceil_div(Jc, 32)), static_cast<unsigned>(ceil_div(m, 32)));
+          transpose_rm_to_cm<<<tg, dim3(32, 8), 0, stream>>>(slab.get(), m, Jc, slab_cm.get());
+          RP_LAUNCH_CHECK();
+          dim3 ag(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(d));
+          gauss_csc_accum<<<ag, 256, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, j0, Jc, slab_cm.get(), m,
+                                                  d_sa);
+          RP_LAUNCH_CHECK();
+        }
+      }
+      return;
+    }
+    case kCountSketch:
+    case kSjlt: {
+      const int blocks = spec.kind == kSjlt ? spec.s : 1;
+      const double entry = spec.kind == kSjlt ? 1.0 / std::sqrt(static_cast<double>(spec.s)) : 1.0;
+      const int64_t rpb = m / blocks;
+      DBuf<int32_t> h(static_cast<size_t>(spec.n * blocks), stream);
+      DBuf<double> sg(static_cast<size_t>(spec.n * blocks), stream);
+      draw_count(spec.seed, spec.n, rpb, blocks, entry, h.get(), sg.get(), stream);
+      zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
+      RP_LAUNCH_CHECK();
+      const int64_t threads = d * blocks;
+      if (!op.sparse) {
+        count_dense<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
+            op.a, op.ld, op.trans, op.n_loc, op.row0, spec.n, d, blocks, rpb, h.get(), sg.get(), d_sa, m);
+      } else {
+        count_csc<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
+            op.csc_off, op.csc_row, op.csc_val, op.row0, spec.n, d, blocks, rpb, h.get(), sg.get(), d_sa, m);
+      }
+      RP_LAUNCH_CHECK();
+      return;
+    }
+    case kSrht: {
+      int64_t npad = 1;
+      int P = 0;
+      while (npad < spec.n) {
+        npad <<= 1;
+        ++P;
+      }
+      DBuf<double> signs(static_cast<size_t>(spec.n), stream);
+      DBuf<int64_t> rows(static_cast<size_t>(m), stream);
+      draw_srht(spec.seed, spec.n, m, signs.get(), rows.get(), stream);
+      DBuf<double> x(static_cast<size_t>(npad * d), stream);
+      if (!op.sparse) {
+        srht_load_dense<<<grid_for(npad * d), 256, 0, stream>>>(op.a, op.ld, op.trans, op.n_loc, op.row0, d,
+                                                                signs.get(), x.get(), npad);
+        RP_LAUNCH_CHECK();
+      } else {
+        zero_fill<<<grid_for(npad * d), 256, 0, stream>>>(x.get(), npad, d, npad);
+        RP_LAUNCH_CHECK();
+        srht_scatter_csc<<<static_cast<unsigned>(d), 128, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, op.row0,
+                                                                       d, signs.get(), x.get(), npad);
+        RP_LAUNCH_CHECK();
+      }
+      // Passes over descending bit ranges of at most 8 bits each.
+      int hi = P;
+      while (hi > 0) {
+        const int bits = std::min(hi, 8);
+        launch_fwht(x.get(), npad, d, hi - bits, bits, stream);
+        hi -= bits;
+      }
+      const double scale = 1.0 / std::sqrt(static_cast<double>(m));
+      srht_gather<<<grid_for(m * d), 256, 0, stream>>>(x.get(), npad, rows.get(), m, d, scale, d_sa);
+      RP_LAUNCH_CHECK();
+      return;
+    }
+  }
+}
+
+}  // namespace rpb

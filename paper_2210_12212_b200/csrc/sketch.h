@@ -1,0 +1,33 @@
+// Sketch application S * M on the device (sketch.cpp:83-248).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "operator.h"
+
+namespace rpb {
+
+enum SketchKind : int { kGaussian = 0, kCountSketch = 1, kSjlt = 2, kSrht = 3, kIdentity = 4 };
+
+struct SketchSpecC {
+  int kind = kIdentity;
+  int64_t m = 0;
+  int64_t n = 0;
+  int s = 1;
+  uint64_t seed = 0;
+};
+
+// SketchSpec::validate (sketch.cpp:202-212).
+void validate_spec(const SketchSpecC& spec);
+
+// d_sa (m x D, column-major, ld = m) = S[:, local rows] * M_local.  For a
+// single rank this is the reference's sketch_apply; for several ranks the
+// partials sum to it (the caller all-reduces).
+void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaStream_t stream);
+
+// Column-major densification of the local rows of M (n_loc x D).
+void densify(const OpView& op, double* d_out, int64_t ld_out, cudaStream_t stream);
+
+}  // namespace rpb

@@ -1,0 +1,716 @@
+"""Python mirror of the reference's ``ridgepath::`` solver API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/ridgepath/{sketch,spectrum,preconditioner,
+path_solver,matrix}.hpp; every call runs on the GPU through
+``libridgepath_b200.so`` (include/ridgepath_b200.h).  There is no CPU
+fallback: without the library or a CUDA device the calls raise.
+
+Exceptions: std::invalid_argument -> ValueError, BasisDivergedError,
+SolverError (path_solver.hpp:18-27), thin_svd failure -> FactorizationError.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libridgepath_b200.so")
+
+RP_HOST, RP_DEVICE = 0, 1
+SKETCH_KINDS = ("gaussian", "countsketch", "sjlt", "srht", "identity")
+RHO_PROVENANCE = ("gaussian", "sjlt", "srht", "identity", "manual")
+
+
+class BasisDivergedError(RuntimeError):
+    """path_solver.hpp:18-21."""
+
+
+class SolverError(RuntimeError):
+    """path_solver.hpp:23-27."""
+
+
+class FactorizationError(RuntimeError):
+    """Shifted sketched Gram not positive definite (the reference's thin_svd
+    runtime_error slot, matrix.cpp:227-228)."""
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# ctypes binding
+# ---------------------------------------------------------------------------
+
+
+class _SketchSpec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("s", ctypes.c_int32), ("m", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("seed", ctypes.c_uint64)]
+
+
+class _PathConfig(ctypes.Structure):
+    _fields_ = [("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double),
+                ("lambdas", ctypes.POINTER(ctypes.c_double)), ("num_lambdas", ctypes.c_int64),
+                ("epsilon", ctypes.c_double), ("num_intervals", ctypes.c_int32)]
+
+
+class _Rho(ctypes.Structure):
+    _fields_ = [("rho1", ctypes.c_double), ("rho2", ctypes.c_double), ("provenance", ctypes.c_int32)]
+
+
+class _Rate(ctypes.Structure):
+    _fields_ = [("lambda0", ctypes.c_double), ("alpha", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("contraction", ctypes.c_double), ("k", ctypes.c_int32)]
+
+
+class Timings(ctypes.Structure):
+    _fields_ = [("setup_seconds", ctypes.c_double), ("eval_seconds", ctypes.c_double),
+                ("total_seconds", ctypes.c_double), ("sketch_seconds", ctypes.c_double),
+                ("factor_seconds", ctypes.c_double), ("basis_seconds", ctypes.c_double),
+                ("copy_seconds", ctypes.c_double), ("retries", ctypes.c_int32), ("gram_mode", ctypes.c_int32),
+                ("launches", ctypes.c_int64), ("gemm_seconds", ctypes.c_double), ("gemm_flops", ctypes.c_double),
+                ("gemm_calls", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_I32 = ctypes.c_int32
+_INT = ctypes.c_int
+
+# Every symbol declared in include/ridgepath_b200.h with its signature.
+SIGNATURES = {
+    "rp_version": ([], ctypes.c_char_p),
+    "rp_create": ([ctypes.POINTER(_P), _INT], _INT),
+    "rp_destroy": ([_P], None),
+    "rp_last_error": ([_P], ctypes.c_char_p),
+    "rp_set_stream": ([_P, _P], _INT),
+    "rp_synchronize": ([_P], _INT),
+    "rp_set_option": ([_P, ctypes.c_char_p, _I64], _INT),
+    "rp_launch_count": ([], _I64),
+    "rp_comm_unique_id": ([_P], _INT),
+    "rp_comm_init": ([_P, _INT, _INT, _P], _INT),
+    "rp_set_dense": ([_P, _I64, _I64, _P, _I64, _INT], _INT),
+    "rp_set_dense_rows": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _INT], _INT),
+    "rp_set_dense_cols": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _INT], _INT),
+    "rp_set_csr": ([_P, _I64, _I64, _P, _P, _P, _INT], _INT),
+    "rp_set_csr_rows": ([_P, _I64, _I64, _I64, _I64, _P, _P, _P, _INT], _INT),
+    "rp_apply": ([_P, _P, _I64, _P, _INT], _INT),
+    "rp_apply_transpose": ([_P, _P, _I64, _P, _INT], _INT),
+    "rp_gram_apply": ([_P, _P, _I64, _P, _INT], _INT),
+    "rp_sketch_apply": ([_P, ctypes.POINTER(_SketchSpec), _INT, _P, _INT], _INT),
+    "rp_precond_build": ([_P, _P, _I64, _I64, _D, _INT, ctypes.POINTER(_P)], _INT),
+    "rp_precond_reshift": ([_P, _P, _D, ctypes.POINTER(_P)], _INT),
+    "rp_precond_apply": ([_P, _P, _P, _I64, _P, _INT], _INT),
+    "rp_precond_destroy": ([_P], None),
+    "rp_ihs_basis": ([_P, _P, _P, _I64, _D, _I32, _P, _INT], _INT),
+    "rp_ihs_basis_core": ([_P, _P, _P, _I64, _D, _I32, _INT, _P, _INT], _INT),
+    "rp_ihs_compose": ([_P, _P, _I64, _I64, _I32, _D, _D, _P, _INT], _INT),
+    "rp_ihs_bin_path": ([_P, _P, _I64, ctypes.POINTER(_PathConfig), ctypes.POINTER(_SketchSpec),
+                         ctypes.POINTER(_Rho), _P, _P, _INT, ctypes.POINTER(Timings)], _INT),
+    "rp_dual_path": ([_P, _P, _I64, ctypes.POINTER(_PathConfig), ctypes.POINTER(_SketchSpec),
+                      ctypes.POINTER(_Rho), _P, _P, _INT, ctypes.POINTER(Timings)], _INT),
+    "rp_log_grid": ([_D, _D, _I32, _P], _INT),
+    "rp_tune_interval": ([_D, _D, ctypes.POINTER(_Rho), _P, _D, ctypes.POINTER(_Rate)], _INT),
+    "rp_auto_interval_count": ([_D, _D], _I32),
+    "rp_interval_split": ([_D, _D, _I32, _P, ctypes.POINTER(_I32)], _INT),
+    "rp_draw_u64": ([_P, _U64, _U64, _I64, _P, _INT], _INT),
+    "rp_draw_uniform01": ([_P, _U64, _I64, _P, _INT], _INT),
+    "rp_draw_sign": ([_P, _U64, _I64, _P, _INT], _INT),
+    "rp_draw_uniform_index": ([_P, _U64, _U64, _I64, _P, _INT], _INT),
+    "rp_draw_normals": ([_P, _U64, _I64, _I64, _D, _P, _INT], _INT),
+    "rp_gaussian_window": ([_P, _U64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _INT], _INT),
+    "rp_count_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
+    "rp_srht_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
+    "rp_mt_selfcheck": ([_U64, _U64], _INT),
+}
+
+
+def lib():
+    """Loads libridgepath_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build() (make -C paper_2210_12212_b200)")
+    L = ctypes.CDLL(LIB_PATH)
+    for name, (args, res) in SIGNATURES.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+_ERRORS = {1: ValueError, 2: BasisDivergedError, 3: SolverError, 4: FactorizationError, 5: DeviceError,
+           6: DeviceError, 7: MemoryError}
+
+
+def _check(st: int, ctx=None):
+    if st != 0:
+        msg = lib().rp_last_error(ctx).decode() if ctx is not None else lib().rp_last_error(None).decode()
+        raise _ERRORS.get(st, DeviceError)(msg or f"rp status {st}")
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+# ---------------------------------------------------------------------------
+# Value types (sketch.hpp, spectrum.hpp, path_solver.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SketchSpec:
+    """sketch.hpp:17-29."""
+    kind: str = "identity"
+    m: int = 0
+    n: int = 0
+    s: int = 1
+    seed: int = 0
+
+    def c(self) -> _SketchSpec:
+        if self.kind not in SKETCH_KINDS:
+            raise ValueError("unknown sketch kind: " + str(self.kind))
+        return _SketchSpec(SKETCH_KINDS.index(self.kind), int(self.s), int(self.m), int(self.n), int(self.seed))
+
+    def with_m(self, m):
+        return SketchSpec(self.kind, m, self.n, self.s, self.seed)
+
+    def with_seed(self, seed):
+        return SketchSpec(self.kind, self.m, self.n, self.s, seed)
+
+
+@dataclass
+class RhoBounds:
+    """spectrum.hpp:32-40."""
+    rho1: float = 1.0
+    rho2: float = 1.0
+    provenance: str = "identity"
+
+    def c(self) -> _Rho:
+        return _Rho(float(self.rho1), float(self.rho2), RHO_PROVENANCE.index(self.provenance))
+
+    @staticmethod
+    def identity():
+        return RhoBounds(1.0, 1.0, "identity")
+
+    @staticmethod
+    def manual(rho1, rho2):
+        if not rho2 > 0.0:
+            raise ValueError("rho bounds: rho2 must be positive")
+        if not rho1 >= rho2:
+            raise ValueError("rho bounds: rho1 must be >= rho2")
+        return RhoBounds(float(rho1), float(rho2), "manual")
+
+
+@dataclass
+class PathConfig:
+    """spectrum.hpp:14-22 (num_intervals None = auto)."""
+    lambda_min: float = 0.0
+    lambda_max: float = 0.0
+    lambdas: Sequence[float] = field(default_factory=list)
+    epsilon: float = 1e-6
+    num_intervals: Optional[int] = None
+
+    def c(self):
+        arr = np.ascontiguousarray(np.asarray(self.lambdas, dtype=np.float64))
+        cfg = _PathConfig(float(self.lambda_min), float(self.lambda_max),
+                          arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(arr.shape[0]),
+                          float(self.epsilon), int(self.num_intervals) if self.num_intervals is not None else 0)
+        if self.num_intervals is not None and self.num_intervals < 1:
+            raise ValueError("path config: L must be >= 1")
+        return cfg, arr
+
+
+@dataclass
+class RateParams:
+    lambda0: float
+    alpha: float
+    kappa: float
+    contraction: float
+    k: int
+
+
+@dataclass
+class Csr:
+    """CsrMatrix (matrix.hpp:16-50): int64 offsets/columns, float64 values."""
+    rows: int
+    cols: int
+    offsets: np.ndarray
+    indices: np.ndarray
+    values: np.ndarray
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+
+@dataclass
+class SketchedMatrix:
+    product: np.ndarray
+    spec: SketchSpec
+
+
+@dataclass
+class BinomialBasis:
+    """path_solver.hpp:34-44: k blocks of dim x K."""
+    terms: List[np.ndarray]
+    tau: float = 0.0
+    lambda_lo: float = 0.0
+    lambda_hi: float = 0.0
+    flavor: str = "ihs"
+
+    @property
+    def k(self):
+        return len(self.terms)
+
+
+@dataclass
+class PathPoint:
+    lam: float
+    solution: np.ndarray
+    seconds: float = 0.0
+
+
+@dataclass
+class RegPathResult:
+    solver: str
+    points: List[PathPoint]
+    setup_seconds: float = 0.0
+    total_seconds: float = 0.0
+    timings: Optional[dict] = None
+
+
+# ---------------------------------------------------------------------------
+# Scalar tuning (host code of the library; bit-identical to spectrum.cpp)
+# ---------------------------------------------------------------------------
+
+
+def log_grid(lambda_min: float, lambda_max: float, count: int) -> List[float]:
+    out = np.empty(max(int(count), 1), dtype=np.float64)
+    _check(lib().rp_log_grid(lambda_min, lambda_max, int(count), _ptr(out)))
+    return out[:count].tolist()
+
+
+def tune_interval(lambda_lo, lambda_hi, rho: RhoBounds, sigma_d=None, eps=1e-6) -> RateParams:
+    r = _Rate()
+    sd = ctypes.c_double(sigma_d) if sigma_d is not None else None
+    _check(lib().rp_tune_interval(lambda_lo, lambda_hi, ctypes.byref(rho.c()),
+                                  ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, eps, ctypes.byref(r)))
+    return RateParams(r.lambda0, r.alpha, r.kappa, r.contraction, r.k)
+
+
+def auto_interval_count(lambda_min, lambda_max) -> int:
+    v = lib().rp_auto_interval_count(lambda_min, lambda_max)
+    if v < 0:
+        raise ValueError(lib().rp_last_error(None).decode())
+    return v
+
+
+def interval_split(lambda_min, lambda_max, num_intervals=None):
+    cnt = _I32(0)
+    _check(lib().rp_interval_split(lambda_min, lambda_max, int(num_intervals or 0), None, ctypes.byref(cnt)))
+    edges = np.empty(2 * cnt.value, dtype=np.float64)
+    _check(lib().rp_interval_split(lambda_min, lambda_max, int(num_intervals or 0), _ptr(edges), ctypes.byref(cnt)))
+    return [(edges[2 * i], edges[2 * i + 1]) for i in range(cnt.value)]
+
+
+def hadamard_pad(n: int) -> int:
+    """sketch.cpp:190-193."""
+    p = 1
+    while p < max(n, 1):
+        p <<= 1
+    return p
+
+
+# ---------------------------------------------------------------------------
+# Context
+# ---------------------------------------------------------------------------
+
+
+class Context:
+    """One GPU (rp_ctx).  Holds the data operator resident in HBM."""
+
+    def __init__(self, device: int = 0):
+        self._h = _P()
+        _check(lib().rp_create(ctypes.byref(self._h), int(device)))
+        self.device = device
+        self._op_key = None
+        self._keep = None
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().rp_destroy(self._h)
+                self._h = _P()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, st):
+        _check(st, self._h)
+
+    def set_option(self, key: str, value: int):
+        self.check(lib().rp_set_option(self._h, key.encode(), int(value)))
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        self.check(lib().rp_set_stream(self._h, _P(stream_ptr) if stream_ptr else None))
+
+    def synchronize(self):
+        self.check(lib().rp_synchronize(self._h))
+
+    # -- operator ------------------------------------------------------------
+    def set_operator(self, a, force: bool = False):
+        """Dense (numpy, n x d) or Csr; a torch CUDA tensor is used in place
+        (column-major: pass A.T-contiguous storage, i.e. a tensor whose
+        transpose is contiguous)."""
+        key = (id(a), getattr(a, "shape", None))
+        if not force and key == self._op_key:
+            return
+        if isinstance(a, Csr):
+            off = np.ascontiguousarray(a.offsets, dtype=np.int64)
+            idx = np.ascontiguousarray(a.indices, dtype=np.int64)
+            val = np.ascontiguousarray(a.values, dtype=np.float64)
+            self.check(lib().rp_set_csr(self._h, a.rows, a.cols, _ptr(off), _ptr(idx), _ptr(val), RP_HOST))
+            self._keep = None
+        elif _is_torch_cuda(a):
+            n, d = a.shape
+            ld = _torch_colmajor_ld(a)
+            self.check(lib().rp_set_dense(self._h, n, d, _P(a.data_ptr()), ld, RP_DEVICE))
+            self._keep = a
+        else:
+            af = _f64(a)
+            n, d = af.shape
+            self.check(lib().rp_set_dense(self._h, n, d, _ptr(af), max(n, 1), RP_HOST))
+            self._keep = None
+        self._op_key = key
+        self._op = a
+
+    def draws_u64(self, seed, count, skip=0):
+        out = np.empty(max(count, 1), dtype=np.uint64)
+        self.check(lib().rp_draw_u64(self._h, seed, skip, count, _ptr(out), RP_HOST))
+        return out[:count]
+
+
+def _is_torch_cuda(a) -> bool:
+    return type(a).__module__.startswith("torch") and getattr(a, "is_cuda", False)
+
+
+def _torch_colmajor_ld(a) -> int:
+    n, d = a.shape
+    st = a.stride()
+    if st[0] == 1 and (d <= 1 or st[1] >= max(n, 1)):
+        return int(st[1]) if d > 1 else max(n, 1)
+    raise ValueError("device operator must be column-major (A.t() contiguous)")
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(int(os.environ.get("RP_DEVICE", "0")))
+    return _default
+
+
+def _rows(a):
+    return a.rows if isinstance(a, Csr) else a.shape[0]
+
+
+def _cols(a):
+    return a.cols if isinstance(a, Csr) else a.shape[1]
+
+
+# ---------------------------------------------------------------------------
+# matrix.hpp
+# ---------------------------------------------------------------------------
+
+
+def apply(a, x, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    x2 = _f64(np.asarray(x).reshape(np.asarray(x).shape[0], -1))
+    if x2.shape[0] != _cols(a):
+        raise ValueError("apply: dimension mismatch")
+    out = np.empty((_rows(a), x2.shape[1]), order="F")
+    ctx.check(lib().rp_apply(ctx.handle, _ptr(x2), x2.shape[1], _ptr(out), RP_HOST))
+    return out.reshape((_rows(a),) + np.asarray(x).shape[1:])
+
+
+def apply_transpose(a, y, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    y2 = _f64(np.asarray(y).reshape(np.asarray(y).shape[0], -1))
+    if y2.shape[0] != _rows(a):
+        raise ValueError("apply_transpose: dimension mismatch")
+    out = np.empty((_cols(a), y2.shape[1]), order="F")
+    ctx.check(lib().rp_apply_transpose(ctx.handle, _ptr(y2), y2.shape[1], _ptr(out), RP_HOST))
+    return out.reshape((_cols(a),) + np.asarray(y).shape[1:])
+
+
+def gram_apply(a, x, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    x2 = _f64(np.asarray(x).reshape(np.asarray(x).shape[0], -1))
+    if x2.shape[0] != _cols(a):
+        raise ValueError("gram_apply: dimension mismatch")
+    out = np.empty((_cols(a), x2.shape[1]), order="F")
+    ctx.check(lib().rp_gram_apply(ctx.handle, _ptr(x2), x2.shape[1], _ptr(out), RP_HOST))
+    return out.reshape((_cols(a),) + np.asarray(x).shape[1:])
+
+
+# ---------------------------------------------------------------------------
+# sketch.hpp
+# ---------------------------------------------------------------------------
+
+
+def sketch_apply(spec: SketchSpec, a, ctx: Optional[Context] = None, transpose_op: bool = False) -> SketchedMatrix:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    d = _rows(a) if transpose_op else _cols(a)
+    if spec.m < 1:
+        raise ValueError("sketch: m must be positive")
+    out = np.empty((spec.m, d), order="F")
+    cs = spec.c()
+    ctx.check(lib().rp_sketch_apply(ctx.handle, ctypes.byref(cs), int(transpose_op), _ptr(out), RP_HOST))
+    return SketchedMatrix(out, spec)
+
+
+# ---------------------------------------------------------------------------
+# preconditioner.hpp
+# ---------------------------------------------------------------------------
+
+
+class Preconditioner:
+    """(SA^T SA + lambda0 I)^{-1}, preconditioner.hpp:24-34."""
+
+    def __init__(self, handle, ctx: Context, m: int, d: int, lambda0: float):
+        self._h = handle
+        self._ctx = ctx
+        self.m, self.d, self._lambda0 = m, d, lambda0
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().rp_precond_destroy(self._h)
+                self._h = _P()
+        except Exception:
+            pass
+
+    @staticmethod
+    def build(sa, lambda0: float, ctx: Optional[Context] = None) -> "Preconditioner":
+        ctx = ctx or default_context()
+        prod = sa.product if isinstance(sa, SketchedMatrix) else sa
+        p = _f64(prod)
+        h = _P()
+        ctx.check(lib().rp_precond_build(ctx.handle, _ptr(p), p.shape[0], p.shape[1], float(lambda0), RP_HOST,
+                                         ctypes.byref(h)))
+        return Preconditioner(h, ctx, p.shape[0], p.shape[1], float(lambda0))
+
+    def reshift(self, new_lambda0: float) -> "Preconditioner":
+        h = _P()
+        self._ctx.check(lib().rp_precond_reshift(self._ctx.handle, self._h, float(new_lambda0), ctypes.byref(h)))
+        return Preconditioner(h, self._ctx, self.m, self.d, float(new_lambda0))
+
+    def apply(self, v) -> np.ndarray:
+        v = np.asarray(v)
+        v2 = _f64(v.reshape(v.shape[0], -1))
+        if v2.shape[0] != self.d:
+            raise ValueError("preconditioner apply: dimension mismatch")
+        out = np.empty_like(v2, order="F")
+        self._ctx.check(lib().rp_precond_apply(self._ctx.handle, self._h, _ptr(v2), v2.shape[1], _ptr(out), RP_HOST))
+        return out.reshape(v.shape)
+
+    def lambda0(self):
+        return self._lambda0
+
+    def dim(self):
+        return self.d
+
+    def sketch_rows(self):
+        return self.m
+
+
+# ---------------------------------------------------------------------------
+# path_solver.hpp
+# ---------------------------------------------------------------------------
+
+
+def _terms_from(buf: np.ndarray, dim: int, K: int, k: int) -> List[np.ndarray]:
+    flat = buf.reshape(-1, order="F")
+    return [flat[j * dim * K:(j + 1) * dim * K].reshape((dim, K), order="F").copy() for j in range(k)]
+
+
+def ihs_basis(a, b, p: Preconditioner, tau: float, k: int, ctx: Optional[Context] = None) -> BinomialBasis:
+    """path_solver.hpp:89-96 (vector b); ihs_basis_matrix for a matrix b."""
+    ctx = ctx or p._ctx
+    ctx.set_operator(a)
+    b = np.asarray(b)
+    if b.shape[0] != _rows(a):
+        raise ValueError("ihs_basis: dimension mismatch")
+    b2 = _f64(b.reshape(b.shape[0], -1))
+    K = b2.shape[1]
+    dim = _cols(a)
+    out = np.empty(dim * K * max(k, 1))
+    ctx.check(lib().rp_ihs_basis(ctx.handle, p._h, _ptr(b2), K, float(tau), int(k), _ptr(out), RP_HOST))
+    return BinomialBasis(_terms_from(out, dim, K, k), float(tau))
+
+
+ihs_basis_matrix = ihs_basis
+
+
+def ihs_compose(basis: BinomialBasis, lam: float, ctx: Optional[Context] = None) -> np.ndarray:
+    """path_solver.hpp:98-101: tau * sum_j (tau lambda)^j u_j (Horner)."""
+    if basis.flavor != "ihs":
+        raise ValueError("ihs_compose: wrong basis flavor")
+    ctx = ctx or default_context()
+    dim, K = basis.terms[0].shape
+    terms = np.concatenate([np.asfortranarray(t).reshape(-1, order="F") for t in basis.terms])
+    out = np.empty((dim, K), order="F")
+    ctx.check(lib().rp_ihs_compose(ctx.handle, _ptr(terms), dim, K, basis.k, float(basis.tau), float(lam), _ptr(out),
+                                   RP_HOST))
+    return out[:, 0] if K == 1 else out
+
+
+def ihs_compose_matrix(basis: BinomialBasis, lam: float, ctx: Optional[Context] = None) -> np.ndarray:
+    out = ihs_compose(basis, lam, ctx)
+    return out.reshape(basis.terms[0].shape)
+
+
+def _run_path(dual: bool, a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
+              ctx: Optional[Context] = None, return_timings=False) -> RegPathResult:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    b = np.asarray(b)
+    if b.shape[0] != _rows(a):
+        raise ValueError(("dual_path" if dual else "ihs_bin_path") + ": dimension mismatch")
+    b2 = _f64(b.reshape(b.shape[0], -1))
+    K = b2.shape[1]
+    T = len(config.lambdas)
+    dim = _cols(a)
+    out = np.empty(dim * K * max(T, 1))
+    cfg, keep = config.c()
+    cs, cr = spec.c(), rho.c()
+    sd = ctypes.c_double(sigma_d) if sigma_d is not None else None
+    tm = Timings()
+    fn = lib().rp_dual_path if dual else lib().rp_ihs_bin_path
+    ctx.check(fn(ctx.handle, _ptr(b2), K, ctypes.byref(cfg), ctypes.byref(cs), ctypes.byref(cr),
+                 ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, _ptr(out), RP_HOST,
+                 ctypes.byref(tm)))
+    del keep
+    pts = []
+    for t in range(T):
+        x = out[t * dim * K:(t + 1) * dim * K].reshape((dim, K), order="F").copy()
+        pts.append(PathPoint(float(config.lambdas[t]), x))
+    return RegPathResult("dual" if dual else "ihs-bin", pts, tm.setup_seconds, tm.total_seconds, tm.as_dict())
+
+
+def ihs_bin_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
+                 ctx: Optional[Context] = None) -> RegPathResult:
+    """path_solver.hpp:109-114 (vector b) / 116-121 (matrix b)."""
+    if spec.n != _rows(a):
+        raise ValueError("ihs_bin_path: spec.n must equal A.rows")
+    return _run_path(False, a, b, config, spec, rho, sigma_d, ctx)
+
+
+ihs_bin_path_matrix = ihs_bin_path
+
+
+def dual_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
+              ctx: Optional[Context] = None) -> RegPathResult:
+    """path_solver.hpp:134-139; a matrix b runs K independent dual paths."""
+    if spec.n != _cols(a):
+        raise ValueError("dual_path: spec.n must equal A.cols (the dual operator is A^T)")
+    return _run_path(True, a, b, config, spec, rho, sigma_d, ctx)
+
+
+# ---------------------------------------------------------------------------
+# Draw contract (device RNG)
+# ---------------------------------------------------------------------------
+
+
+def draw_u64(seed, count, skip=0, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(count, 1), dtype=np.uint64)
+    ctx.check(lib().rp_draw_u64(ctx.handle, seed, skip, count, _ptr(out), RP_HOST))
+    return out[:count]
+
+
+def draw_uniform01(seed, count, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(count, 1))
+    ctx.check(lib().rp_draw_uniform01(ctx.handle, seed, count, _ptr(out), RP_HOST))
+    return out[:count]
+
+
+def draw_sign(seed, count, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(count, 1))
+    ctx.check(lib().rp_draw_sign(ctx.handle, seed, count, _ptr(out), RP_HOST))
+    return out[:count]
+
+
+def draw_uniform_index(seed, bound, count, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(count, 1), dtype=np.uint64)
+    ctx.check(lib().rp_draw_uniform_index(ctx.handle, seed, bound, count, _ptr(out), RP_HOST))
+    return out[:count]
+
+
+def draw_normals(seed, count, first=0, scale=1.0, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(count, 1))
+    ctx.check(lib().rp_draw_normals(ctx.handle, seed, first, count, scale, _ptr(out), RP_HOST))
+    return out[:count]
+
+
+def gaussian_window(seed, m, n, r0, rc, j0, jc, ctx=None):
+    ctx = ctx or default_context()
+    out = np.empty(max(rc * jc, 1))
+    ctx.check(lib().rp_gaussian_window(ctx.handle, seed, m, n, r0, rc, j0, jc, _ptr(out), RP_HOST))
+    return out[:rc * jc].reshape(rc, jc)
+
+
+def count_draws(spec: SketchSpec, ctx=None):
+    ctx = ctx or default_context()
+    blocks = spec.s if spec.kind == "sjlt" else 1
+    h = np.empty(blocks * spec.n, dtype=np.int64)
+    sg = np.empty(blocks * spec.n)
+    cs = spec.c()
+    ctx.check(lib().rp_count_draws(ctx.handle, ctypes.byref(cs), _ptr(h), _ptr(sg), RP_HOST))
+    return h.reshape(blocks, spec.n), sg.reshape(blocks, spec.n)
+
+
+def srht_draws(spec: SketchSpec, ctx=None):
+    ctx = ctx or default_context()
+    signs = np.empty(spec.n)
+    rows = np.empty(spec.m, dtype=np.int64)
+    cs = spec.c()
+    ctx.check(lib().rp_srht_draws(ctx.handle, ctypes.byref(cs), _ptr(signs), _ptr(rows), RP_HOST))
+    return signs, rows
+
+
+def launch_count() -> int:
+    return int(lib().rp_launch_count())
