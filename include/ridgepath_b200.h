@@ -120,6 +120,10 @@ typedef struct {
   double gemm_seconds;    /* summed GEMM kernel time */
   double gemm_flops;      /* algorithmic flops of those GEMMs */
   int64_t gemm_calls;
+  /* factor_seconds split: c = M^T b, Gram matrix G = M^T M, preconditioners */
+  double linear_seconds;
+  double gram_seconds;
+  double precond_seconds;
 } rp_timings;
 
 /* ---- context -------------------------------------------------------------- */

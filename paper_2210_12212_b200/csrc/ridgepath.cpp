@@ -744,7 +744,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   if (where == RP_HOST) RP_CUDA(cudaStreamSynchronize(s));
   copy_secs += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count();
 
-  Events ev(6);
+  Events ev(8);
   RP_CUDA(cudaEventRecord(ev.ev[0], s));
   // 1) Sketch (once), summed over ranks.
   DBuf<double> sa(static_cast<size_t>(spec.m * dim), s);
@@ -761,6 +761,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   } else {
     copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
   }
+  RP_CUDA(cudaEventRecord(ev.ev[5], s));
   // Gram operator: pass over M, or G = M^T M when cheaper.
   GramOp gram;
   gram.ctx = ctx;
@@ -780,58 +781,83 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     }
     if (use_matrix) gram.build_matrix();
   }
-  // 4) Preconditioners for every interval shift (shared sketch, reshift per
-  //    interval: path_solver.cpp:164-170).
+  RP_CUDA(cudaEventRecord(ev.ev[6], s));
+  // 4) Interval ownership.  With the Gram matrix every rank holds the whole
+  //    operator state (SA, c, G are all-reduced), so the intervals -- which are
+  //    independent (path_solver.cpp:168-186) -- are split round-robin and the
+  //    composed x(lambda) summed.  In pass mode every generation needs every
+  //    rank's rows, so all ranks run all intervals.
+  const bool split = ctx->world > 1 && gram.matrix;
+  std::vector<int64_t> own;
+  for (int64_t l = 0; l < L; ++l)
+    if (!split || l % ctx->world == ctx->rank) own.push_back(l);
+  const int64_t Lo = static_cast<int64_t>(own.size());
+  // Preconditioners for the owned shifts (shared sketch, one reshift per
+  // interval: path_solver.cpp:164-170).
   PrecondBatch P;
   std::vector<double> l0s, taus;
   std::vector<int> ks;
-  for (const auto& p : plans) {
-    l0s.push_back(p.params.lambda0);
-    taus.push_back(p.params.alpha);
-    ks.push_back(p.params.k);
+  for (int64_t l : own) {
+    l0s.push_back(plans[l].params.lambda0);
+    taus.push_back(plans[l].params.alpha);
+    ks.push_back(plans[l].params.k);
   }
-  P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
+  if (Lo > 0) P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
   RP_CUDA(cudaEventRecord(ev.ev[2], s));
-  // 5) Bases for all intervals at once; diverged intervals retried at tau/2
-  //    (path_solver.cpp:132-140).
-  BasisRun run;
-  run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, run);
-  std::vector<int64_t> retry;
-  for (int64_t l = 0; l < L; ++l)
-    if (run.diverged[l]) retry.push_back(l);
-  BasisRun run2;
-  std::vector<int> retry_slot(static_cast<size_t>(L), -1);
-  if (!retry.empty()) {
-    PrecondBatch P2;
-    std::vector<double> l0r, taur;
-    std::vector<int> kr;
-    for (size_t i = 0; i < retry.size(); ++i) {
-      l0r.push_back(l0s[retry[i]]);
-      taur.push_back(taus[retry[i]] / 2.0);
-      kr.push_back(ks[retry[i]]);
-      retry_slot[retry[i]] = static_cast<int>(i);
+  // 5) Bases for all owned intervals at once; diverged intervals are retried
+  //    at tau/2 (path_solver.cpp:132-140).
+  BasisRun run, run2;
+  std::vector<int64_t> retry;             // positions in `own`
+  std::vector<int> retry_slot(static_cast<size_t>(Lo), -1);
+  int failed = 0;
+  if (Lo > 0) {
+    run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, run);
+    for (int64_t i = 0; i < Lo; ++i)
+      if (run.diverged[i]) retry.push_back(i);
+    if (!retry.empty()) {
+      PrecondBatch P2;
+      std::vector<double> l0r, taur;
+      std::vector<int> kr;
+      for (size_t j = 0; j < retry.size(); ++j) {
+        l0r.push_back(l0s[retry[j]]);
+        taur.push_back(taus[retry[j]] / 2.0);
+        kr.push_back(ks[retry[j]]);
+        retry_slot[retry[j]] = static_cast<int>(j);
+      }
+      P2.build(ctx, sa.get(), nullptr, spec.m, dim, l0r);
+      run_basis(ctx, gram, P2, cbuf.get(), K, taur, kr, run2);
+      for (int v : run2.diverged) failed |= v;
     }
-    P2.build(ctx, sa.get(), nullptr, spec.m, dim, l0r);
-    run_basis(ctx, gram, P2, cbuf.get(), K, taur, kr, run2);
-    for (int v : run2.diverged)
-      if (v) throw SolverFailure("interval basis diverged twice, even at tau/2");
   }
+  if (ctx->world > 1) {  // every rank must agree before anyone throws
+    DBuf<double> f(1, s);
+    const double fv = failed;
+    RP_CUDA(cudaMemcpyAsync(f.get(), &fv, sizeof(double), cudaMemcpyHostToDevice, s));
+    allreduce(ctx, f.get(), 1);
+    double tot = 0;
+    RP_CUDA(cudaMemcpyAsync(&tot, f.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    failed = tot > 0.0;
+  }
+  if (failed) throw SolverFailure("interval basis diverged twice, even at tau/2");
   RP_CUDA(cudaEventRecord(ev.ev[3], s));
-  // 6) Compose x(lambda) for every grid point (Horner, path_solver.cpp:64-74).
+  // 6) Compose x(lambda) for every owned grid point (Horner,
+  //    path_solver.cpp:64-74).
   const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
   DBuf<double> xs(static_cast<size_t>(dim * K * T), s);
+  if (split) fill(xs.get(), dim * K * T, 0.0, s);
   for (int pass = 0; pass < 2; ++pass) {
     BasisRun& R = pass == 0 ? run : run2;
     if (pass == 1 && retry.empty()) break;
     std::vector<double> lam;
     std::vector<int> itv;
     std::vector<int64_t> tidx;
-    for (int64_t l = 0; l < L; ++l) {
-      const bool mine = (pass == 0) ? retry_slot[l] < 0 : retry_slot[l] >= 0;
+    for (int64_t i = 0; i < Lo; ++i) {
+      const bool mine = (pass == 0) ? retry_slot[i] < 0 : retry_slot[i] >= 0;
       if (!mine) continue;
-      for (int64_t t : plans[l].grid) {
+      for (int64_t t : plans[own[i]].grid) {
         lam.push_back(cfg.lambdas[t]);
-        itv.push_back(pass == 0 ? static_cast<int>(l) : retry_slot[l]);
+        itv.push_back(pass == 0 ? static_cast<int>(i) : retry_slot[i]);
         tidx.push_back(t);
       }
     }
@@ -841,7 +867,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     DBuf<int> d_itv(static_cast<size_t>(Tn), s);
     RP_CUDA(cudaMemcpyAsync(d_lam.get(), lam.data(), sizeof(double) * Tn, cudaMemcpyHostToDevice, s));
     RP_CUDA(cudaMemcpyAsync(d_itv.get(), itv.data(), sizeof(int) * Tn, cudaMemcpyHostToDevice, s));
-    // grid points of one batch are contiguous in t (intervals partition the grid in order)
+    // grid points of one batch are contiguous in t when no interval is skipped
     const bool contiguous = tidx.back() - tidx.front() + 1 == Tn;
     if (contiguous) {
       compose(R.dims, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam.get(), d_itv.get(), Tn,
@@ -854,6 +880,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     }
     RP_CUDA(cudaStreamSynchronize(s));
   }
+  if (split) allreduce(ctx, xs.get(), dim * K * T);  // exact: every entry has one non-zero term
   // 7) Dual recovery v = A^T z = M_local z (path_solver.cpp:342).
   const int64_t out_rows = dual ? op.n_loc : dim;
   OutBuf xo(x_out, static_cast<size_t>(out_rows * K * T), where, s);
@@ -879,6 +906,9 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     tm->retries = static_cast<int32_t>(retry.size());
     tm->gram_mode = gram.matrix ? 1 : 0;
     tm->launches = launch_counter().load() - launches0;
+    tm->linear_seconds = ev.secs(1, 5);
+    tm->gram_seconds = ev.secs(5, 6);
+    tm->precond_seconds = ev.secs(6, 2);
     if (prof) prof->resolve(&tm->gemm_seconds, &tm->gemm_flops, &tm->gemm_calls);
   }
   (void)host_t0;
@@ -1074,6 +1104,12 @@ rp_status rp_create(rp_ctx** out, int device) {
     DeviceGuard g(device);
     RP_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
     ctx->stream = ctx->own;
+    // Keep stream-ordered allocations cached across calls (the default release
+    // threshold of 0 returns every freed block to the driver at each sync).
+    cudaMemPool_t pool;
+    RP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    RP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     mt::init_tables();
   });
   if (st != RP_OK) {
@@ -1572,26 +1608,42 @@ rp_status rp_srht_draws(rp_ctx* ctx, const rp_sketch_spec* specp, double* signs_
 }
 
 int rp_mt_selfcheck(uint64_t seed, uint64_t offset) {
+  // Outputs offset..offset+3 from the jumped window must equal direct
+  // generation; for large offsets "direct" starts from an independent jump to
+  // offset - 1000 followed by 1000 ordinary steps.
   try {
     mt::init_tables();
+    using W = std::vector<uint64_t>;
+    auto step_outputs = [](const W& window, int64_t skip, int count) {
+      W x(window);
+      W out;
+      for (int64_t k = 0; static_cast<int64_t>(out.size()) < count; ++k) {
+        const uint64_t y = (x[k] & mt::kUpper) | (x[k + 1] & mt::kLower);
+        x.push_back(x[k + mt::kM] ^ (y >> 1) ^ ((y & 1ULL) ? mt::kMatrixA : 0ULL));
+        if (k >= skip) {
+          uint64_t v = x.back();
+          v ^= (v >> 29) & 0x5555555555555555ULL;
+          v ^= (v << 17) & 0x71D67FFFEDA60000ULL;
+          v ^= (v << 37) & 0xFFF7EEE000000000ULL;
+          v ^= (v >> 43);
+          out.push_back(v);
+        }
+      }
+      return out;
+    };
     uint64_t w0[mt::kN], w1[mt::kN];
     mt::seed_window(seed, w0);
     mt::host_jump(w0, mt::xpow(offset), w1);
-    std::vector<uint64_t> direct(4);
-    mt::host_outputs(seed, offset, 4, direct.data());
-    uint64_t win[2 * mt::kN];
-    std::memcpy(win, w1, sizeof(w1));
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t y = (win[k] & mt::kUpper) | (win[k + 1] & mt::kLower);
-      win[mt::kN + k] = win[k + mt::kM] ^ (y >> 1) ^ ((y & 1ULL) ? mt::kMatrixA : 0ULL);
-      uint64_t x = win[mt::kN + k];
-      x ^= (x >> 29) & 0x5555555555555555ULL;
-      x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
-      x ^= (x << 37) & 0xFFF7EEE000000000ULL;
-      x ^= (x >> 43);
-      if (x != direct[k]) return 1;
+    const W got = step_outputs(W(w1, w1 + mt::kN), 0, 4);
+    W want(4);
+    if (offset <= (uint64_t{1} << 22)) {
+      mt::host_outputs(seed, offset, 4, want.data());
+    } else {
+      uint64_t w2[mt::kN];
+      mt::host_jump(w0, mt::xpow(offset - 1000), w2);
+      want = step_outputs(W(w2, w2 + mt::kN), 1000, 4);
     }
-    return 0;
+    return got == want ? 0 : 1;
   } catch (...) {
     return 2;
   }

@@ -75,7 +75,8 @@ class Timings(ctypes.Structure):
                 ("factor_seconds", ctypes.c_double), ("basis_seconds", ctypes.c_double),
                 ("copy_seconds", ctypes.c_double), ("retries", ctypes.c_int32), ("gram_mode", ctypes.c_int32),
                 ("launches", ctypes.c_int64), ("gemm_seconds", ctypes.c_double), ("gemm_flops", ctypes.c_double),
-                ("gemm_calls", ctypes.c_int64)]
+                ("gemm_calls", ctypes.c_int64), ("linear_seconds", ctypes.c_double),
+                ("gram_seconds", ctypes.c_double), ("precond_seconds", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -714,3 +715,50 @@ def srht_draws(spec: SketchSpec, ctx=None):
 
 def launch_count() -> int:
     return int(lib().rp_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# Device-resident entry points (operator / b / x already in HBM)
+# ---------------------------------------------------------------------------
+
+
+def set_dense_rows_device(ctx: Context, n_global: int, row0: int, n_local: int, d: int, ptr: int, lda: int):
+    """rp_set_dense_rows with a device pointer (the shard's first row)."""
+    ctx.check(lib().rp_set_dense_rows(ctx.handle, n_global, row0, n_local, d, _P(ptr), lda, RP_DEVICE))
+    ctx._op_key = ("device", ptr, n_global, row0, n_local, d)
+
+
+def set_dense_rows_host(ctx: Context, n_global: int, row0: int, n_local: int, d: int, ptr: int, lda: int):
+    """rp_set_dense_rows from host memory (pinned for full-speed DMA)."""
+    ctx.check(lib().rp_set_dense_rows(ctx.handle, n_global, row0, n_local, d, _P(ptr), lda, RP_HOST))
+    ctx._op_key = ("host", ptr, n_global, row0, n_local, d)
+
+
+def set_dense_cols_device(ctx: Context, n: int, d_global: int, col0: int, d_local: int, ptr: int, lda: int):
+    ctx.check(lib().rp_set_dense_cols(ctx.handle, n, d_global, col0, d_local, _P(ptr), lda, RP_DEVICE))
+    ctx._op_key = ("device-cols", ptr, n, d_global, col0, d_local)
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().rp_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(ctx: Context, rank: int, world: int, uid: bytes):
+    buf = ctypes.create_string_buffer(uid, 128)
+    ctx.check(lib().rp_comm_init(ctx.handle, rank, world, buf))
+
+
+def path_raw(ctx: Context, b_ptr: int, K: int, config: PathConfig, spec: SketchSpec, rho: RhoBounds, x_ptr: int,
+             where: int = RP_DEVICE, dual: bool = False, sigma_d=None) -> Timings:
+    """rp_ihs_bin_path / rp_dual_path on raw pointers (device or host)."""
+    cfg, keep = config.c()
+    cs, cr = spec.c(), rho.c()
+    sd = ctypes.c_double(sigma_d) if sigma_d is not None else None
+    tm = Timings()
+    fn = lib().rp_dual_path if dual else lib().rp_ihs_bin_path
+    ctx.check(fn(ctx.handle, _P(b_ptr), K, ctypes.byref(cfg), ctypes.byref(cs), ctypes.byref(cr),
+                 ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, _P(x_ptr), where, ctypes.byref(tm)))
+    del keep
+    return tm
