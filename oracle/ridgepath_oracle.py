@@ -130,6 +130,7 @@ class Csr:
     offsets: np.ndarray  # int64, rows+1
     indices: np.ndarray  # int64, nnz (strictly increasing per row)
     values: np.ndarray  # float64, nnz
+    _sp: object = None
 
     def __post_init__(self):
         self.offsets = np.ascontiguousarray(self.offsets, dtype=np.int64)
@@ -184,16 +185,20 @@ def _cols(a):
     return a.cols if is_csr(a) else a.shape[1]
 
 
+def _scipy(a):
+    import scipy.sparse as sp
+
+    if getattr(a, "_sp", None) is None:
+        a._sp = sp.csr_matrix((a.values, a.indices, a.offsets), shape=(a.rows, a.cols))
+    return a._sp
+
+
 def apply(a, x: np.ndarray) -> np.ndarray:
-    """matrix.cpp:140-152 / 174-188."""
+    """matrix.cpp:140-152 / 174-188 (CSR: row-wise sums, scipy's CSR kernel)."""
     _require(x.shape[0] == _cols(a), "apply: dimension mismatch")
     if not is_csr(a):
         return a @ x
-    row_of = np.repeat(np.arange(a.rows), np.diff(a.offsets))
-    contrib = a.values[:, None] * x.reshape(x.shape[0], -1)[a.indices]
-    out = np.zeros((a.rows, contrib.shape[1]))
-    np.add.at(out, row_of, contrib)
-    return out.reshape((a.rows,) + x.shape[1:])
+    return np.asarray(_scipy(a) @ x)
 
 
 def apply_transpose(a, y: np.ndarray) -> np.ndarray:
@@ -201,11 +206,7 @@ def apply_transpose(a, y: np.ndarray) -> np.ndarray:
     _require(y.shape[0] == _rows(a), "apply_transpose: dimension mismatch")
     if not is_csr(a):
         return a.T @ y
-    row_of = np.repeat(np.arange(a.rows), np.diff(a.offsets))
-    contrib = a.values[:, None] * y.reshape(y.shape[0], -1)[row_of]
-    out = np.zeros((a.cols, contrib.shape[1]))
-    np.add.at(out, a.indices, contrib)
-    return out.reshape((a.cols,) + y.shape[1:])
+    return np.asarray(_scipy(a).T @ y)
 
 
 _gram_count = 0

@@ -308,12 +308,16 @@ void launch_cfg(const KParams& kp, cudaStream_t stream) {
   RP_LAUNCH_CHECK();
 }
 
+// Tile shapes: 0 = 128x128 (8 warps), 1 = 64x64 (4 warps), 2 = 128x32
+// (4 warps), 3 = 128x16 (4 warps) for skinny right-hand sides.
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
-  if (tile == 128)
-    launch_cfg<128, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream);
-  else
-    launch_cfg<64, 64, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream);
+  switch (tile) {
+    case 0: launch_cfg<128, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream); break;
+    case 1: launch_cfg<64, 64, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
+    case 2: launch_cfg<128, 32, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+    default: launch_cfg<128, 16, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+  }
 }
 
 }  // namespace
@@ -401,15 +405,40 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
                        g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
                        g.stride_b2 % 2 == 0;
 
-  // Split-K depends on (m, k) only, never on n (column determinism).
+  // Split-K.  With col_stable the factor depends on (m, k) only, never on n
+  // (column determinism); otherwise it is picked for full waves over the
+  // 148 SMs, counting only the tiles that run (lower_only skips the rest).
   int split = g.split_k;
   if (split <= 0) {
-    int64_t tiles = ceil_div(g.m, 128) * nb;
-    if (!g.col_stable) tiles *= ceil_div(g.n, 128);
-    const int64_t want = ceil_div(2 * 148, std::max<int64_t>(tiles, 1));
-    const int64_t cap = std::max<int64_t>(1, g.k / 512);
-    split = static_cast<int>(std::min<int64_t>(want, cap));
-    split = std::max(1, std::min(split, 64));
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(64, g.k / 512));
+    if (g.col_stable) {
+      const int64_t tiles_m = ceil_div(g.m, 128) * nb;
+      split = g.k <= 8192 ? 1
+                          : static_cast<int>(std::min<int64_t>(cap, ceil_div(2 * 148, std::max<int64_t>(tiles_m, 1))));
+    } else {
+      const int64_t tm = ceil_div(g.m, 128), tn = ceil_div(g.n, 128);
+      int64_t tiles = tm * tn;
+      if (g.lower_only) tiles = 0;
+      if (g.lower_only)
+        for (int64_t i = 0; i < tm; ++i) tiles += std::min<int64_t>(tn, i + 1);
+      tiles *= nb;
+      if (tiles >= 2 * 148 || cap == 1) {
+        split = 1;
+      } else {
+        // time ~ waves * (K / split) plus a per-split reduction overhead
+        double best = 1e30;
+        split = 1;
+        for (int64_t s2 = 1; s2 <= cap; ++s2) {
+          const double waves = static_cast<double>(ceil_div(tiles * s2, 148));
+          const double cost = waves / static_cast<double>(s2) * (1.0 + 0.03 * static_cast<double>(s2));
+          if (cost < best) {
+            best = cost;
+            split = static_cast<int>(s2);
+          }
+        }
+      }
+    }
+    split = std::max(1, split);
   }
   int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
   if (k_chunk == 0) k_chunk = 16;
@@ -419,7 +448,15 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   if (split > 1)
     kp.ws = workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, stream);
 
-  const int tile = (g.m >= 128 && g.n >= 128) ? 128 : 64;
+  int tile;
+  if (g.m >= 128 && g.n >= 128)
+    tile = 0;
+  else if (g.m >= 128 && g.n <= 16)
+    tile = 3;
+  else if (g.m >= 128 && g.n <= 32)
+    tile = 2;
+  else
+    tile = 1;
   if (ak && bk) {
     aligned ? launch_layout<true, true, 2>(kp, tile, stream) : launch_layout<true, true, 1>(kp, tile, stream);
   } else if (ak && !bk) {
