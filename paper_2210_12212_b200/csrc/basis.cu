@@ -11,9 +11,15 @@ unsigned grid_for(int64_t work, int threads = 256) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), 148 * 32)));
 }
 
-__global__ void build_args_kernel(BasisDims d, int64_t g, const double* __restrict__ y,
-                                  const double* __restrict__ gen, const double* __restrict__ tau,
-                                  double* __restrict__ args) {
+__device__ __forceinline__ double sum_partials(const Partials& P, int64_t b, int64_t i, int64_t j) {
+  const double* q = P.p + b * P.batch_stride + i + j * P.ld;
+  double v = q[0];
+  for (int s = 1; s < P.split; ++s) v += q[s * P.split_stride];
+  return v;
+}
+
+__global__ void build_args_kernel(BasisDims d, int64_t g, Partials y, const double* __restrict__ gen,
+                                  const double* __restrict__ tau, double* __restrict__ args) {
   const int64_t nb = d.L * d.K;
   const int64_t total = d.dim * (g + 1) * nb;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -24,7 +30,7 @@ __global__ void build_args_kernel(BasisDims d, int64_t g, const double* __restri
     const int64_t l = b / d.K, r = b % d.K;
     double v;
     if (j < g) {
-      v = __dmul_rn(tau[l], y[i + (j * nb + b) * d.dim]);
+      v = __dmul_rn(tau[l], sum_partials(y, 0, i, j * nb + b));
       if (j >= 1) v = __dadd_rn(v, gen[i + ((j - 1) * nb + b) * d.dim]);
     } else {
       v = gen[i + ((g - 1) * nb + b) * d.dim];
@@ -33,7 +39,7 @@ __global__ void build_args_kernel(BasisDims d, int64_t g, const double* __restri
   }
 }
 
-__global__ void update_kernel(BasisDims d, int64_t g, const double* __restrict__ applied, const int* __restrict__ kb,
+__global__ void update_kernel(BasisDims d, int64_t g, Partials applied, const int* __restrict__ kb,
                               double* __restrict__ gen, double* __restrict__ tilde, int* __restrict__ flags) {
   const int64_t nb = d.L * d.K;
   const int64_t total = d.dim * (g + 1) * nb;
@@ -44,7 +50,7 @@ __global__ void update_kernel(BasisDims d, int64_t g, const double* __restrict__
     const int64_t j = col / nb, b = col % nb;
     const int64_t l = b / d.K, r = b % d.K;
     if (g >= kb[l]) continue;  // this interval's loop has ended (path_solver.cpp:39)
-    const double a = applied[i + (l * d.kmax * d.K + j * d.K + r) * d.dim];
+    const double a = sum_partials(applied, l, i, j * d.K + r);
     double* gp = gen + i + col * d.dim;
     const double v = (j < g) ? __dsub_rn(*gp, a) : -a;
     *gp = v;
@@ -136,15 +142,15 @@ __global__ void fill_kernel(double* __restrict__ dst, int64_t count, double v) {
 
 }  // namespace
 
-void build_args(const BasisDims& d, int64_t g, const double* y, const double* gen, const double* d_tau,
+void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* gen, const double* d_tau,
                 double* args_im, cudaStream_t stream) {
   build_args_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, y, gen, d_tau, args_im);
   RP_LAUNCH_CHECK();
 }
 
-void update_gen(const BasisDims& d, int64_t g, const double* applied_im, const int* d_k, double* gen, double* tilde,
+void update_gen(const BasisDims& d, int64_t g, const Partials& applied, const int* d_k, double* gen, double* tilde,
                 int* d_flags, cudaStream_t stream) {
-  update_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, applied_im, d_k, gen, tilde, d_flags);
+  update_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, applied, d_k, gen, tilde, d_flags);
   RP_LAUNCH_CHECK();
 }
 

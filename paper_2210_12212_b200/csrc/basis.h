@@ -14,6 +14,8 @@
 
 #include <cstdint>
 
+#include "gemm_f64.h"
+
 namespace rpb {
 
 struct BasisDims {
@@ -26,13 +28,15 @@ struct BasisDims {
 
 // args_im[l][:, j*K + r] = tau_l * Y[:, j*NB + b] + (j >= 1 ? gen[:, (j-1)*NB + b] : 0) for j < g
 // args_im[l][:, g*K + r] = gen[:, (g-1)*NB + b]
-void build_args(const BasisDims& d, int64_t g, const double* y, const double* gen, const double* d_tau,
+// y is the Gram product (possibly as deferred split-K partials).
+void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* gen, const double* d_tau,
                 double* args_im, cudaStream_t stream);
 
 // gen[:, j*NB+b] -= applied[l][:, j*K+r] (j < g); gen[:, g*NB+b] = -applied[l][:, g*K+r];
 // flags[l] |= any non-finite in gen[:, 0..g]; tilde[:, j*NB+b] += gen[:, j*NB+b] (j <= g).
 // Problems whose interval has k_l <= g are left untouched.
-void update_gen(const BasisDims& d, int64_t g, const double* applied_im, const int* d_k, double* gen, double* tilde,
+// applied: batch l = interval, column j*K + r (possibly deferred partials).
+void update_gen(const BasisDims& d, int64_t g, const Partials& applied, const int* d_k, double* gen, double* tilde,
                 int* d_flags, cudaStream_t stream);
 
 // x[:, t*K + r] = tau_l * Horner(tilde of problem l*K + r, tau_l * lambda_t) for t < T,

@@ -25,26 +25,34 @@ constexpr int kGenThreads = 160;  // 156 generator lanes rounded up to 5 warps
 constexpr int kJumpThreads = 320;
 constexpr int kSeqWords = kDeg + kN;  // X_0 .. X_{deg+311}
 
-// dst[job] = poly[job](T) src[job]  (window jump).  One CTA per job; the word
-// sequence X_0..X_{deg(p)+311} is generated into shared memory, then word w of
-// the result is the XOR of X_{i+w} over the set coefficients i of p.
+// dst[job] = poly[job](T) src[job]  (window jump).  `parts` CTAs share a job:
+// each generates the word sequence X_0.. from the source window into shared
+// memory (up to the last coefficient it owns) and XORs X_{i+w} over its slice
+// of the set coefficients i of p into dst (zeroed beforehand) -- a jump costs
+// ~deg/parts sequence-window XORs per CTA instead of deg.
 __global__ void __launch_bounds__(kJumpThreads) jump_kernel(const uint64_t* __restrict__ src_base,
                                                             const int* __restrict__ src_idx,
                                                             uint64_t* __restrict__ dst_base,
                                                             const int* __restrict__ dst_idx,
                                                             const uint64_t* __restrict__ polys,
                                                             const int* __restrict__ poly_idx,
-                                                            const int* __restrict__ poly_deg) {
+                                                            const int* __restrict__ poly_deg, int parts) {
   extern __shared__ uint64_t X[];
-  const int job = blockIdx.x;
+  const int job = blockIdx.x / parts;
+  const int part = blockIdx.x - job * parts;
   const uint64_t* src = src_base + static_cast<int64_t>(src_idx[job]) * kN;
   uint64_t* dst = dst_base + static_cast<int64_t>(dst_idx[job]) * kN;
   const uint64_t* p = polys + static_cast<int64_t>(poly_idx[job]) * kPolyWords;
   const int deg = poly_deg[poly_idx[job]];
+  const int words = deg / 64 + 1;
+  const int per = (words + parts - 1) / parts;
+  const int w0 = part * per;
+  const int w1 = min(words, w0 + per);
+  if (w0 >= w1) return;
   const int t = threadIdx.x;
   for (int i = t; i < kN; i += blockDim.x) X[i] = src[i];
   __syncthreads();
-  const int need = deg + kN;  // words X_0 .. X_{deg+311}
+  const int need = min(deg, w1 * 64 - 1) + kN;  // words X_0 .. X_{last coefficient + 311}
   for (int base = kN; base < need; base += kM) {
     const int k = base + t;
     if (t < kM && k < need) X[k] = d_twist(X[k - kN], X[k - kN + 1], X[k - kM]);
@@ -52,8 +60,7 @@ __global__ void __launch_bounds__(kJumpThreads) jump_kernel(const uint64_t* __re
   }
   if (t < kN) {
     uint64_t acc = 0;
-    const int words = deg / 64 + 1;
-    for (int wi = 0; wi < words; ++wi) {
+    for (int wi = w0; wi < w1; ++wi) {
       uint64_t bits = p[wi];
       while (bits) {
         const int b = __ffsll(static_cast<long long>(bits)) - 1;
@@ -61,7 +68,10 @@ __global__ void __launch_bounds__(kJumpThreads) jump_kernel(const uint64_t* __re
         acc ^= X[wi * 64 + b + t];
       }
     }
-    dst[t] = acc;
+    if (parts == 1)
+      dst[t] = acc;
+    else
+      atomicXor(reinterpret_cast<unsigned long long*>(dst + t), static_cast<unsigned long long>(acc));
   }
 }
 
@@ -127,8 +137,10 @@ void run_jobs(const std::vector<JumpJob>& jobs, uint64_t* d_states, const uint64
     attr = true;
   }
   const int n = static_cast<int>(jobs.size());
-  jump_kernel<<<n, kJumpThreads, smem, stream>>>(src_base, d_meta.get(), d_states, d_meta.get() + n,
-                                                 d_polys.get(), d_meta.get() + 2 * n, d_meta.get() + 3 * n);
+  const int parts = std::max(1, std::min(16, 296 / n));
+  jump_kernel<<<n * parts, kJumpThreads, smem, stream>>>(src_base, d_meta.get(), d_states, d_meta.get() + n,
+                                                         d_polys.get(), d_meta.get() + 2 * n, d_meta.get() + 3 * n,
+                                                         parts);
   RP_LAUNCH_CHECK();
   // Host vectors above must outlive the async copies: synchronize cheaply via
   // the stream before they go out of scope.
@@ -144,6 +156,8 @@ int states_at(uint64_t seed, const std::vector<uint64_t>& offsets, uint64_t* d_s
   for (int64_t r = 1; r < R; ++r)
     require(offsets[r] >= offsets[r - (int64_t{1} << (63 - __builtin_clzll(static_cast<uint64_t>(r))))],
             "mt: offsets must be non-decreasing along the doubling schedule");
+  // every row is produced by exactly one job; multi-CTA jobs XOR into zeros
+  RP_CUDA(cudaMemsetAsync(d_states, 0, sizeof(uint64_t) * kN * static_cast<size_t>(R), stream));
   uint64_t seedw[kN];
   seed_window(seed, seedw);
   DBuf<uint64_t> d_seed(kN, stream);
@@ -347,6 +361,49 @@ __global__ void __launch_bounds__(kGenThreads) srht_fy_kernel(const uint64_t* __
   }
 }
 
+// SRHT fast path: words[0..n) are the signs, words[n + i] the Fisher-Yates
+// draw of pick i when no rejection occurs (flagged otherwise).  The divisions
+// run in parallel; only the swaps stay sequential.
+__global__ void srht_prep_kernel(const uint64_t* __restrict__ words, int64_t n, int64_t m, int64_t npad,
+                                 double* __restrict__ signs, int64_t* __restrict__ jv, int* flag) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t w = words[i];
+    if (i < n) {
+      signs[i] = (w >> 63) ? 1.0 : -1.0;
+    } else {
+      const int64_t p = i - n;
+      const uint64_t bound = static_cast<uint64_t>(npad - p);
+      if (w >= reject_limit(bound)) atomicOr(flag, 1);
+      jv[p] = p + static_cast<int64_t>(w % bound);
+    }
+  }
+}
+
+template <int CAP, bool SMEM>
+__global__ void srht_swap_kernel(const int64_t* __restrict__ jv, int64_t m, int64_t* rows, int64_t* gkeys,
+                                 int64_t* gvals) {
+  extern __shared__ int64_t dyn2[];
+  int64_t* keys = SMEM ? dyn2 : gkeys;
+  int64_t* vals = SMEM ? dyn2 + CAP : gvals;
+  for (int64_t i = threadIdx.x; i < CAP; i += blockDim.x) keys[i] = -1;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t j = jv[i];
+    int64_t* si = map_slot<CAP>(keys, i);
+    const int64_t vi = (*si == i) ? vals[si - keys] : i;
+    int64_t* sj = map_slot<CAP>(keys, j);
+    const int64_t vj = (*sj == j) ? vals[sj - keys] : j;
+    *si = i;
+    vals[si - keys] = vj;
+    sj = map_slot<CAP>(keys, j);
+    *sj = j;
+    vals[sj - keys] = vi;
+    rows[i] = vj;
+  }
+}
+
 std::vector<uint64_t> progression(uint64_t first, uint64_t stride, int64_t count) {
   std::vector<uint64_t> o(static_cast<size_t>(count));
   for (int64_t r = 0; r < count; ++r) o[r] = first + static_cast<uint64_t>(r) * stride;
@@ -355,14 +412,22 @@ std::vector<uint64_t> progression(uint64_t first, uint64_t stride, int64_t count
 
 constexpr int64_t kSegWords = 1 << 16;
 
+// Segment length: one sequential block for short streams (no jump at all),
+// otherwise enough segments to fill the machine twice over.
+int64_t seg_words(int64_t count) {
+  if (count <= (int64_t{1} << 17)) return std::max<int64_t>(count, 2);
+  return std::max<int64_t>(kSegWords, (ceil_div(count, 296) + 1) & ~int64_t{1});
+}
+
 }  // namespace
 
 void draw_words(uint64_t seed, uint64_t skip, int64_t count, WordMode mode, void* d_out, cudaStream_t stream) {
   if (count <= 0) return;
-  const int64_t segs = ceil_div(count, kSegWords);
+  const int64_t seg = seg_words(count);
+  const int64_t segs = ceil_div(count, seg);
   DBuf<uint64_t> st(static_cast<size_t>(segs) * kN, stream);
-  mt::states_at(seed, progression(skip, kSegWords, segs), st.get(), stream);
-  words_kernel<<<static_cast<unsigned>(segs), kGenThreads, 0, stream>>>(st.get(), kSegWords, count,
+  mt::states_at(seed, progression(skip, seg, segs), st.get(), stream);
+  words_kernel<<<static_cast<unsigned>(segs), kGenThreads, 0, stream>>>(st.get(), seg, count,
                                                                          static_cast<int>(mode), d_out);
   RP_LAUNCH_CHECK();
 }
@@ -370,12 +435,13 @@ void draw_words(uint64_t seed, uint64_t skip, int64_t count, WordMode mode, void
 void draw_uniform_index(uint64_t seed, uint64_t bound, int64_t count, uint64_t* d_out, cudaStream_t stream) {
   require(bound >= 1, "uniform_index: bound must be positive");
   if (count <= 0) return;
-  const int64_t segs = ceil_div(count, kSegWords);
+  const int64_t seg = seg_words(count);
+  const int64_t segs = ceil_div(count, seg);
   DBuf<uint64_t> st(static_cast<size_t>(segs) * kN, stream);
   DBuf<int> flag(1, stream);
   RP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), stream));
-  mt::states_at(seed, progression(0, kSegWords, segs), st.get(), stream);
-  uindex_kernel<<<static_cast<unsigned>(segs), kGenThreads, 0, stream>>>(st.get(), kSegWords, count, bound, d_out,
+  mt::states_at(seed, progression(0, seg, segs), st.get(), stream);
+  uindex_kernel<<<static_cast<unsigned>(segs), kGenThreads, 0, stream>>>(st.get(), seg, count, bound, d_out,
                                                                           flag.get());
   RP_LAUNCH_CHECK();
   int hflag = 0;
@@ -493,38 +559,55 @@ void draw_srht(uint64_t seed, int64_t n, int64_t m, double* d_signs, int64_t* d_
   int64_t npad = 1;
   while (npad < n) npad <<= 1;
   require(m <= npad, "srht: m must not exceed the padded size");
-  draw_words(seed, 0, n, WordMode::Sign, d_signs, stream);
-  DBuf<uint64_t> st(kN, stream);
-  mt::states_at(seed, {static_cast<uint64_t>(n)}, st.get(), stream);
   // map capacity: power of two >= 4m (at most 2m distinct keys are touched)
   int64_t cap = 1024;
   while (cap < 4 * m) cap <<= 1;
+  require(cap <= (int64_t{1} << 22), "srht: m too large for the Fisher-Yates map");
   const bool in_smem = cap <= 8192;
   DBuf<int64_t> keys(in_smem ? 1 : static_cast<size_t>(cap), stream), vals(in_smem ? 1 : static_cast<size_t>(cap), stream);
-  auto launch = [&](auto kern, bool smem) {
+  // Fast path: all n + m words at once, divisions in parallel.
+  DBuf<uint64_t> words(static_cast<size_t>(n + m), stream);
+  DBuf<int64_t> jv(static_cast<size_t>(m), stream);
+  DBuf<int> flag(1, stream);
+  RP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), stream));
+  draw_words(seed, 0, n + m, WordMode::Raw, words.get(), stream);
+  srht_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n + m, 256), 148 * 8)), 256, 0, stream>>>(
+      words.get(), n, m, npad, d_signs, jv.get(), flag.get());
+  RP_LAUNCH_CHECK();
+  int hflag = 0;
+  RP_CUDA(cudaMemcpyAsync(&hflag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+  RP_CUDA(cudaStreamSynchronize(stream));
+  auto go = [&](auto seq_kern, auto swap_kern, bool smem) {
     const int bytes = smem ? static_cast<int>(2 * cap * sizeof(int64_t)) : 0;
-    if (smem) RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<1, kGenThreads, bytes, stream>>>(st.get(), m, npad, d_rows, keys.get(), vals.get());
+    if (!hflag) {
+      if (smem) RP_CUDA(cudaFuncSetAttribute(swap_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      swap_kern<<<1, 256, bytes, stream>>>(jv.get(), m, d_rows, keys.get(), vals.get());
+    } else {  // a rejection somewhere: exact sequential consumer from offset n
+      DBuf<uint64_t> st(kN, stream);
+      mt::states_at(seed, {static_cast<uint64_t>(n)}, st.get(), stream);
+      if (smem) RP_CUDA(cudaFuncSetAttribute(seq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      seq_kern<<<1, kGenThreads, bytes, stream>>>(st.get(), m, npad, d_rows, keys.get(), vals.get());
+      RP_CUDA(cudaStreamSynchronize(stream));
+    }
     RP_LAUNCH_CHECK();
   };
+#define RP_FY(C, SM) go(srht_fy_kernel<C, SM>, srht_swap_kernel<C, SM>, SM)
   switch (cap) {
-    case 1024: launch(srht_fy_kernel<1024, true>, true); break;
-    case 2048: launch(srht_fy_kernel<2048, true>, true); break;
-    case 4096: launch(srht_fy_kernel<4096, true>, true); break;
-    case 8192: launch(srht_fy_kernel<8192, true>, true); break;
-    case 16384: launch(srht_fy_kernel<16384, false>, false); break;
-    case 32768: launch(srht_fy_kernel<32768, false>, false); break;
-    case 65536: launch(srht_fy_kernel<65536, false>, false); break;
-    case 131072: launch(srht_fy_kernel<131072, false>, false); break;
-    default: {
-      require(cap <= (int64_t{1} << 22), "srht: m too large for the Fisher-Yates map");
-      if (cap <= 262144) launch(srht_fy_kernel<262144, false>, false);
-      else if (cap <= 524288) launch(srht_fy_kernel<524288, false>, false);
-      else if (cap <= 1048576) launch(srht_fy_kernel<1048576, false>, false);
-      else if (cap <= 2097152) launch(srht_fy_kernel<2097152, false>, false);
-      else launch(srht_fy_kernel<4194304, false>, false);
-    }
+    case 1024: RP_FY(1024, true); break;
+    case 2048: RP_FY(2048, true); break;
+    case 4096: RP_FY(4096, true); break;
+    case 8192: RP_FY(8192, true); break;
+    case 16384: RP_FY(16384, false); break;
+    case 32768: RP_FY(32768, false); break;
+    case 65536: RP_FY(65536, false); break;
+    case 131072: RP_FY(131072, false); break;
+    case 262144: RP_FY(262144, false); break;
+    case 524288: RP_FY(524288, false); break;
+    case 1048576: RP_FY(1048576, false); break;
+    case 2097152: RP_FY(2097152, false); break;
+    default: RP_FY(4194304, false); break;
   }
+#undef RP_FY
   RP_CUDA(cudaStreamSynchronize(stream));
 }
 

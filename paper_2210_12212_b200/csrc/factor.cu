@@ -13,44 +13,71 @@ namespace {
 
 constexpr int NB = 64;
 
-// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix.
-__global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
-                                                  int* info) {
+// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix:
+// one warp per matrix, lane l owns rows l and l + 32 (no block barriers).  The
+// finished column j is copied to a separate array so the trailing update's
+// loads never alias its stores (lets the compiler pipeline the loop).
+__global__ void __launch_bounds__(32) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
+                                                 int* info) {
   __shared__ double T[NB][NB + 1];
+  __shared__ double colj[NB];
   double* A = h + blockIdx.x * stride + k0 + k0 * ld;
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int i = e % kb, j = e / kb;
-    T[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
-  }
-  __syncthreads();
+  const int lane = threadIdx.x;
+#pragma unroll 8
   for (int j = 0; j < kb; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = T[j][j];
-      if (!(d > 0.0) || !isfinite(d)) {
-        if (info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + j + 1);
-        T[j][j] = 1.0;  // keep going; the caller reports the failure
-      } else {
-        T[j][j] = sqrt(d);
+    if (lane < kb) T[lane][j] = A[lane + j * ld];
+    if (lane + 32 < kb) T[lane + 32][j] = A[lane + 32 + j * ld];
+  }
+  __syncwarp();
+  int bad = 0;
+  for (int j = 0; j < kb; ++j) {
+    double d = T[j][j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (!bad) bad = j + 1;
+      d = 1.0;  // keep going; the caller reports the failure
+    }
+    const double piv = sqrt(d);
+    const double inv = 1.0 / piv;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int r = lane + 32 * h2;
+      if (r >= j && r < kb) {
+        const double v = (r == j) ? piv : T[r][j] * inv;
+        T[r][j] = v;
+        colj[r] = v;
       }
     }
-    __syncthreads();
-    const double piv = T[j][j];
-    for (int i = j + 1 + threadIdx.x; i < kb; i += blockDim.x) T[i][j] /= piv;
-    __syncthreads();
-    const int rem = kb - j - 1;
-    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-      const int i = j + 1 + e % rem, c = j + 1 + e / rem;
-      if (i >= c) T[i][c] -= T[i][j] * T[c][j];
+    __syncwarp();
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int r = lane + 32 * h2;
+      if (r > j && r < kb) {
+        const double lrj = colj[r];
+        double* row = &T[r][0];
+        int c = j + 1;
+        for (; c + 3 <= r; c += 4) {
+          const double c0 = colj[c], c1 = colj[c + 1], c2 = colj[c + 2], c3 = colj[c + 3];
+          const double t0 = row[c], t1 = row[c + 1], t2 = row[c + 2], t3 = row[c + 3];
+          row[c] = t0 - lrj * c0;
+          row[c + 1] = t1 - lrj * c1;
+          row[c + 2] = t2 - lrj * c2;
+          row[c + 3] = t3 - lrj * c3;
+        }
+        for (; c <= r; ++c) row[c] -= lrj * colj[c];
+      }
     }
-    __syncthreads();
+    __syncwarp();
   }
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int i = e % kb, j = e / kb;
-    if (i >= j) A[i + j * ld] = T[i][j];
+  if (bad && lane == 0 && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
+#pragma unroll 8
+  for (int j = 0; j < kb; ++j) {
+    if (lane < kb && lane >= j) A[lane + j * ld] = T[lane][j];
+    if (lane + 32 < kb && lane + 32 >= j) A[lane + 32 + j * ld] = T[lane + 32][j];
   }
 }
 
-// Panel solve X * L11^T = B for the rows below the diagonal block.
+// Panel solve X * L11^T = B for the rows below the diagonal block; one thread
+// per row, 128 rows per CTA; four independent partial sums per dot product.
 __global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
                                                   int64_t rows) {
   extern __shared__ double dsm[];
@@ -58,31 +85,35 @@ __global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t
   double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
   double* base = h + blockIdx.y * stride;
   const double* L11 = base + k0 + k0 * ld;
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int i = e % kb, j = e / kb;
-    L[i][j] = L11[i + j * ld];
-  }
+  const int t = threadIdx.x;
+#pragma unroll 8
+  for (int j = 0; j < kb; ++j)
+    if (t < kb) L[t][j] = L11[t + j * ld];
   const int64_t r0 = k0 + kb + static_cast<int64_t>(blockIdx.x) * 128;
   const int nr = static_cast<int>((k0 + kb + rows - r0) < 128 ? (k0 + kb + rows - r0) : 128);
   double* B = base + k0 * ld;  // column k0 of the matrix
-  for (int e = threadIdx.x; e < nr * kb; e += blockDim.x) {
-    const int i = e % nr, j = e / nr;
-    X[i][j] = B[r0 + i + j * ld];
-  }
+#pragma unroll 8
+  for (int j = 0; j < kb; ++j)
+    if (t < nr) X[t][j] = B[r0 + t + j * ld];
   __syncthreads();
-  const int r = threadIdx.x;
-  if (r < nr) {
+  if (t < nr) {
     for (int j = 0; j < kb; ++j) {
-      double s = X[r][j];
-      for (int i = 0; i < j; ++i) s -= X[r][i] * L[j][i];
-      X[r][j] = s / L[j][j];
+      double s0 = X[t][j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = 0;
+      for (; i + 3 < j; i += 4) {
+        s0 -= X[t][i] * L[j][i];
+        s1 -= X[t][i + 1] * L[j][i + 1];
+        s2 -= X[t][i + 2] * L[j][i + 2];
+        s3 -= X[t][i + 3] * L[j][i + 3];
+      }
+      for (; i < j; ++i) s0 -= X[t][i] * L[j][i];
+      X[t][j] = ((s0 + s1) + (s2 + s3)) / L[j][j];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nr * kb; e += blockDim.x) {
-    const int i = e % nr, j = e / nr;
-    B[r0 + i + j * ld] = X[i][j];
-  }
+#pragma unroll 8
+  for (int j = 0; j < kb; ++j)
+    if (t < nr) B[r0 + t + j * ld] = X[t][j];
 }
 
 // In-place inverse of each nb x nb lower-triangular diagonal block; zeroes the
@@ -94,9 +125,11 @@ __global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t l
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * NB;
   const int kb = static_cast<int>((n - k0) < NB ? (n - k0) : NB);
   double* A = h + blockIdx.y * stride + k0 + k0 * ld;
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int i = e % kb, j = e / kb;
-    L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
+  {
+    const int i = threadIdx.x;
+#pragma unroll 8
+    for (int j = 0; j < kb; ++j)
+      if (i < kb) L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
   }
   __syncthreads();
   const int c = threadIdx.x;
@@ -104,15 +137,24 @@ __global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t l
     X[c][c] = 1.0 / L[c][c];
     for (int i = 0; i < c; ++i) X[i][c] = 0.0;
     for (int i = c + 1; i < kb; ++i) {
-      double s = 0.0;
-      for (int k = c; k < i; ++k) s += L[i][k] * X[k][c];
-      X[i][c] = -s / L[i][i];
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = c;
+      for (; k + 3 < i; k += 4) {
+        s0 += L[i][k] * X[k][c];
+        s1 += L[i][k + 1] * X[k + 1][c];
+        s2 += L[i][k + 2] * X[k + 2][c];
+        s3 += L[i][k + 3] * X[k + 3][c];
+      }
+      for (; k < i; ++k) s0 += L[i][k] * X[k][c];
+      X[i][c] = -((s0 + s1) + (s2 + s3)) / L[i][i];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int i = e % kb, j = e / kb;
-    A[i + j * ld] = X[i][j];
+  {
+    const int i = threadIdx.x;
+#pragma unroll 8
+    for (int j = 0; j < kb; ++j)
+      if (i < kb) A[i + j * ld] = X[i][j];
   }
 }
 
@@ -133,7 +175,7 @@ __global__ void shifted_copy_kernel(const double* __restrict__ g, int64_t n, con
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n * n;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = idx % n, j = idx / n;
-    H[idx] = (i == j) ? g[idx] + s : g[idx];
+    H[idx] = (i == j) ? g[idx] + s : (i > j ? g[idx] : 0.0);
   }
 }
 
@@ -157,7 +199,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // 1) Cholesky, lower.
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
-    potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
+    potrf_diag<<<static_cast<unsigned>(batch), 32, 0, stream>>>(h, ld, stride, k0, kb, info.get());
     RP_LAUNCH_CHECK();
     const int64_t rows = n - k0 - kb;
     if (rows <= 0) break;
@@ -194,9 +236,8 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   }
   // 2) Triangular inverse in place.
   {
-    dim3 zg(grid1(n * n), static_cast<unsigned>(batch));
-    zero_upper<<<zg, 256, 0, stream>>>(h, n, ld, stride);
-    RP_LAUNCH_CHECK();
+    // (the strict upper triangle is already zero: shifted_copies writes it so
+    // and potrf only touches the lower triangle)
     dim3 dg(static_cast<unsigned>(ceil_div(n, NB)), static_cast<unsigned>(batch));
     constexpr int kDiagSmem = 2 * NB * (NB + 1) * 8;
     static bool attr = false;
@@ -285,6 +326,8 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     g.batch = batch;
     g.lower_only = true;
     g.mirror = true;
+    g.tri_k = true;  // L^{-1} is lower triangular
+    g.split_k = 1;
     dgemm(g, stream);
   }
   std::vector<int> hinfo(static_cast<size_t>(batch));

@@ -13,13 +13,15 @@
 
 namespace rpb {
 
-// For b < batch: H_b (n x n, column-major, leading dim ld, stride `stride`) is
-// overwritten (scratch); out_b = H_b^{-1} (full symmetric).  Throws
-// FactorFailure if some H_b is not numerically positive definite.
+// For b < batch: H_b (n x n, column-major, leading dim ld, stride `stride`;
+// lower triangle read, strict upper triangle must be zero) is overwritten
+// (scratch); out_b = H_b^{-1} (full symmetric).  Throws FactorFailure if some
+// H_b is not numerically positive definite.
 void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64_t batch, double* out,
                          int64_t ldo, int64_t stride_o, cudaStream_t stream);
 
-// H_b = G + shift_b * I for b < batch (G shared, n x n).
+// H_b = lower(G) + shift_b * I for b < batch (G shared, n x n), strict upper
+// triangle zero -- the input spd_inverse_batched expects.
 void shifted_copies(const double* g, int64_t n, const double* d_shifts, int64_t batch, double* h, cudaStream_t stream);
 
 }  // namespace rpb

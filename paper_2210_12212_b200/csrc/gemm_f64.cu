@@ -59,6 +59,7 @@ struct KParams {
   int64_t k_chunk;  // K per split (multiple of the tile K)
   double* ws;       // split partials: [batch][split][n][m]
   bool lower_only;
+  bool tri_k;  // op(A)(i, k) == 0 for k < i: start the k loop at the tile's first row
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
@@ -149,8 +150,9 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   const int64_t b1 = bidx % p.batch, b2 = bidx / p.batch;
   const double* A = p.a + b1 * p.stride_a + b2 * p.stride_a2;
   const double* B = p.b + b1 * p.stride_b + b2 * p.stride_b2;
-  const int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
+  int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
   const int64_t kend = min(p.k, kbeg + p.k_chunk);
+  if (p.tri_k) kbeg = max(kbeg, m0 & ~static_cast<int64_t>(BK - 1));
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
   double acc[C::FM][C::FN][2];
@@ -308,15 +310,24 @@ void launch_cfg(const KParams& kp, cudaStream_t stream) {
   RP_LAUNCH_CHECK();
 }
 
-// Tile shapes: 0 = 128x128 (8 warps), 1 = 64x64 (4 warps), 2 = 128x32
-// (4 warps), 3 = 128x16 (4 warps) for skinny right-hand sides.
+// Tile shapes, largest first: 128x128 (8 warps), 64x64, 128x32, 64x32,
+// 128x16 (4 warps each).
+struct TileShape {
+  int bm, bn;
+};
+constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128}, {128, 64}};
+constexpr int kNumTiles = 7;
+
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
   switch (tile) {
     case 0: launch_cfg<128, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream); break;
     case 1: launch_cfg<64, 64, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
     case 2: launch_cfg<128, 32, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
-    default: launch_cfg<128, 16, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+    case 3: launch_cfg<64, 32, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
+    case 4: launch_cfg<128, 16, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+    case 5: launch_cfg<64, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream); break;
+    default: launch_cfg<128, 64, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
   }
 }
 
@@ -397,6 +408,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   kp.stride_b2 = g.stride_b2;
   kp.stride_c2 = g.stride_c2;
   kp.lower_only = g.lower_only;
+  kp.tri_k = g.tri_k;
 
   const bool ak = g.opa == Op::T;  // A contiguous along k
   const bool bk = g.opb == Op::N;  // B contiguous along k
@@ -412,9 +424,13 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   if (split <= 0) {
     const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(64, g.k / 512));
     if (g.col_stable) {
+      // a function of k only (and of m for long k): every column of C sees the
+      // same reduction order whatever n is
       const int64_t tiles_m = ceil_div(g.m, 128) * nb;
-      split = g.k <= 8192 ? 1
+      // (k <= 8192: chunks of 128 -- cheap when the consumer sums the partials)
+      split = g.k <= 8192 ? static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, g.k / 128)))
                           : static_cast<int>(std::min<int64_t>(cap, ceil_div(2 * 148, std::max<int64_t>(tiles_m, 1))));
+      if (g.k < 256) split = 1;
     } else {
       const int64_t tm = ceil_div(g.m, 128), tn = ceil_div(g.n, 128);
       int64_t tiles = tm * tn;
@@ -448,15 +464,27 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   if (split > 1)
     kp.ws = workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, stream);
 
-  int tile;
-  if (g.m >= 128 && g.n >= 128)
-    tile = 0;
-  else if (g.m >= 128 && g.n <= 16)
-    tile = 3;
-  else if (g.m >= 128 && g.n <= 32)
-    tile = 2;
-  else
-    tile = 1;
+  // Tile choice: estimated time = waves x per-wave tile work, where a wave is
+  // 148 SMs x CTAs-per-SM for the shape (ties keep the larger tile).
+  int tile = 0;
+  {
+    // CTAs per SM and relative large-problem throughput per shape (measured,
+    // profiles/gemm_tune_r01.txt)
+    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1};
+    static constexpr double kEff[] = {0.93, 0.94, 0.89, 0.91, 0.69, 1.0, 0.98};
+    double best = 1e300;
+    for (int t = 0; t < kNumTiles; ++t) {
+      if (kTiles[t].bn == 16 && g.n > 16) continue;
+      const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
+      const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));
+      const double cost = waves * kTiles[t].bm * kTiles[t].bn * kOcc[t] / kEff[t];
+      if (cost < best * 0.999) {
+        best = cost;
+        tile = t;
+      }
+    }
+  }
+  if (g.force_tile >= 0 && g.force_tile < kNumTiles) tile = g.force_tile;
   if (ak && bk) {
     aligned ? launch_layout<true, true, 2>(kp, tile, stream) : launch_layout<true, true, 1>(kp, tile, stream);
   } else if (ak && !bk) {
@@ -467,7 +495,24 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     aligned ? launch_layout<false, false, 2>(kp, tile, stream) : launch_layout<false, false, 1>(kp, tile, stream);
   }
   g_last_launches = 1;
-  if (split > 1) {
+  const bool defer = g.partials && !g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0;
+  if (g.partials) {
+    Partials& P = *g.partials;
+    if (defer && split > 1) {
+      P.p = kp.ws;
+      P.split = split;
+      P.ld = g.m;
+      P.split_stride = g.m * g.n;
+      P.batch_stride = split * g.m * g.n;
+    } else {
+      P.p = g.c;
+      P.split = 1;
+      P.ld = g.ldc;
+      P.split_stride = 0;
+      P.batch_stride = g.stride_c;
+    }
+  }
+  if (split > 1 && !(defer && g.partials)) {
     dim3 grid(static_cast<unsigned>(std::min<int64_t>(ceil_div(g.m * g.n, 256), 148 * 8)),
               static_cast<unsigned>(nb));
     splitk_reduce<<<grid, 256, 0, stream>>>(kp);

@@ -39,10 +39,30 @@ struct GemmArgs {
   // triangle is filled by a mirror pass when `mirror` is set.
   bool lower_only = false;
   bool mirror = false;
+  // op(A)(i, k) == 0 for k < i (A^T of a lower-triangular matrix): each output
+  // tile skips the k range below its first row.  Requires split_k == 1.
+  bool tri_k = false;
   // Deterministic split-K factor; 0 = heuristic.  With col_stable the
   // heuristic looks at (m, k) only, so column j of C does not depend on n.
   int split_k = 0;
   bool col_stable = false;
+  // Deferred split-K: when the chosen split is > 1 the partial products are
+  // left in `*partials` (see Partials) for the consumer to sum in split order,
+  // and no reduction kernel runs.  Ignored for lower_only / mirror.
+  struct Partials* partials = nullptr;
+  // Tuning hook: force a tile shape index (see gemm_f64.cu kTiles), -1 = auto.
+  int force_tile = -1;
+};
+
+// Where a GEMM result lives when its reduction is deferred.  Element (i, j) of
+// batch b is  sum_{s < split} p[b * batch_stride + s * split_stride + i + j * ld]
+// (summed in s order -- bitwise what the split-K reduction kernel computes).
+struct Partials {
+  const double* p = nullptr;
+  int split = 1;
+  int64_t ld = 0;
+  int64_t split_stride = 0;
+  int64_t batch_stride = 0;
 };
 
 // Launches on `stream`.  `workspace` (may be null) is used for split-K partials;

@@ -31,6 +31,7 @@
 #include "draws.h"
 #include "factor.h"
 #include "gemm_f64.h"
+#include "gram_pass.h"
 #include "mt19937.h"
 #include "operator.h"
 #include "ridgepath_b200.h"
@@ -344,7 +345,10 @@ void op_apply(rp_ctx* ctx, const OpView& op, const double* x, int64_t cols, doub
 // x (D x cols) = M_local^T y (n_loc x cols), summed over ranks
 void op_apply_t(rp_ctx* ctx, const OpView& op, const double* y, int64_t cols, double* x, bool reduce = true) {
   cudaStream_t s = ctx->stream;
-  if (!op.sparse) {
+  if (!op.sparse && !op.trans && cols <= kNarrowMax) {
+    // one HBM pass over the operator (gram_pass.cu)
+    atv_narrow(op.a, op.ld, op.n_loc, op.d, y, cols, x, s);
+  } else if (!op.sparse) {
     GemmArgs g;
     g.opa = op.op_mt();
     g.m = op.d;
@@ -371,13 +375,19 @@ struct GramOp {
   rp_ctx* ctx = nullptr;
   OpView op;
   bool matrix = false;
+  // The fused single-pass kernel serves narrow standalone products
+  // (rp_gram_apply); the recursion keeps one code path for every width so a
+  // column's bits do not depend on how many problems are batched with it.
+  bool allow_fused = false;
   DBuf<double> G;  // D x D when matrix
   DBuf<double> tmp;
 
-  // Y (D x cols) = M^T (M W)  (matrix.cpp:168-172) or G W.
-  void apply(const double* W, int64_t cols, double* Y) {
+  // Y (D x cols) = M^T (M W)  (matrix.cpp:168-172) or G W.  With `out`
+  // the split-K reduction of G W may be left to the consumer.
+  void apply(const double* W, int64_t cols, double* Y, Partials* out = nullptr) {
     cudaStream_t s = ctx->stream;
     if (cols <= 0) return;
+    if (out) *out = Partials{Y, 1, op.d, 0, 0};
     if (matrix) {
       GemmArgs g;
       g.m = op.d;
@@ -390,7 +400,12 @@ struct GramOp {
       g.c = Y;
       g.ldc = op.d;
       g.col_stable = true;
+      g.partials = out;
       dgemm(g, s);
+      return;
+    }
+    if (allow_fused && !op.sparse && !op.trans && cols <= 8 && gram_fused(op.a, op.ld, op.n_loc, op.d, W, cols, Y, s)) {
+      allreduce(ctx, Y, op.d * cols);  // fused single pass over the operator
       return;
     }
     const size_t need = static_cast<size_t>(op.n_loc * cols);
@@ -480,9 +495,11 @@ struct PrecondBatch {
 
   // out_l (d x cols) = P_l in_l for l < L; in/out strided by `sin`/`sout`
   // (sin = 0 broadcasts one input to every interval).
-  void apply(rp_ctx* ctx, const double* in, int64_t sin, int64_t cols, double* out, int64_t sout) const {
+  void apply(rp_ctx* ctx, const double* in, int64_t sin, int64_t cols, double* out, int64_t sout,
+             Partials* part = nullptr) const {
     cudaStream_t s = ctx->stream;
     if (cols <= 0) return;
+    if (part) *part = Partials{out, 1, d, 0, sout};
     if (!woodbury) {
       GemmArgs g;
       g.m = d;
@@ -499,6 +516,7 @@ struct PrecondBatch {
       g.stride_c = sout;
       g.batch = L;
       g.col_stable = true;
+      g.partials = part;
       dgemm(g, s);
       return;
     }
@@ -614,11 +632,12 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
     const int64_t stride_im = dim * kmax * K;
     DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);
     DBuf<double> args(static_cast<size_t>(L * stride_im), s), applied(static_cast<size_t>(L * stride_im), s);
+    Partials py, pa;
     for (int64_t g = 1; g < kmax; ++g) {
-      gram.apply(out.gen.get(), g * NB, y.get());
-      build_args(d, g, y.get(), out.gen.get(), out.d_tau.get(), args.get(), s);
-      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im);
-      update_gen(d, g, applied.get(), out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+      gram.apply(out.gen.get(), g * NB, y.get(), &py);
+      build_args(d, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
+      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
+      update_gen(d, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
     }
   }
   out.diverged.assign(static_cast<size_t>(L), 0);
@@ -1259,6 +1278,7 @@ rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out
     GramOp g;
     g.ctx = ctx;
     g.op = op;
+    g.allow_fused = true;
     if (ncols > 0) g.apply(in.ptr, ncols, out.dev);
     out.finish();
   });

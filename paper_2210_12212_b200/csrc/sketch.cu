@@ -107,19 +107,6 @@ __global__ void count_csc(const int64_t* __restrict__ coff, const int32_t* __res
 
 // ---- SRHT ------------------------------------------------------------------------
 
-// x[i, c] = sign[row0 + i] * M(i, c) at global position row0 + i; zero elsewhere.
-__global__ void srht_load_dense(const double* __restrict__ a, int64_t ld, bool trans, int64_t n_loc, int64_t row0,
-                                int64_t d, const double* __restrict__ signs, double* __restrict__ x, int64_t npad) {
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < npad * d;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx % npad, c = idx / npad;
-    const int64_t li = i - row0;
-    double v = 0.0;
-    if (li >= 0 && li < n_loc) v = signs[i] * (trans ? a[c + li * ld] : a[li + c * ld]);
-    x[idx] = v;
-  }
-}
-
 __global__ void srht_scatter_csc(const int64_t* __restrict__ coff, const int32_t* __restrict__ crow,
                                  const double* __restrict__ cval, int64_t row0, int64_t d,
                                  const double* __restrict__ signs, double* __restrict__ x, int64_t npad) {
@@ -133,64 +120,99 @@ __global__ void srht_scatter_csc(const int64_t* __restrict__ coff, const int32_t
 
 // One pass of butterflies over index bits [lo, lo + B): for every column and
 // every fixed value of the other bits, an S = 2^B point transform with the
-// largest stride first (the reference's descending recursion).
+// largest stride first (the reference's descending recursion, sketch.cpp:25-48).
+// Tile = S x W elements (W consecutive low indices).  from_op: the first pass
+// reads the operator directly (x[i] = sign[i] * M(i - row0, c), zero padding,
+// sketch.cpp:160-162); to_sa: the last pass (lo = 0, W = 1) writes only the
+// sampled rows, scaled, into SA (sketch.cpp:168-170).
+struct FwhtArgs {
+  double* x;  // scratch, npad x d
+  int64_t npad, d;
+  int lo, logW;
+  bool from_op;
+  const double* a;
+  int64_t lda, n_loc, row0;
+  bool trans;
+  const double* signs;
+  bool to_sa;
+  const int64_t* tpos;  // target positions sorted ascending
+  const int32_t* tslot;
+  const int32_t* boff;  // per S-block offsets into tpos (npad/S + 1)
+  double scale;
+  double* sa;
+  int64_t m;
+};
+
 template <int B>
-__global__ void __launch_bounds__(256) fwht_pass(double* __restrict__ x, int64_t npad, int lo, int W) {
+__global__ void __launch_bounds__(256) fwht_pass(FwhtArgs f) {
   constexpr int S = 1 << B;
   extern __shared__ double tile[];  // [S][W]
-  const int64_t groups_per_col = npad / (static_cast<int64_t>(S) * W);
+  const int W = 1 << f.logW;
+  const int64_t groups_per_col = f.npad >> (B + f.logW);
   const int64_t c = blockIdx.x / groups_per_col;
-  const int64_t gidx = blockIdx.x % groups_per_col;
-  const int64_t low_span = int64_t{1} << lo;
-  const int64_t wblocks = low_span / W;  // groups of W consecutive low values
-  const int64_t hi_part = gidx / wblocks;
-  const int64_t l0 = (gidx % wblocks) * W;
-  double* col = x + c * npad;
-  const int64_t base = hi_part * (static_cast<int64_t>(S) << lo) + l0;
-  const int total = S * W;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int t = e / W, l = e % W;
-    tile[e] = col[base + (static_cast<int64_t>(t) << lo) + l];
+  const int64_t gidx = blockIdx.x - c * groups_per_col;
+  const int64_t wblocks = int64_t{1} << (f.lo - f.logW);
+  const int64_t hi_part = gidx >> (f.lo - f.logW);
+  const int64_t l0 = (gidx & (wblocks - 1)) << f.logW;
+  const int64_t base = (hi_part << (B + f.lo)) + l0;
+  const int total = S << f.logW;
+  double* col = f.x + c * f.npad;
+  if (f.from_op) {
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int t = e >> f.logW, l = e & (W - 1);
+      const int64_t i = base + (static_cast<int64_t>(t) << f.lo) + l;
+      const int64_t li = i - f.row0;
+      double v = 0.0;
+      if (li >= 0 && li < f.n_loc) v = f.signs[i] * (f.trans ? f.a[c + li * f.lda] : f.a[li + c * f.lda]);
+      tile[e] = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int t = e >> f.logW, l = e & (W - 1);
+      tile[e] = col[base + (static_cast<int64_t>(t) << f.lo) + l];
+    }
   }
   __syncthreads();
-  for (int h = S / 2; h >= 1; h >>= 1) {
-    for (int e = threadIdx.x; e < total / 2; e += blockDim.x) {
-      const int pair = e / W, l = e % W;
-      const int t = (pair / h) * 2 * h + (pair % h);
-      double* pa = tile + t * W + l;
-      double* pb = tile + (t + h) * W + l;
+#pragma unroll 1
+  for (int lh = B - 1; lh >= 0; --lh) {
+    const int h = 1 << lh;
+    for (int e = threadIdx.x; e < (total >> 1); e += blockDim.x) {
+      const int pair = e >> f.logW, l = e & (W - 1);
+      const int t = ((pair >> lh) << (lh + 1)) + (pair & (h - 1));
+      double* pa = tile + (t << f.logW) + l;
+      double* pb = pa + (h << f.logW);
       const double a = *pa, b = *pb;
       *pa = a + b;
       *pb = a - b;
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int t = e / W, l = e % W;
-    col[base + (static_cast<int64_t>(t) << lo) + l] = tile[e];
+  if (f.to_sa) {  // lo == 0, W == 1: block [base, base + S)
+    const int64_t blk = base >> B;
+    for (int k = f.boff[blk] + threadIdx.x; k < f.boff[blk + 1]; k += blockDim.x)
+      f.sa[f.tslot[k] + c * f.m] = tile[f.tpos[k] - base] * f.scale;
+  } else {
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int t = e >> f.logW, l = e & (W - 1);
+      col[base + (static_cast<int64_t>(t) << f.lo) + l] = tile[e];
+    }
   }
 }
 
-__global__ void srht_gather(const double* __restrict__ x, int64_t npad, const int64_t* __restrict__ rows, int64_t m,
-                            int64_t d, double scale, double* __restrict__ sa) {
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < m * d;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = idx % m, c = idx / m;
-    sa[idx] = x[rows[r] + c * npad] * scale;
-  }
-}
-
-void launch_fwht(double* x, int64_t npad, int64_t d, int lo, int bits, cudaStream_t stream) {
+void launch_fwht(FwhtArgs f, int bits, cudaStream_t stream) {
   const int S = 1 << bits;
-  const int W = static_cast<int>(std::min<int64_t>(int64_t{1} << lo, std::max(1, 4096 / S)));
-  const int64_t blocks = d * (npad / (static_cast<int64_t>(S) * W));
-  const int smem = S * W * 8;
+  int logW = 0;
+  while (logW < f.lo && (S << (logW + 1)) <= 4096) ++logW;
+  f.logW = logW;
+  const int64_t blocks = f.d * (f.npad >> (bits + logW));
+  const int smem = (S << logW) * 8;
   auto go = [&](auto kern) {
     RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(x, npad, lo, W);
+    kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(f);
     RP_LAUNCH_CHECK();
   };
   switch (bits) {
+    case 0: go(fwht_pass<0>); break;
     case 1: go(fwht_pass<1>); break;
     case 2: go(fwht_pass<2>); break;
     case 3: go(fwht_pass<3>); break;
@@ -199,10 +221,6 @@ void launch_fwht(double* x, int64_t npad, int64_t d, int lo, int bits, cudaStrea
     case 6: go(fwht_pass<6>); break;
     case 7: go(fwht_pass<7>); break;
     case 8: go(fwht_pass<8>); break;
-    case 9: go(fwht_pass<9>); break;
-    case 10: go(fwht_pass<10>); break;
-    case 11: go(fwht_pass<11>); break;
-    case 12: go(fwht_pass<12>); break;
     default: throw InvalidArgument("fwht: pass width out of range");
   }
 }
@@ -346,28 +364,80 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       DBuf<double> signs(static_cast<size_t>(spec.n), stream);
       DBuf<int64_t> rows(static_cast<size_t>(m), stream);
       draw_srht(spec.seed, spec.n, m, signs.get(), rows.get(), stream);
+      // Pass plan: descending bit ranges of at most 8 bits, balanced (a
+      // single 0-bit pass when n_pad = 1).
+      std::vector<int> widths;
+      {
+        const int passes = std::max(1, (P + 7) / 8);
+        int rem = P;
+        for (int i = 0; i < passes; ++i) {
+          const int w = (rem + (passes - i) - 1) / (passes - i);
+          widths.push_back(w);
+          rem -= w;
+        }
+      }
+      const int last_bits = widths.back();
+      // Targets sorted by position, bucketed per block of the last pass.
+      std::vector<int64_t> hrows(static_cast<size_t>(m));
+      RP_CUDA(cudaMemcpyAsync(hrows.data(), rows.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToHost, stream));
+      RP_CUDA(cudaStreamSynchronize(stream));
+      std::vector<std::pair<int64_t, int32_t>> tg(static_cast<size_t>(m));
+      for (int64_t r = 0; r < m; ++r) tg[r] = {hrows[r], static_cast<int32_t>(r)};
+      std::sort(tg.begin(), tg.end());
+      const int64_t nblk = npad >> last_bits;
+      std::vector<int64_t> tpos(static_cast<size_t>(m));
+      std::vector<int32_t> meta(static_cast<size_t>(m + nblk + 1));
+      for (int64_t r = 0; r < m; ++r) {
+        tpos[r] = tg[r].first;
+        meta[r] = tg[r].second;
+      }
+      {
+        int64_t k = 0;
+        for (int64_t b = 0; b <= nblk; ++b) {
+          while (k < m && (tpos[k] >> last_bits) < b) ++k;
+          meta[m + b] = static_cast<int32_t>(k);
+        }
+      }
+      DBuf<int64_t> d_tpos(static_cast<size_t>(m), stream);
+      DBuf<int32_t> d_meta(meta.size(), stream);
+      RP_CUDA(cudaMemcpyAsync(d_tpos.get(), tpos.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, stream));
+      RP_CUDA(cudaMemcpyAsync(d_meta.get(), meta.data(), sizeof(int32_t) * meta.size(), cudaMemcpyHostToDevice,
+                              stream));
       DBuf<double> x(static_cast<size_t>(npad * d), stream);
-      if (!op.sparse) {
-        srht_load_dense<<<grid_for(npad * d), 256, 0, stream>>>(op.a, op.ld, op.trans, op.n_loc, op.row0, d,
-                                                                signs.get(), x.get(), npad);
-        RP_LAUNCH_CHECK();
-      } else {
+      FwhtArgs f{};
+      f.x = x.get();
+      f.npad = npad;
+      f.d = d;
+      f.signs = signs.get();
+      f.a = op.a;
+      f.lda = op.ld;
+      f.n_loc = op.n_loc;
+      f.row0 = op.row0;
+      f.trans = op.trans;
+      f.tpos = d_tpos.get();
+      f.tslot = d_meta.get();
+      f.boff = d_meta.get() + m;
+      f.scale = 1.0 / std::sqrt(static_cast<double>(m));
+      f.sa = d_sa;
+      f.m = m;
+      const bool first_from_op = !op.sparse;
+      if (op.sparse) {
         zero_fill<<<grid_for(npad * d), 256, 0, stream>>>(x.get(), npad, d, npad);
         RP_LAUNCH_CHECK();
         srht_scatter_csc<<<static_cast<unsigned>(d), 128, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, op.row0,
                                                                        d, signs.get(), x.get(), npad);
         RP_LAUNCH_CHECK();
       }
-      // Passes over descending bit ranges of at most 8 bits each.
       int hi = P;
-      while (hi > 0) {
-        const int bits = std::min(hi, 8);
-        launch_fwht(x.get(), npad, d, hi - bits, bits, stream);
+      for (size_t i = 0; i < widths.size(); ++i) {
+        const int bits = widths[i];
+        f.lo = hi - bits;
+        f.from_op = (i == 0) && first_from_op;
+        f.to_sa = (i + 1 == widths.size());
+        launch_fwht(f, bits, stream);
         hi -= bits;
       }
-      const double scale = 1.0 / std::sqrt(static_cast<double>(m));
-      srht_gather<<<grid_for(m * d), 256, 0, stream>>>(x.get(), npad, rows.get(), m, d, scale, d_sa);
-      RP_LAUNCH_CHECK();
+      RP_CUDA(cudaStreamSynchronize(stream));  // host target tables must outlive the copies
       return;
     }
   }

@@ -124,3 +124,24 @@ def test_preconditioner_matches_dense_inverse(rp, ctx, oracle):  # test_precondi
         assert v @ pre.apply(v) > 0
     with pytest.raises(ValueError):
         rp.Preconditioner.build(np.ones((2, 2)), 0.0, ctx=ctx)
+
+
+@pytest.mark.parametrize("n,d,k", [(100000, 64, 1), (70001, 200, 2), (8192, 1024, 4), (3000, 2048, 8),
+                                   (513, 33, 3), (40000, 16, 16)])
+def test_narrow_passes(rp, ctx, oracle, n, d, k):
+    """HBM-bound narrow kernels: A^T y (atv_narrow, k <= 16) and the fused
+    single-pass Gram A^T (A w) (k in {1,2,3,4,8}) vs float64 numpy."""
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, d))
+    y = rng.standard_normal((n, k))
+    w = rng.standard_normal((d, k))
+    assert oracle.rel_error(rp.apply_transpose(a, y, ctx=ctx), a.T @ y) < 1e-13
+    assert oracle.rel_error(rp.gram_apply(a, w, ctx=ctx), a.T @ (a @ w)) < 1e-13
+    # column stability (within one kernel family): each column alone gives the same bits
+    if k > 8:
+        return
+    g_all = rp.gram_apply(a, w, ctx=ctx)
+    t_all = rp.apply_transpose(a, y, ctx=ctx)
+    for j in range(k):
+        assert np.array_equal(rp.gram_apply(a, w[:, j].copy(), ctx=ctx), g_all[:, j])
+        assert np.array_equal(rp.apply_transpose(a, y[:, j].copy(), ctx=ctx), t_all[:, j])

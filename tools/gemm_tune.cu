@@ -1,0 +1,84 @@
+// GEMM tile/split tuner: times every tile shape of paper_2210_12212_b200's
+// DMMA GEMM on the shapes the IHS-BIN path issues.  Build + run on the GPU:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2210_12212_b200/csrc \
+//        tools/gemm_tune.cu -o gpurun_out/gemm_tune && gpurun_out/gemm_tune
+#include "../paper_2210_12212_b200/csrc/gemm_f64.cu"
+
+#include <cstdio>
+#include <vector>
+
+using namespace rpb;
+
+struct Shape {
+  const char* name;
+  Op opa, opb;
+  int64_t m, n, k, batch;
+  bool lower, col_stable;
+};
+
+int main() {
+  std::vector<Shape> shapes = {
+      {"GW g=1   (1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 1, false, true},
+      {"GW g=8   (1024x256x1024)", Op::N, Op::N, 1024, 256, 1024, 1, false, true},
+      {"GW g=32  (1024x1024x1024)", Op::N, Op::N, 1024, 1024, 1024, 1, false, true},
+      {"GW g=63  (1024x2016x1024)", Op::N, Op::N, 1024, 2016, 1024, 1, false, true},
+      {"P  g=1   32x(1024x2x1024)", Op::N, Op::N, 1024, 2, 1024, 32, false, true},
+      {"P  g=15  32x(1024x16x1024)", Op::N, Op::N, 1024, 16, 1024, 32, false, true},
+      {"P  g=31  32x(1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 32, false, true},
+      {"P  g=63  32x(1024x64x1024)", Op::N, Op::N, 1024, 64, 1024, 32, false, true},
+      {"SYRK A^T A (1024,65536)", Op::T, Op::N, 1024, 1024, 65536, 1, true, false},
+      {"square 4096^3", Op::N, Op::N, 4096, 4096, 4096, 1, false, false},
+      {"sketch S^T A 2048x1024x65536", Op::T, Op::N, 2048, 1024, 65536, 1, false, false},
+  };
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  size_t maxe = 0;
+  for (auto& sh : shapes)
+    maxe = std::max(maxe, (size_t)std::max({sh.m * sh.k * sh.batch, sh.k * sh.n * sh.batch, sh.m * sh.n * sh.batch}));
+  double *a, *b, *c;
+  cudaMalloc(&a, maxe * 8);
+  cudaMalloc(&b, maxe * 8);
+  cudaMalloc(&c, maxe * 8);
+  cudaMemset(a, 0, maxe * 8);
+  cudaMemset(b, 0, maxe * 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (auto& sh : shapes) {
+    printf("%-32s", sh.name);
+    for (int tile = -1; tile < 7; ++tile) {
+      GemmArgs g;
+      g.opa = sh.opa;
+      g.opb = sh.opb;
+      g.m = sh.m;
+      g.n = sh.n;
+      g.k = sh.k;
+      g.a = a;
+      g.lda = sh.opa == Op::N ? sh.m : sh.k;
+      g.stride_a = sh.m * sh.k;
+      g.b = b;
+      g.ldb = sh.opb == Op::N ? sh.k : sh.n;
+      g.stride_b = sh.k * sh.n;
+      g.c = c;
+      g.ldc = sh.m;
+      g.stride_c = sh.m * sh.n;
+      g.batch = sh.batch;
+      g.lower_only = sh.lower;
+      g.col_stable = sh.col_stable;
+      g.force_tile = tile;
+      for (int w = 0; w < 3; ++w) dgemm(g, s);
+      cudaEventRecord(e0, s);
+      const int iters = 10;
+      for (int it = 0; it < iters; ++it) dgemm(g, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double fl = 2.0 * sh.m * sh.n * sh.k * sh.batch * (sh.lower ? 0.5 : 1.0);
+      printf(" %s%6.1f", tile < 0 ? "auto:" : "", fl / (ms / iters * 1e-3) / 1e12);
+    }
+    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64]\n");
+  }
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
