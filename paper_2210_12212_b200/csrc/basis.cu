@@ -18,63 +18,64 @@ __device__ __forceinline__ double sum_partials(const Partials& P, int64_t b, int
   return v;
 }
 
+// Column-indexed grids: blockIdx.y = output column, threads over rows, so the
+// column bookkeeping (j, b, l, r) is done once per block, not per element.
 __global__ void build_args_kernel(BasisDims d, int64_t g, Partials y, const double* __restrict__ gen,
-                                  const double* __restrict__ tau, double* __restrict__ args) {
+                                  const double* __restrict__ tau, double* __restrict__ args, int64_t col0) {
   const int64_t nb = d.L * d.K;
-  const int64_t total = d.dim * (g + 1) * nb;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx % d.dim;
-    const int64_t col = idx / d.dim;  // = j*NB + b
-    const int64_t j = col / nb, b = col % nb;
-    const int64_t l = b / d.K, r = b % d.K;
+  const int64_t col = blockIdx.y + col0;  // = j*NB + b
+  const int64_t j = col / nb, b = col - j * nb;
+  const int64_t l = b / d.K, r = b - l * d.K;
+  const double tl = tau[l];
+  double* out = args + (l * d.kmax * d.K + j * d.K + r) * d.dim;
+  const double* prev = gen + ((j - 1) * nb + b) * d.dim;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double v;
     if (j < g) {
-      v = __dmul_rn(tau[l], sum_partials(y, 0, i, j * nb + b));
-      if (j >= 1) v = __dadd_rn(v, gen[i + ((j - 1) * nb + b) * d.dim]);
+      v = __dmul_rn(tl, sum_partials(y, 0, i, col));
+      if (j >= 1) v = __dadd_rn(v, prev[i]);
     } else {
       v = gen[i + ((g - 1) * nb + b) * d.dim];
     }
-    args[i + (l * d.kmax * d.K + j * d.K + r) * d.dim] = v;
+    out[i] = v;
   }
 }
 
 __global__ void update_kernel(BasisDims d, int64_t g, Partials applied, const int* __restrict__ kb,
-                              double* __restrict__ gen, double* __restrict__ tilde, int* __restrict__ flags) {
+                              double* __restrict__ gen, double* __restrict__ tilde, int* __restrict__ flags, int64_t col0) {
   const int64_t nb = d.L * d.K;
-  const int64_t total = d.dim * (g + 1) * nb;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx % d.dim;
-    const int64_t col = idx / d.dim;
-    const int64_t j = col / nb, b = col % nb;
-    const int64_t l = b / d.K, r = b % d.K;
-    if (g >= kb[l]) continue;  // this interval's loop has ended (path_solver.cpp:39)
+  const int64_t col = blockIdx.y + col0;
+  const int64_t j = col / nb, b = col - j * nb;
+  const int64_t l = b / d.K, r = b - l * d.K;
+  if (g >= kb[l]) return;  // this interval's loop has ended (path_solver.cpp:39)
+  double* gp = gen + col * d.dim;
+  double* tp = tilde + col * d.dim;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double a = sum_partials(applied, l, i, j * d.K + r);
-    double* gp = gen + i + col * d.dim;
-    const double v = (j < g) ? __dsub_rn(*gp, a) : -a;
-    *gp = v;
-    if (!isfinite(v)) flags[l] = 1;
-    double* tp = tilde + i + col * d.dim;
-    *tp = __dadd_rn(*tp, v);
+    const double v = (j < g) ? __dsub_rn(gp[i], a) : -a;
+    gp[i] = v;
+    bad |= !isfinite(v);
+    tp[i] = __dadd_rn(tp[i], v);
   }
+  if (bad) flags[l] = 1;
 }
 
 __global__ void compose_kernel(BasisDims d, const double* __restrict__ tilde, const double* __restrict__ tau,
                                const int* __restrict__ kb, const double* __restrict__ lambda,
-                               const int* __restrict__ interval, int64_t T, double* __restrict__ x) {
+                               const int* __restrict__ interval, int64_t T, double* __restrict__ x, int64_t col0) {
   const int64_t nb = d.L * d.K;
-  const int64_t total = d.dim * d.K * T;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx % d.dim;
-    const int64_t col = idx / d.dim;  // t*K + r
-    const int64_t t = col / d.K, r = col % d.K;
-    const int l = interval[t];
-    const int64_t b = l * d.K + r;
-    const double ta = tau[l];
-    const double tt = __dmul_rn(ta, lambda[t]);
-    const int k = kb[l];
+  const int64_t col = blockIdx.y + col0;  // t*K + r
+  const int64_t t = col / d.K, r = col - t * d.K;
+  const int l = interval[t];
+  const int64_t b = l * d.K + r;
+  const double ta = tau[l];
+  const double tt = __dmul_rn(ta, lambda[t]);
+  const int k = kb[l];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double v = tilde[i + ((k - 1) * nb + b) * d.dim];
     for (int j = k - 2; j >= 0; --j) v = __dadd_rn(tilde[i + (j * nb + b) * d.dim], __dmul_rn(tt, v));
     x[i + col * d.dim] = __dmul_rn(v, ta);
@@ -142,23 +143,37 @@ __global__ void fill_kernel(double* __restrict__ dst, int64_t count, double v) {
 
 }  // namespace
 
+// Launches `launch(grid, col0)` over column chunks of at most 65535 (grid.y limit).
+template <class F>
+void for_col_chunks(int64_t rows, int64_t cols, F launch) {
+  const unsigned gx = static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 256), 64));
+  for (int64_t c0 = 0; c0 < cols; c0 += 65535) {
+    const int64_t cn = std::min<int64_t>(65535, cols - c0);
+    launch(dim3(gx, static_cast<unsigned>(cn)), c0);
+    RP_LAUNCH_CHECK();
+  }
+}
+
 void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* gen, const double* d_tau,
                 double* args_im, cudaStream_t stream) {
-  build_args_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, y, gen, d_tau, args_im);
-  RP_LAUNCH_CHECK();
+  for_col_chunks(d.dim, (g + 1) * d.nb(), [&](dim3 grid, int64_t c0) {
+    build_args_kernel<<<grid, 256, 0, stream>>>(d, g, y, gen, d_tau, args_im, c0);
+  });
 }
 
 void update_gen(const BasisDims& d, int64_t g, const Partials& applied, const int* d_k, double* gen, double* tilde,
                 int* d_flags, cudaStream_t stream) {
-  update_kernel<<<grid_for(d.dim * (g + 1) * d.nb()), 256, 0, stream>>>(d, g, applied, d_k, gen, tilde, d_flags);
-  RP_LAUNCH_CHECK();
+  for_col_chunks(d.dim, (g + 1) * d.nb(), [&](dim3 grid, int64_t c0) {
+    update_kernel<<<grid, 256, 0, stream>>>(d, g, applied, d_k, gen, tilde, d_flags, c0);
+  });
 }
 
 void compose(const BasisDims& d, const double* tilde, const double* d_tau, const int* d_k, const double* d_lambda,
              const int* d_interval, int64_t T, double* x, cudaStream_t stream) {
   if (T <= 0) return;
-  compose_kernel<<<grid_for(d.dim * d.K * T), 256, 0, stream>>>(d, tilde, d_tau, d_k, d_lambda, d_interval, T, x);
-  RP_LAUNCH_CHECK();
+  for_col_chunks(d.dim, d.K * T, [&](dim3 grid, int64_t c0) {
+    compose_kernel<<<grid, 256, 0, stream>>>(d, tilde, d_tau, d_k, d_lambda, d_interval, T, x, c0);
+  });
 }
 
 void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,

@@ -380,6 +380,22 @@ __global__ void srht_prep_kernel(const uint64_t* __restrict__ words, int64_t n, 
   }
 }
 
+// npad <= 65536: the whole pool as uint16 in shared memory (2 loads + 2 stores
+// per pick instead of hash probes).
+__global__ void srht_swap_small_kernel(const int64_t* __restrict__ jv, int64_t m, int64_t npad, int64_t* rows) {
+  extern __shared__ uint16_t pool16[];
+  for (int64_t i = threadIdx.x; i < npad; i += blockDim.x) pool16[i] = static_cast<uint16_t>(i);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t j = jv[i];
+    const uint16_t vi = pool16[i], vj = pool16[j];
+    pool16[i] = vj;
+    pool16[j] = vi;
+    rows[i] = vj;
+  }
+}
+
 template <int CAP, bool SMEM>
 __global__ void srht_swap_kernel(const int64_t* __restrict__ jv, int64_t m, int64_t* rows, int64_t* gkeys,
                                  int64_t* gvals) {
@@ -577,6 +593,14 @@ void draw_srht(uint64_t seed, int64_t n, int64_t m, double* d_signs, int64_t* d_
   int hflag = 0;
   RP_CUDA(cudaMemcpyAsync(&hflag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
   RP_CUDA(cudaStreamSynchronize(stream));
+  if (!hflag && npad <= 65536) {
+    const int bytes = static_cast<int>(npad * sizeof(uint16_t));
+    RP_CUDA(cudaFuncSetAttribute(srht_swap_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    srht_swap_small_kernel<<<1, 256, bytes, stream>>>(jv.get(), m, npad, d_rows);
+    RP_LAUNCH_CHECK();
+    RP_CUDA(cudaStreamSynchronize(stream));
+    return;
+  }
   auto go = [&](auto seq_kern, auto swap_kern, bool smem) {
     const int bytes = smem ? static_cast<int>(2 * cap * sizeof(int64_t)) : 0;
     if (!hflag) {

@@ -13,22 +13,22 @@ namespace {
 
 constexpr int NB = 64;
 
-// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix:
-// one warp per matrix, lane l owns rows l and l + 32 (no block barriers).  The
-// finished column j is copied to a separate array so the trailing update's
-// loads never alias its stores (lets the compiler pipeline the loop).
-__global__ void __launch_bounds__(32) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
-                                                 int* info) {
+// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix.
+// 256 threads: thread t owns row r = t % 64 and the columns c = t / 64 (mod 4)
+// of the trailing update; every thread recomputes the pivot (no broadcast
+// barrier), two barriers per column.
+__global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
+                                                  int* info) {
   __shared__ double T[NB][NB + 1];
-  __shared__ double colj[NB];
   double* A = h + blockIdx.x * stride + k0 + k0 * ld;
-  const int lane = threadIdx.x;
-#pragma unroll 8
-  for (int j = 0; j < kb; ++j) {
-    if (lane < kb) T[lane][j] = A[lane + j * ld];
-    if (lane + 32 < kb) T[lane + 32][j] = A[lane + 32 + j * ld];
+  const int r = threadIdx.x & (NB - 1);
+  const int part = threadIdx.x >> 6;  // 0..3
+#pragma unroll
+  for (int jj = 0; jj < NB / 4; ++jj) {
+    const int j = part + 4 * jj;
+    if (j < kb && r < kb) T[r][j] = A[r + j * ld];
   }
-  __syncwarp();
+  __syncthreads();
   int bad = 0;
   for (int j = 0; j < kb; ++j) {
     double d = T[j][j];
@@ -37,47 +37,26 @@ __global__ void __launch_bounds__(32) potrf_diag(double* h, int64_t ld, int64_t 
       d = 1.0;  // keep going; the caller reports the failure
     }
     const double piv = sqrt(d);
-    const double inv = 1.0 / piv;
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int r = lane + 32 * h2;
-      if (r >= j && r < kb) {
-        const double v = (r == j) ? piv : T[r][j] * inv;
-        T[r][j] = v;
-        colj[r] = v;
-      }
+    if (part == 0 && r >= j && r < kb) T[r][j] = (r == j) ? piv : T[r][j] / piv;
+    __syncthreads();
+    if (r > j && r < kb) {
+      const double lrj = T[r][j];
+      const int c0 = j + 1 + ((part - (j + 1)) & 3);  // first c > j with c % 4 == part
+      for (int c = c0; c <= r; c += 4) T[r][c] -= lrj * T[c][j];
     }
-    __syncwarp();
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int r = lane + 32 * h2;
-      if (r > j && r < kb) {
-        const double lrj = colj[r];
-        double* row = &T[r][0];
-        int c = j + 1;
-        for (; c + 3 <= r; c += 4) {
-          const double c0 = colj[c], c1 = colj[c + 1], c2 = colj[c + 2], c3 = colj[c + 3];
-          const double t0 = row[c], t1 = row[c + 1], t2 = row[c + 2], t3 = row[c + 3];
-          row[c] = t0 - lrj * c0;
-          row[c + 1] = t1 - lrj * c1;
-          row[c + 2] = t2 - lrj * c2;
-          row[c + 3] = t3 - lrj * c3;
-        }
-        for (; c <= r; ++c) row[c] -= lrj * colj[c];
-      }
-    }
-    __syncwarp();
+    __syncthreads();
   }
-  if (bad && lane == 0 && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
-#pragma unroll 8
-  for (int j = 0; j < kb; ++j) {
-    if (lane < kb && lane >= j) A[lane + j * ld] = T[lane][j];
-    if (lane + 32 < kb && lane + 32 >= j) A[lane + 32 + j * ld] = T[lane + 32][j];
+  if (bad && threadIdx.x == 0 && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
+#pragma unroll
+  for (int jj = 0; jj < NB / 4; ++jj) {
+    const int j = part + 4 * jj;
+    if (j < kb && r < kb && r >= j) A[r + j * ld] = T[r][j];
   }
 }
 
-// Panel solve X * L11^T = B for the rows below the diagonal block; one thread
-// per row, 128 rows per CTA; four independent partial sums per dot product.
+// Panel solve X * L11^T = B for the rows below the diagonal block.  Four
+// threads per row (32 rows per CTA) split every dot product and combine it
+// with two shuffles.
 __global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
                                                   int64_t rows) {
   extern __shared__ double dsm[];
@@ -86,34 +65,37 @@ __global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t
   double* base = h + blockIdx.y * stride;
   const double* L11 = base + k0 + k0 * ld;
   const int t = threadIdx.x;
-#pragma unroll 8
-  for (int j = 0; j < kb; ++j)
-    if (t < kb) L[t][j] = L11[t + j * ld];
-  const int64_t r0 = k0 + kb + static_cast<int64_t>(blockIdx.x) * 128;
-  const int nr = static_cast<int>((k0 + kb + rows - r0) < 128 ? (k0 + kb + rows - r0) : 128);
+#pragma unroll
+  for (int jj = 0; jj < NB / 2; ++jj) {
+    const int j = (t >> 6) + 2 * jj;
+    if (j < kb && (t & 63) < kb) L[t & 63][j] = L11[(t & 63) + j * ld];
+  }
+  const int64_t r0 = k0 + kb + static_cast<int64_t>(blockIdx.x) * 32;
+  const int nr = static_cast<int>((k0 + kb + rows - r0) < 32 ? (k0 + kb + rows - r0) : 32);
   double* B = base + k0 * ld;  // column k0 of the matrix
-#pragma unroll 8
-  for (int j = 0; j < kb; ++j)
-    if (t < nr) X[t][j] = B[r0 + t + j * ld];
-  __syncthreads();
-  if (t < nr) {
-    for (int j = 0; j < kb; ++j) {
-      double s0 = X[t][j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int i = 0;
-      for (; i + 3 < j; i += 4) {
-        s0 -= X[t][i] * L[j][i];
-        s1 -= X[t][i + 1] * L[j][i + 1];
-        s2 -= X[t][i + 2] * L[j][i + 2];
-        s3 -= X[t][i + 3] * L[j][i + 3];
-      }
-      for (; i < j; ++i) s0 -= X[t][i] * L[j][i];
-      X[t][j] = ((s0 + s1) + (s2 + s3)) / L[j][j];
-    }
+#pragma unroll
+  for (int jj = 0; jj < NB / 4; ++jj) {
+    const int j = (t >> 5) + 4 * jj;
+    if (j < kb && (t & 31) < nr) X[t & 31][j] = B[r0 + (t & 31) + j * ld];
   }
   __syncthreads();
-#pragma unroll 8
-  for (int j = 0; j < kb; ++j)
-    if (t < nr) B[r0 + t + j * ld] = X[t][j];
+  // all 32 rows run the recurrence (rows >= nr compute on unused smem) so the
+  // shuffles always see full warps
+  const int row = t >> 2, q = t & 3;
+  for (int j = 0; j < kb; ++j) {
+    double s = 0.0;
+    for (int i = q; i < j; i += 4) s += X[row][i] * L[j][i];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q == 0) X[row][j] = (X[row][j] - s) / L[j][j];
+    __syncwarp();
+  }
+  __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < NB / 4; ++jj) {
+    const int j = (t >> 5) + 4 * jj;
+    if (j < kb && (t & 31) < nr) B[r0 + (t & 31) + j * ld] = X[t & 31][j];
+  }
 }
 
 // In-place inverse of each nb x nb lower-triangular diagonal block; zeroes the
@@ -127,9 +109,9 @@ __global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t l
   double* A = h + blockIdx.y * stride + k0 + k0 * ld;
   {
     const int i = threadIdx.x;
-#pragma unroll 8
-    for (int j = 0; j < kb; ++j)
-      if (i < kb) L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < kb && i < kb) L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
   }
   __syncthreads();
   const int c = threadIdx.x;
@@ -152,9 +134,9 @@ __global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t l
   __syncthreads();
   {
     const int i = threadIdx.x;
-#pragma unroll 8
-    for (int j = 0; j < kb; ++j)
-      if (i < kb) A[i + j * ld] = X[i][j];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < kb && i < kb) A[i + j * ld] = X[i][j];
   }
 }
 
@@ -199,12 +181,12 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // 1) Cholesky, lower.
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
-    potrf_diag<<<static_cast<unsigned>(batch), 32, 0, stream>>>(h, ld, stride, k0, kb, info.get());
+    potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
     RP_LAUNCH_CHECK();
     const int64_t rows = n - k0 - kb;
     if (rows <= 0) break;
-    dim3 tg(static_cast<unsigned>(ceil_div(rows, 128)), static_cast<unsigned>(batch));
-    constexpr int kTrsmSmem = (NB + 128) * (NB + 1) * 8;
+    dim3 tg(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(batch));
+    constexpr int kTrsmSmem = (NB + 32) * (NB + 1) * 8;
     static bool attr = false;
     if (!attr) {
       RP_CUDA(cudaFuncSetAttribute(potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));

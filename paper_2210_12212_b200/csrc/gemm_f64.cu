@@ -427,8 +427,8 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
       // a function of k only (and of m for long k): every column of C sees the
       // same reduction order whatever n is
       const int64_t tiles_m = ceil_div(g.m, 128) * nb;
-      // (k <= 8192: chunks of 128 -- cheap when the consumer sums the partials)
-      split = g.k <= 8192 ? static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, g.k / 128)))
+      // (k <= 8192: chunks of 256 -- cheap when the consumer sums the partials)
+      split = g.k <= 8192 ? static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, g.k / 256)))
                           : static_cast<int>(std::min<int64_t>(cap, ceil_div(2 * 148, std::max<int64_t>(tiles_m, 1))));
       if (g.k < 256) split = 1;
     } else {

@@ -128,7 +128,7 @@ __global__ void srht_scatter_csc(const int64_t* __restrict__ coff, const int32_t
 struct FwhtArgs {
   double* x;  // scratch, npad x d
   int64_t npad, d;
-  int lo, logW;
+  int lo, logW, logG;
   bool from_op;
   const double* a;
   int64_t lda, n_loc, row0;
@@ -146,56 +146,70 @@ struct FwhtArgs {
 template <int B>
 __global__ void __launch_bounds__(256) fwht_pass(FwhtArgs f) {
   constexpr int S = 1 << B;
-  extern __shared__ double tile[];  // [S][W]
+  extern __shared__ double tile[];  // lo > 0: [S][W];  lo == 0: [G][S] (G consecutive groups)
   const int W = 1 << f.logW;
-  const int64_t groups_per_col = f.npad >> (B + f.logW);
+  const int G = f.lo == 0 ? (1 << f.logG) : 1;
+  const int64_t groups_per_col = f.npad >> (B + f.logW + (f.lo == 0 ? f.logG : 0));
   const int64_t c = blockIdx.x / groups_per_col;
   const int64_t gidx = blockIdx.x - c * groups_per_col;
-  const int64_t wblocks = int64_t{1} << (f.lo - f.logW);
-  const int64_t hi_part = gidx >> (f.lo - f.logW);
-  const int64_t l0 = (gidx & (wblocks - 1)) << f.logW;
-  const int64_t base = (hi_part << (B + f.lo)) + l0;
-  const int total = S << f.logW;
+  int64_t base;
+  if (f.lo == 0) {
+    base = gidx << (B + f.logG);
+  } else {
+    const int64_t wblocks = int64_t{1} << (f.lo - f.logW);
+    const int64_t hi_part = gidx >> (f.lo - f.logW);
+    const int64_t l0 = (gidx & (wblocks - 1)) << f.logW;
+    base = (hi_part << (B + f.lo)) + l0;
+  }
+  const int total = (S << f.logW) * G;
   double* col = f.x + c * f.npad;
+  // element e of the tile -> global index (contiguous when lo == 0)
+  auto gindex = [&](int e) -> int64_t {
+    if (f.lo == 0) return base + e;
+    const int t = e >> f.logW, l = e & (W - 1);
+    return base + (static_cast<int64_t>(t) << f.lo) + l;
+  };
   if (f.from_op) {
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int t = e >> f.logW, l = e & (W - 1);
-      const int64_t i = base + (static_cast<int64_t>(t) << f.lo) + l;
+      const int64_t i = gindex(e);
       const int64_t li = i - f.row0;
       double v = 0.0;
       if (li >= 0 && li < f.n_loc) v = f.signs[i] * (f.trans ? f.a[c + li * f.lda] : f.a[li + c * f.lda]);
       tile[e] = v;
     }
   } else {
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int t = e >> f.logW, l = e & (W - 1);
-      tile[e] = col[base + (static_cast<int64_t>(t) << f.lo) + l];
-    }
+    for (int e = threadIdx.x; e < total; e += blockDim.x) tile[e] = col[gindex(e)];
   }
   __syncthreads();
 #pragma unroll 1
   for (int lh = B - 1; lh >= 0; --lh) {
     const int h = 1 << lh;
     for (int e = threadIdx.x; e < (total >> 1); e += blockDim.x) {
-      const int pair = e >> f.logW, l = e & (W - 1);
-      const int t = ((pair >> lh) << (lh + 1)) + (pair & (h - 1));
-      double* pa = tile + (t << f.logW) + l;
-      double* pb = pa + (h << f.logW);
+      double* pa;
+      int step;
+      if (f.lo == 0) {  // e -> (group, pair within group)
+        const int grp = e >> (B - 1), pp = e & ((S >> 1) - 1);
+        pa = tile + (grp << B) + ((pp >> lh) << (lh + 1)) + (pp & (h - 1));
+        step = h;
+      } else {
+        const int pair = e >> f.logW, l = e & (W - 1);
+        const int t = ((pair >> lh) << (lh + 1)) + (pair & (h - 1));
+        pa = tile + (t << f.logW) + l;
+        step = h << f.logW;
+      }
+      double* pb = pa + step;
       const double a = *pa, b = *pb;
       *pa = a + b;
       *pb = a - b;
     }
     __syncthreads();
   }
-  if (f.to_sa) {  // lo == 0, W == 1: block [base, base + S)
-    const int64_t blk = base >> B;
-    for (int k = f.boff[blk] + threadIdx.x; k < f.boff[blk + 1]; k += blockDim.x)
+  if (f.to_sa) {  // lo == 0: blocks [base + g*S, base + (g+1)*S)
+    const int64_t blk0 = base >> B;
+    for (int k = f.boff[blk0] + threadIdx.x; k < f.boff[blk0 + G]; k += blockDim.x)
       f.sa[f.tslot[k] + c * f.m] = tile[f.tpos[k] - base] * f.scale;
   } else {
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int t = e >> f.logW, l = e & (W - 1);
-      col[base + (static_cast<int64_t>(t) << f.lo) + l] = tile[e];
-    }
+    for (int e = threadIdx.x; e < total; e += blockDim.x) col[gindex(e)] = tile[e];
   }
 }
 
@@ -203,9 +217,13 @@ void launch_fwht(FwhtArgs f, int bits, cudaStream_t stream) {
   const int S = 1 << bits;
   int logW = 0;
   while (logW < f.lo && (S << (logW + 1)) <= 4096) ++logW;
+  int logG = 0;  // lo == 0: consecutive groups per CTA
+  if (f.lo == 0)
+    while ((S << (logG + 1)) <= 4096 && (int64_t{S} << (logG + 1)) <= f.npad) ++logG;
   f.logW = logW;
-  const int64_t blocks = f.d * (f.npad >> (bits + logW));
-  const int smem = (S << logW) * 8;
+  f.logG = logG;
+  const int64_t blocks = f.d * (f.npad >> (bits + logW + logG));
+  const int smem = (S << (logW + logG)) * 8;
   auto go = [&](auto kern) {
     RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(f);
