@@ -301,6 +301,36 @@ def run_ours(args, w):
                                "MEASURED_PEAKS.json has no FP64 figure; DMMA issue peak measured 37.1 TFLOP/s "
                                "(profiles/fp64_peaks_r01.txt)"}
 
+    # HBM-bound single passes over A (north_star: the fused Gram-matvec pass
+    # A^T (A w) against the HBM roofline), timed with CUDA events on the stream.
+    passes = {}
+    if world == 1:
+        hbm = 6449.1
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                hbm = float(json.load(f).get("hbm_gbs", hbm))
+        except Exception:
+            pass
+        for name, fn, wcols in (("gram_fused_w1", rp.gram_apply_raw, 1), ("gram_fused_w4", rp.gram_apply_raw, 4),
+                                ("atb_w1", rp.apply_transpose_raw, 1)):
+            rows_in = d if fn is rp.gram_apply_raw else nl
+            xin = torch.randn(rows_in * wcols, dtype=torch.float64, device=dev)
+            xout = torch.empty(d * wcols, dtype=torch.float64, device=dev)
+            for _ in range(2):
+                fn(ctx, xin.data_ptr(), wcols, xout.data_ptr())
+            torch.cuda.synchronize(dev)
+            reps = 10
+            p0, p1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            p0.record(stream)
+            for _ in range(reps):
+                fn(ctx, xin.data_ptr(), wcols, xout.data_ptr())
+            p1.record(stream)
+            torch.cuda.synchronize(dev)
+            t = p0.elapsed_time(p1) * 1e-3 / reps
+            byts = 8.0 * nl * d
+            passes[name] = {"seconds": t, "algorithmic_bytes": byts, "achieved_gbs": byts / t / 1e9,
+                            "frac_hbm": byts / t / 1e9 / hbm}
+
     # e2e through the public API with host buffers: pinned A and b copied in,
     # x copied out, every step.
     e2e = None
@@ -344,7 +374,8 @@ def run_ours(args, w):
                            "parallelism": f"row-sharded x{world}, NCCL all-reduce, intervals split" if world > 1
                            else "single GPU",
                            "phases_s": phases},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "roofline": roofline, "hbm_passes": passes or None, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk,
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -16,6 +16,7 @@
 #include "common.h"
 #include "draws.h"
 #include "mt_device.cuh"
+#include "glibc_libm.cuh"
 
 namespace rpb {
 namespace mt {
@@ -491,14 +492,22 @@ namespace {
 
 // Box-Muller exactly as SeededRng::normal (rng.hpp:43-55): u1, u2 from two
 // consecutive words, r = sqrt(-2 log u1), cos first, sin second.
+// log / sin / cos are glibc's own algorithms and tables (glibc_libm.cuh), so
+// the entries equal the reference's bit for bit; without the extracted tables
+// (RP_GLIBC_EXACT 0) CUDA's libm is used and entries agree to ~1 ulp.
 __device__ __forceinline__ void box_muller(uint64_t w1, uint64_t w2, double& c, double& s) {
   const double u1 = d_uniform01(w1);
   const double u2 = d_uniform01(w2);
-  const double r = sqrt(__dmul_rn(-2.0, log(u1)));
   const double two_pi = 6.283185307179586476925286766559;
   const double th = __dmul_rn(two_pi, u2);
+#if RP_GLIBC_EXACT
+  const double r = __dsqrt_rn(__dmul_rn(-2.0, glibc::log(u1)));
+  const double cv = glibc::cos(th), sv = glibc::sin(th);
+#else
+  const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
   double sv, cv;
   sincos(th, &sv, &cv);
+#endif
   c = __dmul_rn(r, cv);
   s = __dmul_rn(r, sv);
 }

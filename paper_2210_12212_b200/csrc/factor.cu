@@ -47,105 +47,35 @@ __global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t
     __syncthreads();
   }
   if (bad && threadIdx.x == 0 && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
-#pragma unroll
-  for (int jj = 0; jj < NB / 4; ++jj) {
-    const int j = part + 4 * jj;
-    if (j < kb && r < kb && r >= j) A[r + j * ld] = T[r][j];
-  }
-}
-
-// Panel solve X * L11^T = B for the rows below the diagonal block.  Four
-// threads per row (32 rows per CTA) split every dot product and combine it
-// with two shuffles.
-__global__ void __launch_bounds__(128) potrf_trsm(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
-                                                  int64_t rows) {
-  extern __shared__ double dsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  double* base = h + blockIdx.y * stride;
-  const double* L11 = base + k0 + k0 * ld;
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int jj = 0; jj < NB / 2; ++jj) {
-    const int j = (t >> 6) + 2 * jj;
-    if (j < kb && (t & 63) < kb) L[t & 63][j] = L11[(t & 63) + j * ld];
-  }
-  const int64_t r0 = k0 + kb + static_cast<int64_t>(blockIdx.x) * 32;
-  const int nr = static_cast<int>((k0 + kb + rows - r0) < 32 ? (k0 + kb + rows - r0) : 32);
-  double* B = base + k0 * ld;  // column k0 of the matrix
-#pragma unroll
-  for (int jj = 0; jj < NB / 4; ++jj) {
-    const int j = (t >> 5) + 4 * jj;
-    if (j < kb && (t & 31) < nr) X[t & 31][j] = B[r0 + (t & 31) + j * ld];
-  }
-  __syncthreads();
-  // all 32 rows run the recurrence (rows >= nr compute on unused smem) so the
-  // shuffles always see full warps
-  const int row = t >> 2, q = t & 3;
-  for (int j = 0; j < kb; ++j) {
-    double s = 0.0;
-    for (int i = q; i < j; i += 4) s += X[row][i] * L[j][i];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q == 0) X[row][j] = (X[row][j] - s) / L[j][j];
-    __syncwarp();
-  }
-  __syncthreads();
-#pragma unroll
-  for (int jj = 0; jj < NB / 4; ++jj) {
-    const int j = (t >> 5) + 4 * jj;
-    if (j < kb && (t & 31) < nr) B[r0 + (t & 31) + j * ld] = X[t & 31][j];
-  }
-}
-
-// In-place inverse of each nb x nb lower-triangular diagonal block; zeroes the
-// strict upper triangle of the whole matrix on the way.
-__global__ void __launch_bounds__(64) trtri_diag(double* h, int64_t n, int64_t ld, int64_t stride) {
-  extern __shared__ double dsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * NB;
-  const int kb = static_cast<int>((n - k0) < NB ? (n - k0) : NB);
-  double* A = h + blockIdx.y * stride + k0 + k0 * ld;
+  // L11^{-1} by columns: four threads per column c split each dot product
+  // X[i][c] = -(sum_{k=c}^{i-1} L[i][k] X[k][c]) / L[i][i].  X (lower) is kept
+  // transposed in the unused strict upper triangle of T (X[i][c] at T[c][i]),
+  // its diagonal in xd.
+  __shared__ double xd[NB];
   {
-    const int i = threadIdx.x;
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (j < kb && i < kb) L[i][j] = (i >= j) ? A[i + j * ld] : 0.0;
-  }
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (c < kb) {
-    X[c][c] = 1.0 / L[c][c];
-    for (int i = 0; i < c; ++i) X[i][c] = 0.0;
-    for (int i = c + 1; i < kb; ++i) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = c;
-      for (; k + 3 < i; k += 4) {
-        s0 += L[i][k] * X[k][c];
-        s1 += L[i][k + 1] * X[k + 1][c];
-        s2 += L[i][k + 2] * X[k + 2][c];
-        s3 += L[i][k + 3] * X[k + 3][c];
-      }
-      for (; k < i; ++k) s0 += L[i][k] * X[k][c];
-      X[i][c] = -((s0 + s1) + (s2 + s3)) / L[i][i];
+    const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+    const bool live = c < kb;
+    const double xcc = live ? 1.0 / T[c][c] : 0.0;
+    if (live && q == 0) xd[c] = xcc;
+    // uniform trip count across the warp (the shuffles need every lane)
+    for (int i = 1; i < NB; ++i) {
+      const bool act = live && i > c && i < kb;
+      double sum = 0.0;
+      if (act)
+        for (int k = c + q; k < i; k += 4) sum += T[i][k] * (k == c ? xcc : T[c][k]);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (act && q == 0) T[c][i] = -sum / T[i][i];
+      __syncwarp();
     }
   }
   __syncthreads();
-  {
-    const int i = threadIdx.x;
+  // the diagonal block now holds L11^{-1} (zero above the diagonal): the
+  // panel solve becomes a GEMM and the later triangular inverse starts from it
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (j < kb && i < kb) A[i + j * ld] = X[i][j];
-  }
-}
-
-__global__ void zero_upper(double* h, int64_t n, int64_t ld, int64_t stride) {
-  double* A = h + blockIdx.y * stride;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n * n;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx % n, j = idx / n;
-    if (i < j) A[i + j * ld] = 0.0;
+  for (int jj = 0; jj < NB / 4; ++jj) {
+    const int j = part + 4 * jj;
+    if (j < kb && r < kb) A[r + j * ld] = (r > j) ? T[j][r] : (r == j ? xd[r] : 0.0);
   }
 }
 
@@ -185,15 +115,30 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     RP_LAUNCH_CHECK();
     const int64_t rows = n - k0 - kb;
     if (rows <= 0) break;
-    dim3 tg(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(batch));
-    constexpr int kTrsmSmem = (NB + 32) * (NB + 1) * 8;
-    static bool attr = false;
-    if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-      attr = true;
+    {
+      // Panel: A21 <- A21 * L11^{-T}.  In place is safe: N = kb <= 64 fits one
+      // 128x64 tile, so each CTA owns whole rows and reads its full A tile
+      // before the epilogue writes them.
+      GemmArgs t;
+      t.opa = Op::N;
+      t.opb = Op::T;
+      t.m = rows;
+      t.n = kb;
+      t.k = kb;
+      t.a = h + (k0 + kb) + k0 * ld;
+      t.lda = ld;
+      t.stride_a = stride;
+      t.b = h + k0 + k0 * ld;  // L11^{-1}
+      t.ldb = ld;
+      t.stride_b = stride;
+      t.c = h + (k0 + kb) + k0 * ld;
+      t.ldc = ld;
+      t.stride_c = stride;
+      t.batch = batch;
+      t.split_k = 1;
+      t.force_tile = 6;  // 128 x 64
+      dgemm(t, stream);
     }
-    potrf_trsm<<<tg, 128, kTrsmSmem, stream>>>(h, ld, stride, k0, kb, rows);
-    RP_LAUNCH_CHECK();
     GemmArgs g;  // A22 -= A21 A21^T (lower)
     g.opa = Op::N;
     g.opb = Op::T;
@@ -220,15 +165,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   {
     // (the strict upper triangle is already zero: shifted_copies writes it so
     // and potrf only touches the lower triangle)
-    dim3 dg(static_cast<unsigned>(ceil_div(n, NB)), static_cast<unsigned>(batch));
-    constexpr int kDiagSmem = 2 * NB * (NB + 1) * 8;
-    static bool attr = false;
-    if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(trtri_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem));
-      attr = true;
-    }
-    trtri_diag<<<dg, 64, kDiagSmem, stream>>>(h, n, ld, stride);
-    RP_LAUNCH_CHECK();
+    // (the diagonal blocks already hold their inverses, written by potrf_diag)
     DBuf<double> tmp;
     for (int64_t s = NB; s < n; s *= 2) {
       const int64_t pairs_full = n / (2 * s);

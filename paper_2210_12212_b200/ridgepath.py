@@ -762,3 +762,13 @@ def path_raw(ctx: Context, b_ptr: int, K: int, config: PathConfig, spec: SketchS
                  ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, _P(x_ptr), where, ctypes.byref(tm)))
     del keep
     return tm
+
+
+def gram_apply_raw(ctx: Context, x_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
+    """rp_gram_apply on raw pointers: out = A^T (A x) for the context's operator."""
+    ctx.check(lib().rp_gram_apply(ctx.handle, _P(x_ptr), ncols, _P(out_ptr), where))
+
+
+def apply_transpose_raw(ctx: Context, y_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
+    """rp_apply_transpose on raw pointers: out = A^T y."""
+    ctx.check(lib().rp_apply_transpose(ctx.handle, _P(y_ptr), ncols, _P(out_ptr), where))
