@@ -63,6 +63,16 @@ __global__ void update_kernel(BasisDims d, int64_t g, Partials applied, const in
   if (bad) flags[l] = 1;
 }
 
+__global__ void seed_args_kernel(BasisDims d, const double* __restrict__ gen, double* __restrict__ args, int64_t col0) {
+  const int64_t b = blockIdx.y + col0;  // problem
+  const int64_t l = b / d.K, r = b - l * d.K;
+  double* out = args + (l * d.kmax * d.K + d.K + r) * d.dim;
+  const double* src = gen + b * d.dim;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = src[i];
+}
+
 __global__ void compose_kernel(BasisDims d, const double* __restrict__ tilde, const double* __restrict__ tau,
                                const int* __restrict__ kb, const double* __restrict__ lambda,
                                const int* __restrict__ interval, int64_t T, double* __restrict__ x, int64_t col0) {
@@ -158,6 +168,13 @@ void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* 
                 double* args_im, cudaStream_t stream) {
   for_col_chunks(d.dim, (g + 1) * d.nb(), [&](dim3 grid, int64_t c0) {
     build_args_kernel<<<grid, 256, 0, stream>>>(d, g, y, gen, d_tau, args_im, c0);
+  });
+}
+
+void seed_args(const BasisDims& d, const double* gen, double* args_im, cudaStream_t stream) {
+  if (d.kmax < 2) return;
+  for_col_chunks(d.dim, d.nb(), [&](dim3 grid, int64_t c0) {
+    seed_args_kernel<<<grid, 256, 0, stream>>>(d, gen, args_im, c0);
   });
 }
 

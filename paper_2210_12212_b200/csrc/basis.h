@@ -32,6 +32,10 @@ struct BasisDims {
 void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* gen, const double* d_tau,
                 double* args_im, cudaStream_t stream);
 
+// args_im[l][:, K + r] = gen[:, b] (the generation-1 argument column; the
+// fused recursion epilogue writes the later ones, see gemm_f64.h).
+void seed_args(const BasisDims& d, const double* gen, double* args_im, cudaStream_t stream);
+
 // gen[:, j*NB+b] -= applied[l][:, j*K+r] (j < g); gen[:, g*NB+b] = -applied[l][:, g*K+r];
 // flags[l] |= any non-finite in gen[:, 0..g]; tilde[:, j*NB+b] += gen[:, j*NB+b] (j <= g).
 // Problems whose interval has k_l <= g are left untouched.

@@ -13,69 +13,90 @@ namespace {
 
 constexpr int NB = 64;
 
-// Unblocked Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix.
-// 256 threads: thread t owns row r = t % 64 and the columns c = t / 64 (mod 4)
-// of the trailing update; every thread recomputes the pivot (no broadcast
-// barrier), two barriers per column.
+// Cholesky of the kb x kb diagonal block at (k0, k0) of each matrix, then its
+// triangular inverse, written back in place (the panel solve becomes a GEMM
+// and the later trtri starts from the diagonal inverses).  256 threads:
+// thread (r = t % 64, p = t / 64) keeps row r's columns c = 4 cc + p in
+// registers; L's columns are published in shared memory one per step.  Rows
+// and columns >= kb are padded with the identity.
 __global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
                                                   int* info) {
-  __shared__ double T[NB][NB + 1];
+  __shared__ double Ls[NB][NB + 1];  // Ls[c][r] = L(r, c)
+  __shared__ double xrow[NB];
+  __shared__ double piv_s;
   double* A = h + blockIdx.x * stride + k0 + k0 * ld;
   const int r = threadIdx.x & (NB - 1);
   const int part = threadIdx.x >> 6;  // 0..3
+  double t[NB / 4];
 #pragma unroll
-  for (int jj = 0; jj < NB / 4; ++jj) {
-    const int j = part + 4 * jj;
-    if (j < kb && r < kb) T[r][j] = A[r + j * ld];
+  for (int cc = 0; cc < NB / 4; ++cc) {
+    const int c = 4 * cc + part;
+    t[cc] = (r < kb && c < kb) ? (c <= r ? A[r + c * ld] : 0.0) : (r == c ? 1.0 : 0.0);
   }
-  __syncthreads();
+  // The step loops stay rolled (small code: the kernel is latency bound, and a
+  // fully unrolled 64-step body runs out of instruction cache); t[jc] with a
+  // run-time jc is read and written through selects.
   int bad = 0;
-  for (int j = 0; j < kb; ++j) {
-    double d = T[j][j];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (!bad) bad = j + 1;
-      d = 1.0;  // keep going; the caller reports the failure
-    }
-    const double piv = sqrt(d);
-    if (part == 0 && r >= j && r < kb) T[r][j] = (r == j) ? piv : T[r][j] / piv;
-    __syncthreads();
-    if (r > j && r < kb) {
-      const double lrj = T[r][j];
-      const int c0 = j + 1 + ((part - (j + 1)) & 3);  // first c > j with c % 4 == part
-      for (int c = c0; c <= r; c += 4) T[r][c] -= lrj * T[c][j];
-    }
-    __syncthreads();
-  }
-  if (bad && threadIdx.x == 0 && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
-  // L11^{-1} by columns: four threads per column c split each dot product
-  // X[i][c] = -(sum_{k=c}^{i-1} L[i][k] X[k][c]) / L[i][i].  X (lower) is kept
-  // transposed in the unused strict upper triangle of T (X[i][c] at T[c][i]),
-  // its diagonal in xd.
-  __shared__ double xd[NB];
-  {
-    const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
-    const bool live = c < kb;
-    const double xcc = live ? 1.0 / T[c][c] : 0.0;
-    if (live && q == 0) xd[c] = xcc;
-    // uniform trip count across the warp (the shuffles need every lane)
-    for (int i = 1; i < NB; ++i) {
-      const bool act = live && i > c && i < kb;
-      double sum = 0.0;
-      if (act)
-        for (int k = c + q; k < i; k += 4) sum += T[i][k] * (k == c ? xcc : T[c][k]);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      if (act && q == 0) T[c][i] = -sum / T[i][i];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // the diagonal block now holds L11^{-1} (zero above the diagonal): the
-  // panel solve becomes a GEMM and the later triangular inverse starts from it
+#pragma unroll 1
+  for (int j = 0; j < NB; ++j) {
+    const int jc = j >> 2, jp = j & 3;
+    double tj = t[0];
 #pragma unroll
-  for (int jj = 0; jj < NB / 4; ++jj) {
-    const int j = part + 4 * jj;
-    if (j < kb && r < kb) A[r + j * ld] = (r > j) ? T[j][r] : (r == j ? xd[r] : 0.0);
+    for (int cc = 1; cc < NB / 4; ++cc) tj = (cc == jc) ? t[cc] : tj;
+    if (part == jp && r == j) piv_s = tj;
+    __syncthreads();
+    double dpiv = piv_s;
+    if (!(dpiv > 0.0) || !isfinite(dpiv)) {
+      if (!bad) bad = j + 1;
+      dpiv = 1.0;  // keep going; the caller reports the failure
+    }
+    const double piv = sqrt(dpiv);
+    const double rpiv = 1.0 / piv;
+    if (part == jp && r >= j) {
+      const double l = (r == j) ? piv : tj * rpiv;
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) t[cc] = (cc == jc) ? l : t[cc];
+      Ls[j][r] = l;
+    }
+    if (r < j && part == 0) Ls[j][r] = 0.0;
+    __syncthreads();
+    if (r > j) {
+      const double lr = Ls[j][r];
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) {
+        const int c = 4 * cc + part;
+        if (c > j && c <= r) t[cc] -= lr * Ls[j][c];
+      }
+    }
+  }
+  if (bad && threadIdx.x == 0 && bad <= kb && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
+  // X = L^{-1} row by row: X(j, :) = (e_j - sum_{i<j} L(j, i) X(i, :)) / L(j, j).
+  double x[NB / 4];
+#pragma unroll
+  for (int cc = 0; cc < NB / 4; ++cc) x[cc] = (4 * cc + part == r) ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int j = 0; j < NB; ++j) {
+    if (r == j) {
+      const double rdjj = 1.0 / Ls[j][j];
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) {
+        x[cc] = x[cc] * rdjj;
+        xrow[4 * cc + part] = x[cc];
+      }
+    }
+    __syncthreads();
+    if (r > j) {
+      const double lrj = Ls[j][r];
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc)
+        if (4 * cc + part <= j) x[cc] -= lrj * xrow[4 * cc + part];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int cc = 0; cc < NB / 4; ++cc) {
+    const int c = 4 * cc + part;
+    if (r < kb && c < kb) A[r + c * ld] = (c <= r) ? x[cc] : 0.0;
   }
 }
 

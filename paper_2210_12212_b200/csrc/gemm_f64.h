@@ -46,12 +46,38 @@ struct GemmArgs {
   // heuristic looks at (m, k) only, so column j of C does not depend on n.
   int split_k = 0;
   bool col_stable = false;
-  // Deferred split-K: when the chosen split is > 1 the partial products are
-  // left in `*partials` (see Partials) for the consumer to sum in split order,
-  // and no reduction kernel runs.  Ignored for lower_only / mirror.
+    // Set to where the result lives (always C: split-K partials are reduced
+  // inside the GEMM kernel, in split order, by the last CTA of each tile).
   struct Partials* partials = nullptr;
   // Tuning hook: force a tile shape index (see gemm_f64.cu kTiles), -1 = auto.
   int force_tile = -1;
+  // Fused consumer of C (replaces the plain store; see RecursionEpilogue).
+  const struct RecursionEpilogue* epilogue = nullptr;
+};
+
+// Epilogues of the binomial-basis recursion (path_solver.cpp:37-49) fused
+// into the GEMM that produces their input, so each generation is two kernels.
+// Problems b = l*K + r (interval l, right-hand side r); gen / tilde are
+// dim x (kmax*NB) with column j*NB + b; args is interval-major
+// (dim x kmax*K per interval, column j*K + r).  See basis.h.
+//   kArgs   C = G * gen[:, :g*NB] (column j*NB + b):
+//           args[l][:, j*K + r] = tau_l * C + (j >= 1 ? gen[:, (j-1)*NB + b] : 0)
+//   kUpdate C_l = P_l * args[l][:, :(g+1)*K] (batch l, column j*K + r), for
+//           intervals with g < k_l:  gen[:, j*NB+b] = (j < g ? gen - C : -C),
+//           tilde += gen, flags[l] |= non-finite, and the next generation's
+//           last argument column args[l][:, (g+1)*K + r] = gen[:, g*NB + b].
+// Element-wise arithmetic is the standalone kernels' (build_args / update_gen),
+// so both routes give identical bits.
+struct RecursionEpilogue {
+  enum Kind { kArgs = 1, kUpdate = 2 };
+  int kind = 0;
+  int64_t dim = 0, L = 0, K = 0, kmax = 0, g = 0;
+  const double* tau = nullptr;
+  const int* kb = nullptr;
+  double* gen = nullptr;
+  double* tilde = nullptr;
+  double* args = nullptr;
+  int* flags = nullptr;
 };
 
 // Where a GEMM result lives when its reduction is deferred.  Element (i, j) of

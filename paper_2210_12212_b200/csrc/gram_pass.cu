@@ -3,7 +3,11 @@
 // Algorithmic bytes: atv_narrow reads A once (8 n d bytes) plus y; gram_fused
 // reads A once for z = A^T (A w) -- the reference evaluates the same product
 // as two passes, apply_transpose(a, apply(a, x)) (matrix.cpp:168-172).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "common.h"
 #include "gram_pass.h"
@@ -12,6 +16,7 @@ namespace rpb {
 namespace {
 
 constexpr int kChunkRows = 8192;  // rows per warp task in atv_narrow
+constexpr int kRB = 64;           // rows per atv step: 2 per lane, one 16-byte load per column
 
 template <int K>
 __device__ __forceinline__ void warp_reduce(double (&acc)[K]) {
@@ -22,12 +27,12 @@ __device__ __forceinline__ void warp_reduce(double (&acc)[K]) {
 }
 
 // One warp per (column c, row chunk q): partial[q][c + k d] = sum over the
-// chunk's rows of A[i, c] y[i, k].  Lane l handles rows l, l + 32, ... (two per
-// step, unrolled), then a fixed xor-tree reduction.
+// chunk's rows of A[i, c] y[i, k].  Lane l loads rows 2l, 2l+1 of every
+// 64-row step (16-byte loads, eight steps in flight), then the xor tree.
 template <int K>
 __global__ void __launch_bounds__(256) atv_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
                                                           int64_t d, const double* __restrict__ y, int64_t chunks,
-                                                          double* __restrict__ part) {
+                                                          double* __restrict__ part, bool vec) {
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (task >= d * chunks) return;
@@ -37,22 +42,32 @@ __global__ void __launch_bounds__(256) atv_partial_kernel(const double* __restri
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  int64_t i = r0 + lane;
-  for (; i + 96 < r1; i += 128) {
-    const double a0 = __ldg(col + i), a1 = __ldg(col + i + 32), a2 = __ldg(col + i + 64), a3 = __ldg(col + i + 96);
+  int64_t i = r0;
+  if (vec) {
+    constexpr int U = 8;
+    for (; i + U * kRB <= r1; i += U * kRB) {
+      double2 av[U];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double* yk = y + k * n;
-      acc[k] = fma(a0, yk[i], acc[k]);
-      acc[k] = fma(a1, yk[i + 32], acc[k]);
-      acc[k] = fma(a2, yk[i + 64], acc[k]);
-      acc[k] = fma(a3, yk[i + 96], acc[k]);
+      for (int u = 0; u < U; ++u) av[u] = __ldg(reinterpret_cast<const double2*>(col + i + u * kRB + 2 * lane));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double2 yv = __ldg(reinterpret_cast<const double2*>(y + k * n + i + u * kRB + 2 * lane));
+          acc[k] = fma(av[u].x, yv.x, acc[k]);
+          acc[k] = fma(av[u].y, yv.y, acc[k]);
+        }
     }
   }
-  for (; i < r1; i += 32) {
-    const double a0 = __ldg(col + i);
+  for (; i < r1; i += kRB) {
+    const int64_t ra = i + 2 * lane, rb = ra + 1;
+    const double a0 = ra < r1 ? __ldg(col + ra) : 0.0, a1 = rb < r1 ? __ldg(col + rb) : 0.0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = fma(a0, y[i + k * n], acc[k]);
+    for (int k = 0; k < K; ++k) {
+      const double y0 = ra < r1 ? y[k * n + ra] : 0.0, y1 = rb < r1 ? y[k * n + rb] : 0.0;
+      acc[k] = fma(a0, y0, acc[k]);
+      acc[k] = fma(a1, y1, acc[k]);
+    }
   }
   warp_reduce<K>(acc);
   if (lane == 0) {
@@ -65,131 +80,414 @@ __global__ void sum_chunks_kernel(const double* __restrict__ part, int64_t chunk
                                   double* __restrict__ x) {
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // sum in chunk order; loads issued eight at a time (latency overlap)
     double s = part[idx];
-    for (int64_t q = 1; q < chunks; ++q) s += part[q * total + idx];
+    int64_t q = 1;
+    for (; q + 8 <= chunks; q += 8) {
+      double t8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t8[u] = part[(q + u) * total + idx];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += t8[u];
+    }
+    for (; q < chunks; ++q) s += part[q * total + idx];
     x[idx] = s;
   }
 }
 
-// ---- fused single-pass Gram: z = A^T (A w) ------------------------------------
+// ---- TMA-staged column passes: z = A^T (A w)  and  x = A^T y ----------------
+//
+// A (n x d, column-major) is cut into 32-row blocks; persistent CTAs (one per
+// SM) own blocks b, b + grid, ...  A producer warp streams 16 KB tiles of A
+// through a shared-memory ring with 2-D TMA (cp.async.bulk.tensor, completion
+// on mbarriers), so the memory stream runs ahead of the math with no
+// registers held; sixteen consumer warps work on each tile.  Two tile shapes:
+//   "row" tiles  32 rows x  64 columns, plain layout   (y_b = A_b w: lane = row,
+//                warp = 4 columns; y partials stay in registers)
+//   "col" tiles  16 rows x 128 columns, 128B-swizzled (z += A_b^T y_b: 4 lanes
+//                per column, 4 rows each; the swizzle makes the transposed
+//                128-bit reads conflict-free; z accumulates in shared memory)
+// GRAM (z = A^T A w): the row tiles of block b+1 (from HBM, L2 evict_last)
+// are interleaved with the col tiles of block b (the same bytes, re-read one
+// block later from L2, evict_first), so the HBM stream never pauses and no
+// per-row-block cross-lane reduction is needed for z.  The L2 working set is
+// one block per SM (148 x 32 x d x 8 B, 39 MB at d = 1024).
+// ATV  (x = A^T y): col tiles only, from HBM.
+// Sums run in a fixed order (rows within a lane, xor tree over 4 lanes, blocks
+// in CTA order, CTA partials in CTA order, then the n % 32 tail): the result
+// is deterministic and each output column's arithmetic is independent of K.
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+constexpr int kPR = 32;                    // rows per block
+constexpr int kPWarps = 16;                // consumer warps
+constexpr int kRowTileCols = 128;          // row tile: 32 x 128
+constexpr int kColTileRows = 16;           // col tile: 16 x 256
+constexpr int kColTileCols = 256;
+constexpr int kRowU = kRowTileCols / kPWarps;        // row-tile columns per warp (8)
+constexpr int kColG = kColTileCols / (kPWarps * 8);  // col-tile column groups per warp (2)
+constexpr int kPMaxStages = 6;
+constexpr int kPStageDoubles = 4096;       // 32 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// One 2-D TMA box into a ring stage (elements past the end are zero-filled).
+__device__ __forceinline__ void tma_box(double* dst, const CUtensorMap* map, int row0, int col0, uint64_t* bar,
+                                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row0), "r"(col0), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPWarps * 32) : "memory"); }
 
-// Persistent CTAs; CTA b handles row blocks b, b + grid, ...  Each row block
-// (R rows x d columns, R*8-byte segments of every column) is staged in shared
-// memory with cp.async (double-buffered), y_blk = A_blk w is formed from it,
-// and z_cta += A_blk^T y_blk accumulates in registers (columns t, t+256, ...).
-template <int K>
-__global__ void __launch_bounds__(256) gram_fused_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
-                                                         int64_t d, int R, const double* __restrict__ w,
-                                                         double* __restrict__ ws, int cols_per_thread) {
-  extern __shared__ __align__(16) double sm[];
-  double* buf[2] = {sm, sm + static_cast<int64_t>(R) * d};
-  double* yblk = sm + 2 * static_cast<int64_t>(R) * d;  // [R][K]
-  double* red = yblk + R * K;                           // [256][K] partial dots
-  const int t = threadIdx.x;
-  const int64_t nblocks = (n + R - 1) / R;
-  const bool vec = (R % 2 == 0) && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+// The tile sequence of one CTA, shared by producer and consumers.
+//   GRAM: row tiles of block 0; then for each block i, interleaved:
+//         col tile s of block i (s < Q2), row tile s of block i+1 (s < Q1)
+//   ATV:  col tiles of each block
+struct TileSeq {
+  int q1, q2;  // row tiles / col tiles per block
+  __device__ TileSeq(int64_t d)
+      : q1(static_cast<int>((d + kRowTileCols - 1) / kRowTileCols)),
+        q2(static_cast<int>(2 * ((d + kColTileCols - 1) / kColTileCols))) {}
+};
 
-  auto stage = [&](int64_t blk, double* dst) {
-    const int64_t r0 = blk * R;
-    const int rr = static_cast<int>((n - r0) < R ? (n - r0) : R);
-    if (vec && rr == R) {
-      const int per_col = R / 2;
-      for (int64_t e = t; e < d * per_col; e += blockDim.x) {
-        const int64_t c = e / per_col;
-        const int h = static_cast<int>(e - c * per_col);
-        cp_async16(dst + c * R + 2 * h, a + c * lda + r0 + 2 * h);
+// Ring bookkeeping.
+struct RingPos {
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ void next(int stages) {
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+template <int K, bool GRAM>
+__global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
+    colpass_kernel(const __grid_constant__ CUtensorMap rowmap, const __grid_constant__ CUtensorMap colmap, int64_t n,
+                   int64_t nfull, int64_t d, const double* __restrict__ v, double* __restrict__ ws, int stages) {
+  extern __shared__ __align__(1024) double sm_raw[];
+  // 1024-byte aligned ring (the 128B swizzle pattern is defined on address bits 4-9)
+  // (offset arithmetic on the shared array keeps the accesses LDS/STS)
+  double* ring = sm_raw + (((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u) >> 3);
+  double* zs = ring + stages * kPStageDoubles;  // [d][K]
+  double* ypart = zs + d * K;                   // [kPWarps][32][K]
+  double* ycur = ypart + kPWarps * kPR * K;     // [K][kPR + 1] (padded: conflict-free)
+  __shared__ __align__(8) uint64_t full[kPMaxStages], empty[kPMaxStages];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const TileSeq seq(d);
+  const int64_t my_blocks = blockIdx.x < nfull ? (nfull - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto block_row = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * kPR; };
+  if (t == 0) {
+    for (int s2 = 0; s2 < stages; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], kPWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int64_t e = t; e < d * K; e += blockDim.x) zs[e] = 0.0;
+  __syncthreads();
+
+  if (wid == kPWarps) {  // producer
+    if (lane != 0) return;
+    uint64_t pol_last, pol_first;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    RingPos rp;
+    auto put = [&](const CUtensorMap* map, int64_t row, int64_t col, uint64_t pol) {
+      mbar_wait(&empty[rp.stage], rp.phase ^ 1);
+      mbar_arrive_expect_tx(&full[rp.stage], kPStageDoubles * 8);
+      tma_box(ring + rp.stage * kPStageDoubles, map, static_cast<int>(row), static_cast<int>(col), &full[rp.stage],
+              pol);
+      rp.next(stages);
+    };
+    if (GRAM) {
+      if (my_blocks > 0)
+        for (int64_t s2 = 0; s2 < seq.q1; ++s2) put(&rowmap, block_row(0), s2 * kRowTileCols, pol_last);
+      for (int64_t i = 0; i < my_blocks; ++i) {
+        const bool more = i + 1 < my_blocks;
+        for (int64_t s2 = 0; s2 < max(seq.q1, seq.q2); ++s2) {
+          if (s2 < seq.q2)
+            put(&colmap, block_row(i) + kColTileRows * (s2 & 1), kColTileCols * (s2 >> 1), pol_first);
+          if (more && s2 < seq.q1) put(&rowmap, block_row(i + 1), s2 * kRowTileCols, pol_last);
+        }
       }
     } else {
-      for (int64_t e = t; e < d * R; e += blockDim.x) {
-        const int64_t c = e / R;
-        const int r = static_cast<int>(e - c * R);
-        if (r < rr)
-          cp_async8(dst + c * R + r, a + c * lda + r0 + r);
-        else
-          dst[c * R + r] = 0.0;
+      for (int64_t i = 0; i < my_blocks; ++i)
+        for (int64_t s2 = 0; s2 < seq.q2; ++s2)
+          put(&colmap, block_row(i) + kColTileRows * (s2 & 1), kColTileCols * (s2 >> 1), pol_first);
+    }
+    return;
+  }
+
+  RingPos rp;
+  const int d32 = static_cast<int>(d);
+  double acc[K];  // y partial of row `lane` over this warp's columns
+  // row tile s of some block: acc += A[rows, c] w[c]
+  auto row_tile = [&](int s2) {
+    mbar_wait(&full[rp.stage], rp.phase);
+    const double* st = ring + rp.stage * kPStageDoubles + (wid * kRowU) * kPR + lane;
+    double av[kRowU];
+#pragma unroll
+    for (int u = 0; u < kRowU; ++u) av[u] = st[u * kPR];
+    const int cbase = s2 * kRowTileCols + wid * kRowU;
+#pragma unroll
+    for (int u = 0; u < kRowU; ++u) {
+      if (cbase + u < d32)
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = fma(av[u], __ldg(v + cbase + u + k * d32), acc[k]);
+    }
+    // release the stage only once its values are consumed (the arrive does
+    // not wait for this warp's outstanding shared-memory loads)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[rp.stage]);
+    rp.next(stages);
+  };
+  // col tile s of the block whose y is in ycur: z[c] += A[rows, c] . y[rows];
+  // 4 lanes per column (rq = rows 4rq..4rq+3), kColG column groups per warp
+  const int rq = lane & 3;
+  auto col_tile = [&](int s2) {
+    mbar_wait(&full[rp.stage], rp.phase);
+    const int rb = kColTileRows * (s2 & 1) + 4 * rq;
+    double pv[kColG][K];
+#pragma unroll
+    for (int g2 = 0; g2 < kColG; ++g2) {
+      const int cl = g2 * (kPWarps * 8) + wid * 8 + (lane >> 2);
+      const double* st = ring + rp.stage * kPStageDoubles + cl * kColTileRows;
+      const double2 x0 = *reinterpret_cast<const double2*>(st + (((2 * rq) ^ (cl & 7)) << 1));
+      const double2 x1 = *reinterpret_cast<const double2*>(st + (((2 * rq + 1) ^ (cl & 7)) << 1));
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double* yk = ycur + k * (kPR + 1) + rb;
+        double p = x0.x * yk[0];
+        p = fma(x0.y, yk[1], p);
+        p = fma(x1.x, yk[2], p);
+        p = fma(x1.y, yk[3], p);
+        pv[g2][k] = p;
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::);
+    __syncwarp();  // (stage values consumed: release it)
+    if (lane == 0) mbar_arrive(&empty[rp.stage]);
+    rp.next(stages);
+    // sum over the 4 lanes of each column: xor 2, then xor 1; with K >= 2 as
+    // a reduce-scatter (each lane keeps half the values at each step)
+#pragma unroll
+    for (int g2 = 0; g2 < kColG; ++g2) {
+      const int c = kColTileCols * (s2 >> 1) + g2 * (kPWarps * 8) + wid * 8 + (lane >> 2);
+      double* q = pv[g2];
+      if (K == 1) {
+        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 2);
+        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 1);
+        if (rq == 0 && c < d32) zs[c] += q[0];
+      } else {
+        constexpr int H = K / 2;
+        {
+          const bool up = lane & 2;
+#pragma unroll
+          for (int i2 = 0; i2 < H; ++i2) {
+            const double send = up ? q[i2] : q[i2 + H];
+            const double keep = up ? q[i2 + H] : q[i2];
+            q[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+        }
+        constexpr int Q4 = (H / 2 > 0) ? H / 2 : 1;
+        if (H >= 2) {
+          const bool up = lane & 1;
+#pragma unroll
+          for (int i2 = 0; i2 < Q4; ++i2) {
+            const double send = up ? q[i2] : q[i2 + Q4];
+            const double keep = up ? q[i2 + Q4] : q[i2];
+            q[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
+          const int base = ((lane & 2) ? H : 0) + ((lane & 1) ? Q4 : 0);
+          if (c < d32)
+#pragma unroll
+            for (int i2 = 0; i2 < Q4; ++i2) zs[c * K + base + i2] += q[i2];
+        } else {  // K == 2
+          q[0] += __shfl_xor_sync(0xffffffffu, q[0], 1);
+          if ((lane & 1) == 0 && c < d32) zs[c * K + ((lane & 2) ? 1 : 0)] += q[0];
+        }
+      }
+    }
+  };
+  auto reduce_y = [&]() {  // ycur = sum of the warps' y partials, warp order
+#pragma unroll
+    for (int k = 0; k < K; ++k) ypart[(wid * kPR + lane) * K + k] = acc[k];
+    consumer_sync();  // (also: every col tile of the previous block is done)
+    if (wid == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double sacc = ypart[lane * K + k];
+        for (int w2 = 1; w2 < kPWarps; ++w2) sacc += ypart[(w2 * kPR + lane) * K + k];
+        ycur[k * (kPR + 1) + lane] = sacc;
+      }
+    }
+    consumer_sync();
   };
 
-  double z[8][K];
+  if (GRAM) {
+    if (my_blocks > 0) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-#pragma unroll
-    for (int k = 0; k < K; ++k) z[j][k] = 0.0;
-
-  int64_t blk = blockIdx.x;
-  int cur = 0;
-  if (blk < nblocks) stage(blk, buf[0]);
-  for (; blk < nblocks; blk += gridDim.x) {
-    const int64_t nxt = blk + gridDim.x;
-    if (nxt < nblocks) {
-      stage(nxt, buf[cur ^ 1]);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
+      for (int k = 0; k < K; ++k) acc[k] = 0.0;
+      for (int s2 = 0; s2 < seq.q1; ++s2) row_tile(s2);
+      reduce_y();
     }
-    __syncthreads();
-    const double* A = buf[cur];
-    // y_blk[r][k] = sum_c A[r, c] w[c, k]: thread t -> row r = t % R, column
-    // slice q = t / R (fixed slices, fixed reduction order below).
-    const int slices = blockDim.x / R;
-    {
-      const int r = t % R, q = t / R;
+    for (int64_t i = 0; i < my_blocks; ++i) {
+      const bool more = i + 1 < my_blocks;
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = 0.0;
+      for (int s2 = 0; s2 < max(seq.q1, seq.q2); ++s2) {
+        if (s2 < seq.q2) col_tile(s2);
+        if (more && s2 < seq.q1) row_tile(s2);
+      }
+      if (more) reduce_y();
+    }
+  } else {
+    for (int64_t i = 0; i < my_blocks; ++i) {
+      consumer_sync();  // previous block's col tiles are done with ycur
+      if (wid == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) ycur[k * (kPR + 1) + lane] = __ldg(v + k * n + block_row(i) + lane);
+      consumer_sync();
+      for (int s2 = 0; s2 < seq.q2; ++s2) col_tile(s2);
+    }
+  }
+  consumer_sync();
+  for (int64_t e = t; e < d * K; e += kPWarps * 32) {
+    const int64_t c = e / K;
+    const int k = static_cast<int>(e - c * K);
+    ws[static_cast<int64_t>(blockIdx.x) * d * K + c + k * d] = zs[e];
+  }
+}
+
+// The last n % 32 rows (one CTA): the same sums, written as one more partial.
+template <int K, bool GRAM>
+__global__ void __launch_bounds__(256) colpass_tail_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
+                                                           int64_t r0, int64_t d, const double* __restrict__ v,
+                                                           double* __restrict__ out) {
+  __shared__ double yt[kPR][K];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int rows = static_cast<int>(n - r0);
+  if (GRAM) {  // y_tail[r] = sum_c A[r, c] w[c]: one warp per row
+    for (int r = wid; r < rows; r += blockDim.x / 32) {
       double acc[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = 0.0;
-      if (q < slices) {
-        for (int64_t c = q; c < d; c += slices) {
-          const double v = A[c * R + r];
+      for (int64_t c = lane; c < d; c += 32) {
+        const double x = a[c * lda + r0 + r];
 #pragma unroll
-          for (int k = 0; k < K; ++k) acc[k] = fma(v, __ldg(w + c + k * d), acc[k]);
-        }
+        for (int k = 0; k < K; ++k) acc[k] = fma(x, v[c + k * d], acc[k]);
       }
+      warp_reduce<K>(acc);
+      if (lane == 0)
 #pragma unroll
-      for (int k = 0; k < K; ++k) red[t * K + k] = acc[k];
+        for (int k = 0; k < K; ++k) yt[r][k] = acc[k];
     }
-    __syncthreads();
-    if (t < R) {
+  } else if (t < rows) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        double s = red[t * K + k];
-        for (int q = 1; q < slices; ++q) s += red[(q * R + t) * K + k];
-        yblk[t * K + k] = s;
-      }
-    }
-    __syncthreads();
-    // z[c] += sum_r A[r, c] y_blk[r]
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t c = t + static_cast<int64_t>(j) * blockDim.x;
-      if (j >= cols_per_thread || c >= d) break;
-      const double* col = A + c * R;
-      for (int r = 0; r < R; ++r) {
-        const double v = col[r];
-#pragma unroll
-        for (int k = 0; k < K; ++k) z[j][k] = fma(v, yblk[r * K + k], z[j][k]);
-      }
-    }
-    __syncthreads();
-    cur ^= 1;
+    for (int k = 0; k < K; ++k) yt[t][k] = v[k * n + r0 + t];
   }
+  __syncthreads();
+  for (int64_t c = t; c < d; c += blockDim.x) {
+    double acc[K];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int64_t c = t + static_cast<int64_t>(j) * blockDim.x;
-    if (j >= cols_per_thread || c >= d) break;
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int r = 0; r < rows; ++r) {
+      const double x = a[c * lda + r0 + r];
 #pragma unroll
-    for (int k = 0; k < K; ++k) ws[static_cast<int64_t>(blockIdx.x) * d * K + c + k * d] = z[j][k];
+      for (int k = 0; k < K; ++k) acc[k] = fma(x, yt[r][k], acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[c + k * d] = acc[k];
   }
+}
+
+// Launches the column pass; false if the operator is not 16-byte aligned.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Tensor map of the column-major operator: dims (rows n, columns d), box
+// rows x cols; the smem image is [column][row].
+bool operator_tensor_map(CUtensorMap* map, const double* a, int64_t lda, int64_t n, int64_t d, int box_rows,
+                         int box_cols, bool swizzle128) {
+  auto enc = tensor_map_encoder();
+  if (!enc || n >= (int64_t{1} << 31) || d >= (int64_t{1} << 31)) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(d)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int K, bool GRAM>
+bool colpass_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double* v, double* out, cudaStream_t s) {
+  if (lda % 2 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0 || d <= 0 || n <= 0) return false;
+  CUtensorMap rowmap, colmap;
+  if (!operator_tensor_map(&rowmap, a, lda, n, d, kPR, kRowTileCols, false) ||
+      !operator_tensor_map(&colmap, a, lda, n, d, kColTileRows, kColTileCols, true))
+    return false;
+  const size_t fixed = sizeof(double) * (static_cast<size_t>(d) * K + kPWarps * kPR * K + (kPR + 1) * K);
+  const size_t budget = 220 * 1024;
+  constexpr size_t stage_bytes = kPStageDoubles * sizeof(double);
+  if (fixed + 3 * stage_bytes + 1024 > budget || d >= (int64_t{1} << 30)) return false;
+  const int stages = static_cast<int>(std::min<size_t>(kPMaxStages, (budget - fixed - 1024) / stage_bytes));
+  const size_t smem = fixed + static_cast<size_t>(stages) * stage_bytes + 1024;  // (+ alignment slack)
+  int dev = 0, sms = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t nfull = n / kPR;
+  const bool tail = n % kPR != 0;
+  const int grid = static_cast<int>(std::min<int64_t>(nfull, sms));
+  const int64_t parts = grid + (tail ? 1 : 0);
+  DBuf<double> ws(static_cast<size_t>(parts) * d * K, s);
+  if (grid > 0) {
+    RP_CUDA(cudaFuncSetAttribute(colpass_kernel<K, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    colpass_kernel<K, GRAM><<<grid, (kPWarps + 1) * 32, smem, s>>>(rowmap, colmap, n, nfull, d, v, ws.get(), stages);
+    RP_LAUNCH_CHECK();
+  }
+  if (tail) {
+    colpass_tail_kernel<K, GRAM><<<1, 256, 0, s>>>(a, lda, n, nfull * kPR, d, v, ws.get() + grid * d * K);
+    RP_LAUNCH_CHECK();
+  }
+  sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(d * K, 256), 1184)), 256, 0, s>>>(
+      ws.get(), parts, d * K, out);
+  RP_LAUNCH_CHECK();
+  return true;
 }
 
 template <int K>
@@ -197,44 +495,54 @@ void atv_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double
   const int64_t chunks = ceil_div(n, kChunkRows);
   const int64_t warps = d * chunks;
   DBuf<double> part(static_cast<size_t>(chunks * d * K), s);
+  const bool vec = (lda % 2 == 0) && (n % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(y)) % 16 == 0);
   atv_partial_kernel<K><<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, s>>>(a, lda, n, d, y, chunks,
-                                                                                          part.get());
+                                                                                          part.get(), vec);
   RP_LAUNCH_CHECK();
   sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(d * K, 256), 1184)), 256, 0, s>>>(
       part.get(), chunks, d * K, x);
   RP_LAUNCH_CHECK();
 }
 
-template <int K>
-bool fused_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, double* z, cudaStream_t s) {
-  // rows per block: R * d * 8 * 2 (double buffer) <= ~200 KB, R a multiple of 4
-  int R = static_cast<int>(std::min<int64_t>(32, (200 * 1024) / (16 * d)));
-  R &= ~3;
-  if (R < 4 || d > 256 * 8) return false;
-  const int cols_per_thread = static_cast<int>(ceil_div(d, 256));
-  const int64_t nblocks = ceil_div(n, R);
-  const int grid = static_cast<int>(std::min<int64_t>(nblocks, 148));
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(R) * d + R * K + 256 * K);
-  RP_CUDA(cudaFuncSetAttribute(gram_fused_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
-  DBuf<double> ws(static_cast<size_t>(grid) * d * K, s);
-  gram_fused_kernel<K><<<grid, 256, smem, s>>>(a, lda, n, d, R, w, ws.get(), cols_per_thread);
-  RP_LAUNCH_CHECK();
-  sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(d * K, 256), 1184)), 256, 0, s>>>(
-      ws.get(), grid, d * K, z);
-  RP_LAUNCH_CHECK();
-  return true;
-}
+}  // namespace
 
+namespace {
+// One group of kw columns through the column pass (false: does not fit).
+template <bool GRAM>
+bool colpass_group(int64_t kw, const double* a, int64_t lda, int64_t n, int64_t d, const double* v, double* out,
+                   cudaStream_t s) {
+  switch (kw) {
+    case 8: return colpass_launch<8, GRAM>(a, lda, n, d, v, out, s);
+    case 4: return colpass_launch<4, GRAM>(a, lda, n, d, v, out, s);
+    case 2: return colpass_launch<2, GRAM>(a, lda, n, d, v, out, s);
+    default: return colpass_launch<1, GRAM>(a, lda, n, d, v, out, s);
+  }
+}
+// Columns j .. k-1 in groups of 8/4/2/1, each group as wide as fits the
+// shared-memory budget (a column's arithmetic does not depend on its group).
+// Returns the number of columns done (< k only if a single column fails).
+template <bool GRAM>
+int64_t colpass_columns(const double* a, int64_t lda, int64_t n, int64_t d, const double* v, int64_t v_ld,
+                        int64_t k, double* out, cudaStream_t s) {
+  int64_t j = 0;
+  while (j < k) {
+    int64_t kw = k - j >= 8 ? 8 : k - j >= 4 ? 4 : k - j >= 2 ? 2 : 1;
+    while (kw >= 1 && !colpass_group<GRAM>(kw, a, lda, n, d, v + j * v_ld, out + j * d, s)) kw /= 2;
+    if (kw < 1) break;
+    j += kw;
+  }
+  return j;
+}
 }  // namespace
 
 void atv_narrow(const double* a, int64_t lda, int64_t n, int64_t d, const double* y, int64_t k, double* x,
                 cudaStream_t stream) {
   require(k >= 1 && k <= kNarrowMax, "atv_narrow: 1 <= k <= 16");
   if (d <= 0) return;
-  // Process columns of y in groups of the instantiated widths; each output
-  // column's arithmetic is the same whatever group it falls in.
   int64_t j = 0;
+  if (n % 2 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0)
+    j = colpass_columns<false>(a, lda, n, d, y, n, k, x, stream);
+  // (unaligned operators: one warp per column and row chunk)
   while (j < k) {
     const int64_t left = k - j;
     const double* yj = y + j * n;
@@ -257,15 +565,8 @@ void atv_narrow(const double* a, int64_t lda, int64_t n, int64_t d, const double
 
 bool gram_fused(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
                 cudaStream_t stream) {
-  if (k < 1 || k > 8 || d <= 0 || n <= 0) return false;  // widths 1-4 and 8 are instantiated
-  switch (k) {
-    case 1: return fused_launch<1>(a, lda, n, d, w, z, stream);
-    case 2: return fused_launch<2>(a, lda, n, d, w, z, stream);
-    case 3: return fused_launch<3>(a, lda, n, d, w, z, stream);
-    case 4: return fused_launch<4>(a, lda, n, d, w, z, stream);
-    case 8: return fused_launch<8>(a, lda, n, d, w, z, stream);
-    default: return false;
-  }
+  if (k < 1 || k > 8 || d <= 0 || n <= 0) return false;
+  return colpass_columns<true>(a, lda, n, d, w, d, k, z, stream) == k;
 }
 
 }  // namespace rpb

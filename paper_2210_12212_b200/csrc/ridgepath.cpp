@@ -384,10 +384,12 @@ struct GramOp {
 
   // Y (D x cols) = M^T (M W)  (matrix.cpp:168-172) or G W.  With `out`
   // the split-K reduction of G W may be left to the consumer.
-  void apply(const double* W, int64_t cols, double* Y, Partials* out = nullptr) {
+  void apply(const double* W, int64_t cols, double* Y, Partials* out = nullptr,
+             const RecursionEpilogue* epi = nullptr) {
     cudaStream_t s = ctx->stream;
     if (cols <= 0) return;
     if (out) *out = Partials{Y, 1, op.d, 0, 0};
+    require(!epi || matrix, "gram: fused epilogue needs the Gram matrix");
     if (matrix) {
       GemmArgs g;
       g.m = op.d;
@@ -401,6 +403,7 @@ struct GramOp {
       g.ldc = op.d;
       g.col_stable = true;
       g.partials = out;
+      g.epilogue = epi;
       dgemm(g, s);
       return;
     }
@@ -496,10 +499,11 @@ struct PrecondBatch {
   // out_l (d x cols) = P_l in_l for l < L; in/out strided by `sin`/`sout`
   // (sin = 0 broadcasts one input to every interval).
   void apply(rp_ctx* ctx, const double* in, int64_t sin, int64_t cols, double* out, int64_t sout,
-             Partials* part = nullptr) const {
+             Partials* part = nullptr, const RecursionEpilogue* epi = nullptr) const {
     cudaStream_t s = ctx->stream;
     if (cols <= 0) return;
     if (part) *part = Partials{out, 1, d, 0, sout};
+    require(!epi || !woodbury, "preconditioner: fused epilogue needs the explicit inverse");
     if (!woodbury) {
       GemmArgs g;
       g.m = d;
@@ -517,6 +521,7 @@ struct PrecondBatch {
       g.batch = L;
       g.col_stable = true;
       g.partials = part;
+      g.epilogue = epi;
       dgemm(g, s);
       return;
     }
@@ -630,14 +635,40 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
   copy_cols(out.gen.get(), dim, NB, dim, out.tilde.get(), dim, s);
   if (kmax > 1) {
     const int64_t stride_im = dim * kmax * K;
-    DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);
-    DBuf<double> args(static_cast<size_t>(L * stride_im), s), applied(static_cast<size_t>(L * stride_im), s);
-    Partials py, pa;
-    for (int64_t g = 1; g < kmax; ++g) {
-      gram.apply(out.gen.get(), g * NB, y.get(), &py);
-      build_args(d, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
-      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
-      update_gen(d, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+    DBuf<double> args(static_cast<size_t>(L * stride_im), s);
+    if (gram.matrix && !P.woodbury) {
+      // Two kernels per generation: the Gram GEMM builds the preconditioner
+      // arguments in its epilogue, the preconditioner GEMM updates gen/tilde
+      // (and seeds the next generation's last argument column) in its own.
+      seed_args(d, out.gen.get(), args.get(), s);
+      RecursionEpilogue e;
+      e.dim = dim;
+      e.L = L;
+      e.K = K;
+      e.kmax = kmax;
+      e.tau = out.d_tau.get();
+      e.kb = out.d_k.get();
+      e.gen = out.gen.get();
+      e.tilde = out.tilde.get();
+      e.args = args.get();
+      e.flags = flags.get();
+      for (int64_t g = 1; g < kmax; ++g) {
+        e.g = g;
+        e.kind = RecursionEpilogue::kArgs;
+        gram.apply(out.gen.get(), g * NB, nullptr, nullptr, &e);
+        e.kind = RecursionEpilogue::kUpdate;
+        P.apply(ctx, args.get(), stride_im, (g + 1) * K, nullptr, stride_im, nullptr, &e);
+      }
+    } else {
+      DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);
+      DBuf<double> applied(static_cast<size_t>(L * stride_im), s);
+      Partials py, pa;
+      for (int64_t g = 1; g < kmax; ++g) {
+        gram.apply(out.gen.get(), g * NB, y.get(), &py);
+        build_args(d, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
+        P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
+        update_gen(d, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+      }
     }
   }
   out.diverged.assign(static_cast<size_t>(L), 0);
