@@ -58,7 +58,6 @@ struct KParams {
   int split;        // number of K splits
   int64_t k_chunk;  // K per split (multiple of the tile K)
   double* ws;       // split partials: [batch][split][n][m]
-  int* counters;    // per output tile: splits finished (reset by the last one)
   bool lower_only;
   bool mirror;  // lower_only: also write the transposed element (C symmetric)
   bool tri_k;   // op(A)(i, k) == 0 for k < i: start the k loop at the tile's first row
@@ -358,47 +357,20 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
     __syncthreads();  // smem / cinfo are reused by the next warp-column
   };
   if (p.split > 1) {
-    for (int w = 0; w < WN; ++w) {
-      stage(w);
-      for_tile(w, [&](int64_t row, int64_t col, double v) { W[sidx * mn + row + col * p.m] = v; });
-    }
-    __threadfence();
-    __syncthreads();
-    __shared__ int s_last;
-    const int64_t tile_id = (bidx * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    if (tid == 0) {
-      const int prev = atomicAdd(p.counters + tile_id, 1);
-      s_last = prev == p.split - 1;
-      if (s_last) p.counters[tile_id] = 0;  // ready for the next launch
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int w = 0; w < WN; ++w) {
-      const int64_t col0 = n0 + w * C::TN;
-      for (int base = tid; base < PER; base += U * C::THREADS) {
-        double v[U];
+    // split-K: this split's partial tile goes straight from registers to the
+    // workspace; the sum over splits (in split order) happens in the consumer
+    // (deferred Partials) or in splitk_reduce
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = 0.0;
-        for (int t = 0; t < p.split; ++t) {  // partials summed in split order
-          double q[U];
+    for (int i = 0; i < C::FM; ++i) {
+      const int64_t row = m0 + wm * C::TM + i * 8 + r8;
+      if (row >= p.m) continue;
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
-            q[u] = 0.0;
-            if (idx < PER && m0 + rr < p.m && col0 + cc < p.n) q[u] = __ldcg(W + t * mn + (m0 + rr) + (col0 + cc) * p.m);
-          }
+      for (int j = 0; j < C::FN; ++j)
 #pragma unroll
-          for (int u = 0; u < U; ++u) v[u] = t == 0 ? q[u] : v[u] + q[u];
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = n0 + wn * C::TN + j * 8 + 2 * k4 + e;
+          if (col < p.n && !(p.lower_only && row < col)) W[sidx * mn + row + col * p.m] = acc[i][j][e];
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * C::THREADS;
-          if (idx < PER) smem[(idx / BM) * SLD + idx % BM] = v[u];
-        }
-      }
-      __syncthreads();
-      finish(w);
     }
     return;
   }
@@ -408,26 +380,42 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   }
 }
 
+// Deterministic split-K reduction: partials summed in split order 0..S-1;
+// lower_only + mirror also writes the transposed element.
+__global__ void splitk_reduce(KParams p) {
+  const int64_t total = p.m * p.n;
+  const int64_t bidx = blockIdx.y;
+  const double* W = p.ws + bidx * p.split * total;
+  double* Cb = p.c + (bidx % p.batch) * p.stride_c + (bidx / p.batch) * p.stride_c2;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx % p.m, col = idx / p.m;
+    if (p.lower_only && row < col) continue;
+    double s = W[idx];
+    for (int t = 1; t < p.split; ++t) s += W[t * total + idx];
+    double* dst = Cb + row + col * p.ldc;
+    const double out = (p.beta == 0.0) ? p.alpha * s : p.alpha * s + p.beta * (*dst);
+    *dst = out;
+    if (p.mirror && row > col) Cb[col + row * p.ldc] = out;
+  }
+}
+
 struct Workspace {
   std::mutex mu;
   double* ptr = nullptr;
   size_t bytes = 0;
-  int* counters = nullptr;
-  size_t ncounters = 0;
   int device = -1;
 };
 Workspace g_ws;
 
-// Split-K partials (bytes) and zeroed tile counters (count); grown on demand.
-void workspace(size_t bytes, size_t counters, cudaStream_t stream, double** ws, int** cnt) {
+// Split-K partials; grown on demand (the grow path synchronizes the stream).
+double* workspace(size_t bytes, cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(g_ws.mu);
   int dev = 0;
   RP_CUDA(cudaGetDevice(&dev));
-  if (g_ws.device != dev) {  // (buffers of another device are abandoned)
+  if (g_ws.device != dev) {  // (a buffer of another device is abandoned)
     g_ws.ptr = nullptr;
     g_ws.bytes = 0;
-    g_ws.counters = nullptr;
-    g_ws.ncounters = 0;
     g_ws.device = dev;
   }
   if (g_ws.bytes < bytes) {
@@ -439,19 +427,7 @@ void workspace(size_t bytes, size_t counters, cudaStream_t stream, double** ws, 
     RP_CUDA(cudaMalloc(&g_ws.ptr, bytes));
     g_ws.bytes = bytes;
   }
-  if (g_ws.ncounters < counters) {
-    if (g_ws.counters) {
-      RP_CUDA(cudaStreamSynchronize(stream));
-      RP_CUDA(cudaFree(g_ws.counters));
-    }
-    g_ws.counters = nullptr;
-    const size_t n = std::max<size_t>(counters, 1 << 16);
-    RP_CUDA(cudaMalloc(&g_ws.counters, n * sizeof(int)));
-    RP_CUDA(cudaMemset(g_ws.counters, 0, n * sizeof(int)));
-    g_ws.ncounters = n;
-  }
-  *ws = g_ws.ptr;
-  *cnt = g_ws.counters;
+  return g_ws.ptr;
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
@@ -492,7 +468,11 @@ void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
 
 }  // namespace
 
+int choose_split(const GemmArgs& g);
+
 int dgemm_last_launches() { return g_last_launches; }
+
+int dgemm_split(const GemmArgs& g) { return choose_split(g); }
 
 namespace {
 thread_local GemmProfiler* g_prof = nullptr;
@@ -540,42 +520,9 @@ void dgemm(const GemmArgs& g, cudaStream_t stream) {
   g_prof->recs.push_back(r);
 }
 
-namespace {
-void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
-  g_last_launches = 0;
-  require(g.m >= 0 && g.n >= 0 && g.k >= 0 && g.batch >= 1 && g.batch2 >= 1, "dgemm: negative dimensions");
-  if (g.m == 0 || g.n == 0) return;
+// Split-K factor of a product (see dgemm_split in gemm_f64.h).
+int choose_split(const GemmArgs& g) {
   const int64_t nb = g.batch * g.batch2;
-  KParams kp{};
-  kp.m = g.m;
-  kp.n = g.n;
-  kp.k = g.k;
-  kp.alpha = g.alpha;
-  kp.beta = g.beta;
-  kp.a = g.a;
-  kp.lda = g.lda;
-  kp.stride_a = g.stride_a;
-  kp.b = g.b;
-  kp.ldb = g.ldb;
-  kp.stride_b = g.stride_b;
-  kp.c = g.c;
-  kp.ldc = g.ldc;
-  kp.stride_c = g.stride_c;
-  kp.batch = g.batch;
-  kp.batch2 = g.batch2;
-  kp.stride_a2 = g.stride_a2;
-  kp.stride_b2 = g.stride_b2;
-  kp.stride_c2 = g.stride_c2;
-  kp.lower_only = g.lower_only;
-  kp.tri_k = g.tri_k;
-
-  const bool ak = g.opa == Op::T;  // A contiguous along k
-  const bool bk = g.opb == Op::N;  // B contiguous along k
-  const bool aligned = (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(g.b) % 16 == 0) && g.lda % 2 == 0 &&
-                       g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
-                       g.stride_b2 % 2 == 0;
-
   // Split-K.  With col_stable the factor depends on (m, k) only, never on n
   // (column determinism); otherwise it is picked for full waves over the
   // 148 SMs, counting only the tiles that run (lower_only skips the rest).
@@ -617,6 +564,48 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   }
   int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
   if (k_chunk == 0) k_chunk = 16;
+  return static_cast<int>(std::max<int64_t>(1, ceil_div(g.k, k_chunk)));
+}
+
+namespace {
+void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
+  g_last_launches = 0;
+  require(g.m >= 0 && g.n >= 0 && g.k >= 0 && g.batch >= 1 && g.batch2 >= 1, "dgemm: negative dimensions");
+  if (g.m == 0 || g.n == 0) return;
+  const int64_t nb = g.batch * g.batch2;
+  KParams kp{};
+  kp.m = g.m;
+  kp.n = g.n;
+  kp.k = g.k;
+  kp.alpha = g.alpha;
+  kp.beta = g.beta;
+  kp.a = g.a;
+  kp.lda = g.lda;
+  kp.stride_a = g.stride_a;
+  kp.b = g.b;
+  kp.ldb = g.ldb;
+  kp.stride_b = g.stride_b;
+  kp.c = g.c;
+  kp.ldc = g.ldc;
+  kp.stride_c = g.stride_c;
+  kp.batch = g.batch;
+  kp.batch2 = g.batch2;
+  kp.stride_a2 = g.stride_a2;
+  kp.stride_b2 = g.stride_b2;
+  kp.stride_c2 = g.stride_c2;
+  kp.lower_only = g.lower_only;
+  kp.tri_k = g.tri_k;
+
+  const bool ak = g.opa == Op::T;  // A contiguous along k
+  const bool bk = g.opb == Op::N;  // B contiguous along k
+  const bool aligned = (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(g.b) % 16 == 0) && g.lda % 2 == 0 &&
+                       g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
+                       g.stride_b2 % 2 == 0;
+
+  int split = choose_split(g);
+  int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
+  if (k_chunk == 0) k_chunk = 16;
   split = static_cast<int>(std::max<int64_t>(1, ceil_div(g.k, k_chunk)));
   kp.split = split;
   kp.k_chunk = k_chunk;
@@ -642,12 +631,10 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     }
   }
   if (g.force_tile >= 0 && g.force_tile < kNumTiles) tile = g.force_tile;
-  if (split > 1) {
-    const size_t tiles = static_cast<size_t>(ceil_div(g.m, kTiles[tile].bm) * ceil_div(g.n, kTiles[tile].bn) * nb);
-    workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, tiles, stream, &kp.ws, &kp.counters);
-  }
+  if (split > 1) kp.ws = workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, stream);
   if (g.epilogue) {
-    require(!g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0, "dgemm: fused epilogue needs a plain product");
+    require(!g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0 && split == 1,
+            "dgemm: fused epilogue needs a plain, unsplit product");
     kp.epi = *g.epilogue;
   }
   if (g.mirror) require(g.lower_only && g.m == g.n && g.beta == 0.0, "dgemm: mirror needs a square lower_only output");
@@ -662,7 +649,16 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     aligned ? launch_layout<false, false, 2>(kp, tile, stream) : launch_layout<false, false, 1>(kp, tile, stream);
   }
   g_last_launches = 1;
-  if (g.partials) *g.partials = Partials{g.c, 1, g.ldc, 0, g.stride_c};
+  const bool defer = g.partials && split > 1 && !g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0;
+  if (g.partials)
+    *g.partials = defer ? Partials{kp.ws, split, g.m, g.m * g.n, split * g.m * g.n}
+                        : Partials{g.c, 1, g.ldc, 0, g.stride_c};
+  if (split > 1 && !defer) {
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(ceil_div(g.m * g.n, 256), 148 * 8)), static_cast<unsigned>(nb));
+    splitk_reduce<<<grid, 256, 0, stream>>>(kp);
+    RP_LAUNCH_CHECK();
+    ++g_last_launches;
+  }
 }
 
 }  // namespace

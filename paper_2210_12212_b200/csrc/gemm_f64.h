@@ -46,8 +46,9 @@ struct GemmArgs {
   // heuristic looks at (m, k) only, so column j of C does not depend on n.
   int split_k = 0;
   bool col_stable = false;
-    // Set to where the result lives (always C: split-K partials are reduced
-  // inside the GEMM kernel, in split order, by the last CTA of each tile).
+    // Deferred split-K: when the chosen split is > 1 the partial products are
+  // left in `*partials` (see Partials) for the consumer to sum in split order,
+  // and no reduction kernel runs.  Ignored for lower_only / mirror.
   struct Partials* partials = nullptr;
   // Tuning hook: force a tile shape index (see gemm_f64.cu kTiles), -1 = auto.
   int force_tile = -1;
@@ -94,6 +95,10 @@ struct Partials {
 // Launches on `stream`.  `workspace` (may be null) is used for split-K partials;
 // when null and a split is wanted, an internal cached buffer is used.
 void dgemm(const GemmArgs& g, cudaStream_t stream);
+
+// The split-K factor dgemm() would use for `g` (1 = no split: a fused
+// epilogue is only allowed then).
+int dgemm_split(const GemmArgs& g);
 
 // Number of kernel launches issued by the last dgemm() call on this thread.
 int dgemm_last_launches();

@@ -403,6 +403,15 @@ struct GramOp {
       g.ldc = op.d;
       g.col_stable = true;
       g.partials = out;
+      if (epi && dgemm_split(g) > 1) {
+        // split-K product: the partials stay deferred and the recursion's
+        // standalone argument kernel consumes them
+        require(out != nullptr && Y != nullptr, "gram: split product needs an output buffer");
+        dgemm(g, s);
+        BasisDims bd{epi->dim, epi->L, epi->K, epi->kmax};
+        build_args(bd, epi->g, *out, epi->gen, epi->tau, epi->args, s);
+        return;
+      }
       g.epilogue = epi;
       dgemm(g, s);
       return;
@@ -521,6 +530,7 @@ struct PrecondBatch {
       g.batch = L;
       g.col_stable = true;
       g.partials = part;
+      if (epi) g.split_k = 1;  // (the L-way batch fills the GPU; a fused epilogue needs no split)
       g.epilogue = epi;
       dgemm(g, s);
       return;
@@ -636,6 +646,7 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
   if (kmax > 1) {
     const int64_t stride_im = dim * kmax * K;
     DBuf<double> args(static_cast<size_t>(L * stride_im), s);
+    DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);  // (used when the Gram product is split)
     if (gram.matrix && !P.woodbury) {
       // Two kernels per generation: the Gram GEMM builds the preconditioner
       // arguments in its epilogue, the preconditioner GEMM updates gen/tilde
@@ -652,15 +663,15 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
       e.tilde = out.tilde.get();
       e.args = args.get();
       e.flags = flags.get();
+      Partials py;
       for (int64_t g = 1; g < kmax; ++g) {
         e.g = g;
         e.kind = RecursionEpilogue::kArgs;
-        gram.apply(out.gen.get(), g * NB, nullptr, nullptr, &e);
+        gram.apply(out.gen.get(), g * NB, y.get(), &py, &e);
         e.kind = RecursionEpilogue::kUpdate;
         P.apply(ctx, args.get(), stride_im, (g + 1) * K, nullptr, stride_im, nullptr, &e);
       }
     } else {
-      DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);
       DBuf<double> applied(static_cast<size_t>(L * stride_im), s);
       Partials py, pa;
       for (int64_t g = 1; g < kmax; ++g) {

@@ -5,6 +5,7 @@
 #include "../paper_2210_12212_b200/csrc/gemm_f64.cu"
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 using namespace rpb;
@@ -16,7 +17,9 @@ struct Shape {
   bool lower, col_stable;
 };
 
-int main() {
+int main(int argc, char** argv) {
+  // optional: gemm_tune SHAPE TILE -> one shape/tile, few iterations (for ncu)
+  const int only_shape = argc > 2 ? atoi(argv[1]) : -1, only_tile = argc > 2 ? atoi(argv[2]) : -9;
   std::vector<Shape> shapes = {
       {"GW g=1   (1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 1, false, true},
       {"GW g=8   (1024x256x1024)", Op::N, Op::N, 1024, 256, 1024, 1, false, true},
@@ -44,9 +47,12 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (auto& sh : shapes) {
+  for (size_t si = 0; si < shapes.size(); ++si) {
+    auto& sh = shapes[si];
+    if (only_shape >= 0 && static_cast<int>(si) != only_shape) continue;
     printf("%-32s", sh.name);
     for (int tile = -1; tile < 7; ++tile) {
+      if (only_tile != -9 && tile != only_tile) continue;
       GemmArgs g;
       g.opa = sh.opa;
       g.opb = sh.opb;
@@ -68,7 +74,7 @@ int main() {
       g.force_tile = tile;
       for (int w = 0; w < 3; ++w) dgemm(g, s);
       cudaEventRecord(e0, s);
-      const int iters = 10;
+      const int iters = only_shape >= 0 ? 2 : 10;
       for (int it = 0; it < iters; ++it) dgemm(g, s);
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
