@@ -105,9 +105,9 @@ __global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, int64
 }
 
 __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
-                                 double* __restrict__ out, int64_t ldo) {
+                                 double* __restrict__ out, int64_t ldo, int64_t cblk0) {
   __shared__ double tile[32][33];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = (static_cast<int64_t>(blockIdx.y) + cblk0) * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + threadIdx.x, c = c0 + k;
     if (r < rows && c < cols) tile[k][threadIdx.x] = in[r + c * ldi];
@@ -201,9 +201,13 @@ void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const d
 
 void transpose(const double* in, int64_t rows, int64_t cols, int64_t ldi, double* out, int64_t ldo,
                cudaStream_t stream) {
-  dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(cols, 32)));
-  transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(in, rows, cols, ldi, out, ldo);
-  RP_LAUNCH_CHECK();
+  // (grid.y is limited to 65535 blocks: column blocks go in chunks)
+  const int64_t cblks = ceil_div(cols, 32);
+  for (int64_t cb = 0; cb < cblks; cb += 65535) {
+    dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(std::min<int64_t>(65535, cblks - cb)));
+    transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(in, rows, cols, ldi, out, ldo, cb);
+    RP_LAUNCH_CHECK();
+  }
 }
 
 void spmm_csr_rm(const int64_t* off, const int32_t* col, const double* val, int64_t n, int64_t c, const double* x_rm,

@@ -28,10 +28,17 @@ __global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t
   const int r = threadIdx.x & (NB - 1);
   const int part = threadIdx.x >> 6;  // 0..3
   double t[NB / 4];
+  {
+    // all 16 loads issued unconditionally (clamped addresses), then selected
+    const int rc = min(r, kb - 1);
+    double v[NB / 4];
 #pragma unroll
-  for (int cc = 0; cc < NB / 4; ++cc) {
-    const int c = 4 * cc + part;
-    t[cc] = (r < kb && c < kb) ? (c <= r ? A[r + c * ld] : 0.0) : (r == c ? 1.0 : 0.0);
+    for (int cc = 0; cc < NB / 4; ++cc) v[cc] = A[rc + static_cast<int64_t>(min(4 * cc + part, kb - 1)) * ld];
+#pragma unroll
+    for (int cc = 0; cc < NB / 4; ++cc) {
+      const int c = 4 * cc + part;
+      t[cc] = (r < kb && c < kb) ? (c <= r ? v[cc] : 0.0) : (r == c ? 1.0 : 0.0);
+    }
   }
   // The step loops stay rolled (small code: the kernel is latency bound, and a
   // fully unrolled 64-step body runs out of instruction cache); t[jc] with a

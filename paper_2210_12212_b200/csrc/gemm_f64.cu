@@ -159,6 +159,73 @@ __device__ __forceinline__ void load_tile(double* sm, const double* g, int64_t l
   }
 }
 
+// Per-thread copy plan of one operand tile (MN_T x BK of op(X)), computed
+// once per CTA: global source of each 16-byte chunk at the first k tile, its
+// shared-memory slot, and how many bytes the MN bound leaves.  Each k tile
+// then only adds a fixed stride; the k bound is checked on the last tile only.
+template <int MN_T, int BK, int LD, int THREADS, bool KMAJ, int VEC>
+struct TileCopier {
+  static constexpr int CPR = KMAJ ? BK / VEC : MN_T / VEC;  // chunks per smem row
+  static constexpr int TOTAL = KMAJ ? MN_T * CPR : BK * CPR;
+  static constexpr int NCH = (TOTAL + THREADS - 1) / THREADS;
+  const double* src[NCH];
+  int dst[NCH];
+  int kk[NCH];
+  int bytes[NCH];  // < 0: no chunk
+  int64_t kstep;
+  __device__ __forceinline__ void init(const double* g, int64_t ld, int64_t mn0, int64_t mn_lim, int64_t kbeg,
+                                       int tid) {
+#pragma unroll
+    for (int n = 0; n < NCH; ++n) {
+      const int c = tid + n * THREADS;
+      int mm, k;
+      if (KMAJ) {
+        mm = c / CPR;
+        k = (c % CPR) * VEC;
+      } else {
+        k = c / CPR;
+        mm = (c % CPR) * VEC;
+      }
+      const int64_t gm = mn0 + mm;
+      kk[n] = k;
+      dst[n] = KMAJ ? mm * LD + k : k * LD + mm;
+      if (c >= TOTAL) {
+        bytes[n] = -1;
+        src[n] = g;
+      } else if (gm >= mn_lim) {
+        bytes[n] = 0;
+        src[n] = g;
+      } else {
+        bytes[n] = KMAJ ? VEC * 8 : static_cast<int>(mn_lim - gm < VEC ? mn_lim - gm : VEC) * 8;
+        src[n] = KMAJ ? g + (kbeg + k) + gm * ld : g + gm + (kbeg + k) * ld;
+      }
+    }
+    kstep = KMAJ ? BK : BK * ld;
+  }
+  // k tile `kt`; k_rem = valid k values left from this tile's first k
+  __device__ __forceinline__ void issue(double* sm, int kt, int64_t k_rem) const {
+    const int64_t off = static_cast<int64_t>(kt) * kstep;
+    const bool full = k_rem >= BK;
+#pragma unroll
+    for (int n = 0; n < NCH; ++n) {
+      if (bytes[n] < 0) continue;
+      int b = bytes[n];
+      if (!full) {
+        const int64_t kv = k_rem - kk[n];
+        if (KMAJ)
+          b = kv <= 0 ? 0 : (kv < VEC ? static_cast<int>(kv) * 8 : b);
+        else if (kv <= 0)
+          b = 0;
+      }
+      const double* sp = b > 0 ? src[n] + off : src[n];
+      if (VEC == 2)
+        cp_async16(sm + dst[n], sp, b);
+      else
+        cp_async8(sm + dst[n], sp, b);
+    }
+  }
+};
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
 __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
@@ -192,12 +259,14 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  TileCopier<BM, BK, C::A_LD, C::THREADS, AK, VEC> ca;
+  TileCopier<BN, BK, C::B_LD, C::THREADS, BKM, VEC> cb;
+  ca.init(A, p.lda, m0, p.m, kbeg, tid);
+  cb.init(B, p.ldb, n0, p.n, kbeg, tid);
   auto issue = [&](int kt, int stage) {
-    const int64_t k0 = kbeg + static_cast<int64_t>(kt) * BK;
-    load_tile<BM, BK, C::A_LD, C::THREADS, AK, VEC>(As + stage * C::A_STAGE, A, p.lda, m0, p.m, k0,
-                                                      kend, tid);
-    load_tile<BN, BK, C::B_LD, C::THREADS, BKM, VEC>(Bs + stage * C::B_STAGE, B, p.ldb, n0, p.n, k0,
-                                                       kend, tid);
+    const int64_t k_rem = kend - kbeg - static_cast<int64_t>(kt) * BK;
+    ca.issue(As + stage * C::A_STAGE, kt, k_rem);
+    cb.issue(Bs + stage * C::B_STAGE, kt, k_rem);
   };
 
 #pragma unroll
@@ -208,16 +277,19 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
 
   const int r8 = lane >> 2;  // fragment row / column within the 8-wide tile
   const int k4 = lane & 3;   // fragment k index
+  int rstage = 0, wstage = STAGES - 1;  // (rolling stage indices, no modulo)
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       const int nk = kt + STAGES - 1;
-      if (nk < ktiles) issue(nk, nk % STAGES);
+      if (nk < ktiles) issue(nk, wstage);
       cp_async_commit();
+      wstage = wstage + 1 == STAGES ? 0 : wstage + 1;
     }
-    const double* as = As + (kt % STAGES) * C::A_STAGE;
-    const double* bs = Bs + (kt % STAGES) * C::B_STAGE;
+    const double* as = As + rstage * C::A_STAGE;
+    const double* bs = Bs + rstage * C::B_STAGE;
+    rstage = rstage + 1 == STAGES ? 0 : rstage + 1;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[C::FM], bf[C::FN];
@@ -439,6 +511,9 @@ void launch_cfg(const KParams& kp, cudaStream_t stream) {
     RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
+  require(ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
+              ceil_div(kp.m, BM) < (int64_t{1} << 31),
+          "dgemm: problem too large for one launch grid");
   dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
             static_cast<unsigned>(kp.batch * kp.batch2 * kp.split));
   kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(kp);
@@ -450,8 +525,9 @@ void launch_cfg(const KParams& kp, cudaStream_t stream) {
 struct TileShape {
   int bm, bn;
 };
-constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128}, {128, 64}};
-constexpr int kNumTiles = 7;
+constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128},
+                                {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}};
+constexpr int kNumTiles = 11;
 
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
@@ -462,7 +538,13 @@ void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
     case 3: launch_cfg<64, 32, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
     case 4: launch_cfg<128, 16, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
     case 5: launch_cfg<64, 128, 16, 2, 4, 3, AK, BKM, VEC>(kp, stream); break;
-    default: launch_cfg<128, 64, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    case 6: launch_cfg<128, 64, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    // 4 warps with 32 x 64 / 64 x 32 warp tiles: more DMMAs per fragment load
+    case 7: launch_cfg<64, 128, 16, 2, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    case 8: launch_cfg<128, 64, 16, 2, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    // BK = 32, 2 stages: half the barriers per flop
+    case 9: launch_cfg<64, 128, 32, 2, 4, 2, AK, BKM, VEC>(kp, stream); break;
+    default: launch_cfg<128, 64, 32, 4, 2, 2, AK, BKM, VEC>(kp, stream); break;
   }
 }
 
@@ -616,11 +698,14 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   {
     // CTAs per SM and relative large-problem throughput per shape (measured,
     // profiles/gemm_tune_r01.txt)
-    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1};
-    static constexpr double kEff[] = {0.93, 0.94, 0.89, 0.91, 0.69, 1.0, 0.98};
+    // (profiles/r01_gemm_tune.txt: large-problem throughput relative to the
+    // best shape; 9, 10 = BK 32 variants, kept for tuning only)
+    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2};
+    static constexpr double kEff[] = {0.82, 0.95, 0.92, 0.93, 0.75, 0.96, 0.95, 0.90, 1.0, 0.0, 0.0};
     double best = 1e300;
     for (int t = 0; t < kNumTiles; ++t) {
       if (kTiles[t].bn == 16 && g.n > 16) continue;
+      if (kEff[t] <= 0.0) continue;
       const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
       const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));
       const double cost = waves * kTiles[t].bm * kTiles[t].bn * kOcc[t] / kEff[t];

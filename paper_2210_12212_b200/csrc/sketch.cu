@@ -262,8 +262,8 @@ __global__ void transpose_rm_to_cm(const double* __restrict__ in, int64_t rows, 
 // SA[:, c] += S_slab[:, j] * v over the CSC entries (j in the slab) of column c.
 __global__ void gauss_csc_accum(const int64_t* __restrict__ coff, const int32_t* __restrict__ crow,
                                 const double* __restrict__ cval, int64_t j0, int64_t J,
-                                const double* __restrict__ s_cm, int64_t m, double* __restrict__ sa) {
-  const int64_t c = blockIdx.y;
+                                const double* __restrict__ s_cm, int64_t m, double* __restrict__ sa, int64_t c0) {
+  const int64_t c = blockIdx.y + c0;
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < m;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double acc = sa[r + c * m];
@@ -343,10 +343,12 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
           dim3 tg(static_cast<unsigned>(ceil_div(Jc, 32)), static_cast<unsigned>(ceil_div(m, 32)));
           transpose_rm_to_cm<<<tg, dim3(32, 8), 0, stream>>>(slab.get(), m, Jc, slab_cm.get());
           RP_LAUNCH_CHECK();
-          dim3 ag(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(d));
-          gauss_csc_accum<<<ag, 256, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, j0, Jc, slab_cm.get(), m,
-                                                  d_sa);
-          RP_LAUNCH_CHECK();
+          for (int64_t c0 = 0; c0 < d; c0 += 65535) {  // (grid.y <= 65535)
+            dim3 ag(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(std::min<int64_t>(65535, d - c0)));
+            gauss_csc_accum<<<ag, 256, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, j0, Jc, slab_cm.get(), m,
+                                                    d_sa, c0);
+            RP_LAUNCH_CHECK();
+          }
         }
       }
       return;

@@ -51,7 +51,7 @@ int main(int argc, char** argv) {
     auto& sh = shapes[si];
     if (only_shape >= 0 && static_cast<int>(si) != only_shape) continue;
     printf("%-32s", sh.name);
-    for (int tile = -1; tile < 7; ++tile) {
+    for (int tile = -1; tile < 11; ++tile) {
       if (only_tile != -9 && tile != only_tile) continue;
       GemmArgs g;
       g.opa = sh.opa;
@@ -83,7 +83,7 @@ int main(int argc, char** argv) {
       double fl = 2.0 * sh.m * sh.n * sh.k * sh.batch * (sh.lower ? 0.5 : 1.0);
       printf(" %s%6.1f", tile < 0 ? "auto:" : "", fl / (ms / iters * 1e-3) / 1e12);
     }
-    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64]\n");
+    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64, 64x128w4, 128x64w4, 64x128k32, 128x64k32]\n");
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
