@@ -165,6 +165,16 @@ RP_API rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y
 RP_API rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double* x, int where);
 RP_API rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out, int where);
 
+/* losses / losses_matrix (ref/src/path_solver.cpp:425-454) for T solutions at
+ * once, against the context's operator (primal view):
+ *   loss[t] = 0.5 ||A X_t - B||_F^2 + 0.5 lambda[t] ||X_t||_F^2
+ * X_t = x + t*d*K (d x K, column-major), B: n_local x K (this rank's rows),
+ * lambda may be NULL (no regularization term: the reference's test loss).
+ * With several ranks (row shards) every rank receives the global sum.
+ * x, b, lambda and loss all live on `where`. */
+RP_API rp_status rp_losses(rp_ctx* ctx, const double* b, int64_t K, int64_t T, const double* x,
+                           const double* lambda, double* loss, int where);
+
 /* sketch_apply (sketch.hpp:43): SA (m x d) of the context's operator;
  * `transpose_op` = 1 sketches A^T instead (the dual route's operator). */
 RP_API rp_status rp_sketch_apply(rp_ctx* ctx, const rp_sketch_spec* spec, int transpose_op, double* sa, int where);

@@ -151,7 +151,60 @@ __global__ void fill_kernel(double* __restrict__ dst, int64_t count, double v) {
     dst[idx] = v;
 }
 
+// One CTA per column: strided per-thread sums (rows in a fixed order), then a
+// fixed shared-memory tree.
+__global__ void __launch_bounds__(256) column_sq_kernel(const double* __restrict__ r, int64_t rows, int64_t ldr,
+                                                        const double* __restrict__ b, int64_t K, int64_t ldb,
+                                                        double* __restrict__ out, int64_t col0) {
+  __shared__ double red[256];
+  const int64_t j = blockIdx.x + col0;
+  const double* rc = r + j * ldr;
+  const double* bc = b ? b + (j % K) * ldb : nullptr;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += 256) {
+    const double v = bc ? __dsub_rn(rc[i], bc[i]) : rc[i];
+    acc = fma(v, v, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int h = 128; h >= 1; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = red[0];
+}
+
+__global__ void combine_losses_kernel(const double* __restrict__ rn, const double* __restrict__ xn,
+                                      const double* __restrict__ lambda, int64_t T, int64_t K,
+                                      double* __restrict__ loss) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < T;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0, q = 0.0;
+    for (int64_t k = 0; k < K; ++k) {
+      s += rn[t * K + k];
+      if (xn) q += xn[t * K + k];
+    }
+    loss[t] = lambda && xn ? 0.5 * s + 0.5 * lambda[t] * q : 0.5 * s;
+  }
+}
+
 }  // namespace
+
+void column_sq_norms(const double* r, int64_t rows, int64_t cols, int64_t ldr, const double* b, int64_t K,
+                     int64_t ldb, double* out, cudaStream_t stream) {
+  for (int64_t c0 = 0; c0 < cols; c0 += (int64_t{1} << 30)) {
+    const int64_t cn = std::min<int64_t>(int64_t{1} << 30, cols - c0);
+    column_sq_kernel<<<static_cast<unsigned>(cn), 256, 0, stream>>>(r, rows, ldr, b, K, ldb, out, c0);
+    RP_LAUNCH_CHECK();
+  }
+}
+
+void combine_losses(const double* rn, const double* xn, const double* lambda, int64_t T, int64_t K, double* loss,
+                    cudaStream_t stream) {
+  if (T <= 0) return;
+  combine_losses_kernel<<<grid_for(T), 256, 0, stream>>>(rn, xn, lambda, T, K, loss);
+  RP_LAUNCH_CHECK();
+}
 
 // Launches `launch(grid, col0)` over column chunks of at most 65535 (grid.y limit).
 template <class F>

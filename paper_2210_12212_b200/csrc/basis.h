@@ -52,6 +52,15 @@ void compose(const BasisDims& d, const double* tilde, const double* d_tau, const
 void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,
                    const double* d_lambda0, double* out, cudaStream_t stream);
 
+// Loss pieces (path_solver.cpp:425-454).  For output column j of R
+// (rows x cols, ld ldr): out[j] = sum_r (R[r, j] - B[r, j % K])^2 (B may be
+// null: plain sum of squares), summed over rows in a fixed order.
+void column_sq_norms(const double* r, int64_t rows, int64_t cols, int64_t ldr, const double* b, int64_t K,
+                     int64_t ldb, double* out, cudaStream_t stream);
+// loss[t] = 0.5 * sum_k rn[t K + k] + 0.5 * lambda[t] * sum_k xn[t K + k]  (lambda/xn may be null)
+void combine_losses(const double* rn, const double* xn, const double* lambda, int64_t T, int64_t K, double* loss,
+                    cudaStream_t stream);
+
 // Row-major helpers for the CSR Gram.
 void transpose(const double* in, int64_t rows, int64_t cols, int64_t ldi, double* out, int64_t ldo,
                cudaStream_t stream);  // out (cols x rows, col-major) = in^T (in: rows x cols col-major)

@@ -1326,6 +1326,35 @@ rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out
   });
 }
 
+rp_status rp_losses(rp_ctx* ctx, const double* b, int64_t K, int64_t T, const double* x, const double* lambda,
+                    double* lossp, int where) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const OpView op = ctx->op.primal();
+    require(K >= 1 && T >= 0, "losses: dimension mismatch");
+    cudaStream_t s = ctx->stream;
+    InBuf xb(x, static_cast<size_t>(op.d * K * T), where, s);
+    InBuf bb(b, static_cast<size_t>(op.n_loc * K), where, s);
+    InBuf lb(lambda, lambda ? static_cast<size_t>(T) : 0, where, s);
+    OutBuf out(lossp, static_cast<size_t>(T), where, s);
+    if (T > 0) {
+      DBuf<double> rn(static_cast<size_t>(T * K), s), xn(static_cast<size_t>(T * K), s);
+      // residuals in chunks of solutions (R: n_local x chunk*K, <= ~1 GiB)
+      const int64_t per = std::max<int64_t>(1, (int64_t{1} << 27) / std::max<int64_t>(1, op.n_loc * K));
+      DBuf<double> r(static_cast<size_t>(op.n_loc * K * std::min<int64_t>(per, T)), s);
+      for (int64_t t0 = 0; t0 < T; t0 += per) {
+        const int64_t tc = std::min<int64_t>(per, T - t0);
+        op_apply(ctx, op, xb.ptr + t0 * op.d * K, tc * K, r.get());
+        column_sq_norms(r.get(), op.n_loc, tc * K, op.n_loc, bb.ptr, K, op.n_loc, rn.get() + t0 * K, s);
+      }
+      allreduce(ctx, rn.get(), T * K);  // row shards: sum the partial squared norms
+      if (lb.ptr) column_sq_norms(xb.ptr, op.d, T * K, op.d, nullptr, 1, 0, xn.get(), s);
+      combine_losses(rn.get(), lb.ptr ? xn.get() : nullptr, lb.ptr, T, K, out.dev, s);
+    }
+    out.finish();
+  });
+}
+
 rp_status rp_sketch_apply(rp_ctx* ctx, const rp_sketch_spec* specp, int transpose_op, double* sa, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {

@@ -111,6 +111,7 @@ SIGNATURES = {
     "rp_apply": ([_P, _P, _I64, _P, _INT], _INT),
     "rp_apply_transpose": ([_P, _P, _I64, _P, _INT], _INT),
     "rp_gram_apply": ([_P, _P, _I64, _P, _INT], _INT),
+    "rp_losses": ([_P, _P, _I64, _I64, _P, _P, _P, _INT], _INT),
     "rp_sketch_apply": ([_P, ctypes.POINTER(_SketchSpec), _INT, _P, _INT], _INT),
     "rp_precond_build": ([_P, _P, _I64, _I64, _D, _INT, ctypes.POINTER(_P)], _INT),
     "rp_precond_reshift": ([_P, _P, _D, ctypes.POINTER(_P)], _INT),
@@ -289,6 +290,8 @@ class PathPoint:
     lam: float
     solution: np.ndarray
     seconds: float = 0.0
+    train_loss: float = 0.0  # 0.5 ||A x - b||^2 + 0.5 lam ||x||^2  (path_solver.cpp:425-439)
+    test_loss: Optional[float] = None  # 0.5 ||A_test x - b_test||^2 when a test set is given
 
 
 @dataclass
@@ -600,8 +603,29 @@ def ihs_compose_matrix(basis: BinomialBasis, lam: float, ctx: Optional[Context] 
     return out.reshape(basis.terms[0].shape)
 
 
+def losses(a, b, x, lambdas=None, ctx: Optional[Context] = None) -> np.ndarray:
+    """losses / losses_matrix (path_solver.cpp:425-454) for T solutions at once:
+    x is d x K x T (or d x T for K = 1), b is n x K; returns
+    0.5 ||A X_t - B||_F^2 (+ 0.5 lambda_t ||X_t||_F^2 when lambdas is given)."""
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    b2 = _f64(np.asarray(b).reshape(np.asarray(b).shape[0], -1))
+    K = b2.shape[1]
+    x = np.asarray(x, dtype=np.float64)
+    d = _cols(a)
+    T = x.size // (d * K) if x.size else 0
+    if b2.shape[0] != _rows(a) or x.size != d * K * T:
+        raise ValueError("losses: dimension mismatch")
+    xs = np.ascontiguousarray(x.reshape(d, K, T).transpose(2, 1, 0)).reshape(-1)  # t-major, column-major d x K
+    lam = _f64(np.asarray(lambdas, dtype=np.float64)) if lambdas is not None else None
+    out = np.empty(max(T, 1))
+    ctx.check(lib().rp_losses(ctx.handle, _ptr(b2.reshape(-1, order="F").copy()), K, T, _ptr(xs),
+                              _ptr(lam) if lam is not None else None, _ptr(out), RP_HOST))
+    return out[:T]
+
+
 def _run_path(dual: bool, a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
-              ctx: Optional[Context] = None, return_timings=False) -> RegPathResult:
+              ctx: Optional[Context] = None, return_timings=False, a_test=None, b_test=None) -> RegPathResult:
     ctx = ctx or default_context()
     ctx.set_operator(a)
     b = np.asarray(b)
@@ -621,30 +645,51 @@ def _run_path(dual: bool, a, b, config: PathConfig, spec: SketchSpec, rho: RhoBo
                  ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, _ptr(out), RP_HOST,
                  ctypes.byref(tm)))
     del keep
+    # per-point losses as the reference's loss callbacks (path_solver.cpp:298-303,
+    # 318-323, 342-347): train always, test when a test set is given
+    lam = np.asarray(config.lambdas, dtype=np.float64)
+    primal_dim = _cols(a)
+    train = _losses_flat(ctx, b2, K, T, out, lam) if T else np.empty(0)
+    test = None
+    if a_test is not None and b_test is not None and T:
+        bt = _f64(np.asarray(b_test).reshape(np.asarray(b_test).shape[0], -1))
+        if _cols(a_test) != primal_dim or bt.shape[1] != K or bt.shape[0] != _rows(a_test):
+            raise ValueError("losses: test dimension mismatch")
+        ctx.set_operator(a_test)
+        test = _losses_flat(ctx, bt, K, T, out, None)
+        ctx.set_operator(a)
     pts = []
     for t in range(T):
         x = out[t * dim * K:(t + 1) * dim * K].reshape((dim, K), order="F").copy()
-        pts.append(PathPoint(float(config.lambdas[t]), x))
+        pts.append(PathPoint(float(config.lambdas[t]), x, train_loss=float(train[t]),
+                             test_loss=float(test[t]) if test is not None else None))
     return RegPathResult("dual" if dual else "ihs-bin", pts, tm.setup_seconds, tm.total_seconds, tm.as_dict())
 
 
+def _losses_flat(ctx, b2, K, T, x_flat, lam):
+    out = np.empty(max(T, 1))
+    ctx.check(lib().rp_losses(ctx.handle, _ptr(np.asfortranarray(b2).reshape(-1, order="F").copy()), K, T,
+                              _ptr(x_flat), _ptr(lam) if lam is not None else None, _ptr(out), RP_HOST))
+    return out[:T]
+
+
 def ihs_bin_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
-                 ctx: Optional[Context] = None) -> RegPathResult:
+                 ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
     """path_solver.hpp:109-114 (vector b) / 116-121 (matrix b)."""
     if spec.n != _rows(a):
         raise ValueError("ihs_bin_path: spec.n must equal A.rows")
-    return _run_path(False, a, b, config, spec, rho, sigma_d, ctx)
+    return _run_path(False, a, b, config, spec, rho, sigma_d, ctx, a_test=a_test, b_test=b_test)
 
 
 ihs_bin_path_matrix = ihs_bin_path
 
 
 def dual_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_d=None,
-              ctx: Optional[Context] = None) -> RegPathResult:
+              ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
     """path_solver.hpp:134-139; a matrix b runs K independent dual paths."""
     if spec.n != _cols(a):
         raise ValueError("dual_path: spec.n must equal A.cols (the dual operator is A^T)")
-    return _run_path(True, a, b, config, spec, rho, sigma_d, ctx)
+    return _run_path(True, a, b, config, spec, rho, sigma_d, ctx, a_test=a_test, b_test=b_test)
 
 
 # ---------------------------------------------------------------------------

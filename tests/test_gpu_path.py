@@ -300,3 +300,50 @@ def test_grid_edge_cases(rp, ctx, oracle):
         for gp, rp_ in zip(got.points, ref.points):
             assert gp.lam == rp_.lam
             assert oracle.rel_error(gp.solution, rp_.solution) < TOL
+
+
+def test_path_losses_match_oracle(rp, ctx, oracle):
+    """Per-point train/test losses (path_solver.cpp:298-303, 318-323, 342-347,
+    425-454): every PathPoint of the device path carries the reference's
+    losses of its own solution."""
+    rng = np.random.default_rng(17)
+    n, d, nt = 300, 20, 90
+    a = rng.standard_normal((n, d))
+    b = a @ rng.standard_normal(d) + 0.1 * rng.standard_normal(n)
+    at = rng.standard_normal((nt, d))
+    bt = at @ rng.standard_normal(d)
+    grid = rp.log_grid(1e-2, 1e1, 7)
+    cfg = rp.PathConfig(1e-2, 1e1, grid, 1e-6)
+    spec = rp.SketchSpec("gaussian", 60, n, 1, 3)
+    rho = rp.RhoBounds.manual(*oracle.mp_rho(d, 60)) if hasattr(oracle, "mp_rho") else rp.RhoBounds.manual(
+        (1 + (d / 60) ** 0.5) ** 2, (1 - (d / 60) ** 0.5) ** 2)
+    path = rp.ihs_bin_path(a, b, cfg, spec, rho, ctx=ctx, a_test=at, b_test=bt)
+    for p in path.points:
+        tr, te = oracle.losses(a, b, p.solution[:, 0], p.lam, at, bt)
+        assert p.train_loss == pytest.approx(tr, rel=1e-12)
+        assert p.test_loss == pytest.approx(te, rel=1e-12)
+    # matrix right-hand side (losses_matrix: Frobenius norms)
+    B = np.stack([b, -2 * b + 0.3], axis=1)
+    BT = np.stack([bt, bt], axis=1)
+    pm = rp.ihs_bin_path(a, B, cfg, spec, rho, ctx=ctx, a_test=at, b_test=BT)
+    for p in pm.points:
+        tr, te = oracle.losses(a, B, p.solution, p.lam, at, BT)
+        assert p.train_loss == pytest.approx(tr, rel=1e-12)
+        assert p.test_loss == pytest.approx(te, rel=1e-12)
+    # sparse operator, no test set
+    c = oracle.Csr.from_dense(np.where(rng.random((n, d)) < 0.3, a, 0.0))
+    gc = rp.Csr(c.rows, c.cols, c.offsets, c.indices, c.values)
+    x = rng.standard_normal((d, 5))
+    lams = np.linspace(0.1, 2.0, 5)
+    got = rp.losses(gc, b, x, lams, ctx=ctx)
+    for t in range(5):
+        assert got[t] == pytest.approx(oracle.losses(c, b, x[:, t], lams[t])[0], rel=1e-12)
+    assert np.allclose(rp.losses(gc, b, x, None, ctx=ctx),
+                       [oracle.losses(c, b, x[:, t], 0.0)[0] for t in range(5)], rtol=1e-12)
+    # dual path: losses of the recovered solution against the primal data
+    aw = rng.standard_normal((40, 120))
+    bw = rng.standard_normal(40)
+    dpath = rp.dual_path(aw, bw, rp.PathConfig(1e-1, 1e1, rp.log_grid(1e-1, 1e1, 4), 1e-6),
+                         rp.SketchSpec("gaussian", 80, 120, 1, 5), rp.RhoBounds.manual(1.0, 1e-5), ctx=ctx)
+    for p in dpath.points:
+        assert p.train_loss == pytest.approx(oracle.losses(aw, bw, p.solution[:, 0], p.lam)[0], rel=1e-12)
