@@ -164,6 +164,9 @@ RP_API rp_status rp_set_csr_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, in
 RP_API rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int where);
 RP_API rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double* x, int where);
 RP_API rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out, int where);
+/* With rp_set_option(ctx, "profile", 1): device seconds (CUDA events on the
+ * context stream) of the last rp_apply_transpose / rp_gram_apply call. */
+RP_API rp_status rp_last_device_seconds(rp_ctx* ctx, double* seconds);
 
 /* losses / losses_matrix (ref/src/path_solver.cpp:425-454) for T solutions at
  * once, against the context's operator (primal view):

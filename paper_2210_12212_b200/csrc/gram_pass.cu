@@ -76,6 +76,29 @@ __global__ void __launch_bounds__(256) atv_partial_kernel(const double* __restri
   }
 }
 
+// Deterministic sum over the chunk partials, two fixed levels: 16 threads per
+// output each sum the chunks g, g + 16, g + 32, ... (in order), then the 16
+// group sums are added in group order.  256 threads = 16 outputs x 16 groups.
+__global__ void __launch_bounds__(256) sum_chunks_tree_kernel(const double* __restrict__ part, int64_t chunks,
+                                                              int64_t total, double* __restrict__ x) {
+  __shared__ double red[16][17];
+  const int o = threadIdx.x & 15, g = threadIdx.x >> 4;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 16 + o;
+  double s = 0.0;
+  if (idx < total) {
+    int64_t q = g;
+    if (q < chunks) s = part[q * total + idx];
+    for (q += 16; q < chunks; q += 16) s += part[q * total + idx];
+  }
+  red[g][o] = s;
+  __syncthreads();
+  if (g == 0 && idx < total) {
+    double t = red[0][o];
+    for (int h = 1; h < 16 && h < chunks; ++h) t += red[h][o];
+    x[idx] = t;
+  }
+}
+
 __global__ void sum_chunks_kernel(const double* __restrict__ part, int64_t chunks, int64_t total,
                                   double* __restrict__ x) {
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -469,14 +492,18 @@ bool colpass_launch(const double* a, int64_t lda, int64_t n, int64_t d, const do
   int dev = 0, sms = 0;
   RP_CUDA(cudaGetDevice(&dev));
   RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static thread_local size_t smem_set = 0;  // (per instantiation: raise the limit once)
   const int64_t nfull = n / kPR;
   const bool tail = n % kPR != 0;
   const int grid = static_cast<int>(std::min<int64_t>(nfull, sms));
   const int64_t parts = grid + (tail ? 1 : 0);
   DBuf<double> ws(static_cast<size_t>(parts) * d * K, s);
   if (grid > 0) {
-    RP_CUDA(cudaFuncSetAttribute(colpass_kernel<K, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+    if (smem > smem_set) {
+      RP_CUDA(cudaFuncSetAttribute(colpass_kernel<K, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      smem_set = smem;
+    }
     colpass_kernel<K, GRAM><<<grid, (kPWarps + 1) * 32, smem, s>>>(rowmap, colmap, n, nfull, d, v, ws.get(), stages);
     RP_LAUNCH_CHECK();
   }
@@ -484,8 +511,7 @@ bool colpass_launch(const double* a, int64_t lda, int64_t n, int64_t d, const do
     colpass_tail_kernel<K, GRAM><<<1, 256, 0, s>>>(a, lda, n, nfull * kPR, d, v, ws.get() + grid * d * K);
     RP_LAUNCH_CHECK();
   }
-  sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(d * K, 256), 1184)), 256, 0, s>>>(
-      ws.get(), parts, d * K, out);
+  sum_chunks_tree_kernel<<<static_cast<unsigned>(ceil_div(d * K, 16)), 256, 0, s>>>(ws.get(), parts, d * K, out);
   RP_LAUNCH_CHECK();
   return true;
 }

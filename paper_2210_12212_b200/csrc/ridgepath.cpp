@@ -285,6 +285,7 @@ struct rp_ctx {
   ncclComm_t comm = nullptr;
   int gram_mode = -1;
   bool profile = false;
+  double last_device_seconds = 0.0;  // profile: device time of the last product call
   std::string err;
 };
 
@@ -1286,6 +1287,32 @@ rp_status rp_set_csr_rows(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n
   });
 }
 
+// With the profile option, brackets the device work of one product call with
+// CUDA events (the C-ABI call itself synchronizes, so host timing would add
+// the round trip): rp_last_device_seconds() returns it.
+struct DeviceTimer {
+  rp_ctx* ctx;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  explicit DeviceTimer(rp_ctx* c) : ctx(c) {
+    if (!ctx->profile) return;
+    RP_CUDA(cudaEventCreate(&e0));
+    RP_CUDA(cudaEventCreate(&e1));
+    RP_CUDA(cudaEventRecord(e0, ctx->stream));
+  }
+  void stop() {
+    if (!e0) return;
+    RP_CUDA(cudaEventRecord(e1, ctx->stream));
+    RP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    ctx->last_device_seconds = ms * 1e-3;
+  }
+  ~DeviceTimer() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+};
+
 rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
@@ -1305,7 +1332,9 @@ rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double
     require(ncols >= 0, "apply_transpose: dimension mismatch");
     InBuf in(y, static_cast<size_t>(op.n_loc * ncols), where, ctx->stream);
     OutBuf out(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
+    DeviceTimer timer(ctx);
     if (ncols > 0) op_apply_t(ctx, op, in.ptr, ncols, out.dev, true);
+    timer.stop();
     out.finish();
   });
 }
@@ -1321,9 +1350,17 @@ rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* out
     g.ctx = ctx;
     g.op = op;
     g.allow_fused = true;
+    DeviceTimer timer(ctx);
     if (ncols > 0) g.apply(in.ptr, ncols, out.dev);
+    timer.stop();
     out.finish();
   });
+}
+
+rp_status rp_last_device_seconds(rp_ctx* ctx, double* seconds) {
+  if (!ctx || !seconds) return RP_EINVAL;
+  *seconds = ctx->last_device_seconds;
+  return RP_OK;
 }
 
 rp_status rp_losses(rp_ctx* ctx, const double* b, int64_t K, int64_t T, const double* x, const double* lambda,

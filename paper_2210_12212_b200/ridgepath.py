@@ -112,6 +112,7 @@ SIGNATURES = {
     "rp_apply_transpose": ([_P, _P, _I64, _P, _INT], _INT),
     "rp_gram_apply": ([_P, _P, _I64, _P, _INT], _INT),
     "rp_losses": ([_P, _P, _I64, _I64, _P, _P, _P, _INT], _INT),
+    "rp_last_device_seconds": ([_P, ctypes.POINTER(_D)], _INT),
     "rp_sketch_apply": ([_P, ctypes.POINTER(_SketchSpec), _INT, _P, _INT], _INT),
     "rp_precond_build": ([_P, _P, _I64, _I64, _D, _INT, ctypes.POINTER(_P)], _INT),
     "rp_precond_reshift": ([_P, _P, _D, ctypes.POINTER(_P)], _INT),
@@ -812,6 +813,13 @@ def path_raw(ctx: Context, b_ptr: int, K: int, config: PathConfig, spec: SketchS
 def gram_apply_raw(ctx: Context, x_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
     """rp_gram_apply on raw pointers: out = A^T (A x) for the context's operator."""
     ctx.check(lib().rp_gram_apply(ctx.handle, _P(x_ptr), ncols, _P(out_ptr), where))
+
+
+def last_device_seconds(ctx: Context) -> float:
+    """Device seconds of the last apply_transpose / gram_apply (profile option on)."""
+    v = ctypes.c_double(0.0)
+    ctx.check(lib().rp_last_device_seconds(ctx.handle, ctypes.byref(v)))
+    return v.value
 
 
 def apply_transpose_raw(ctx: Context, y_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
