@@ -136,7 +136,59 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   require(n >= 1 && batch >= 1, "spd_inverse: empty problem");
   DBuf<int> info(static_cast<size_t>(batch), stream);
   RP_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int) * batch, stream));
-  // 1) Cholesky, lower.
+  // 1) Cholesky, lower, right-looking with one panel of lookahead: after the
+  // panel solve of block k, the next block column is updated on `stream`
+  // (then block k+1 is factored there) while the rest of the trailing matrix
+  // is updated on an auxiliary stream -- the latency-bound diagonal kernels
+  // (one CTA per matrix) overlap the big trailing GEMMs.  All GEMMs here run
+  // unsplit, so they share no workspace.
+  // The critical chain (diagonal kernels, panel solves, next-column updates)
+  // runs on a high-priority stream so its CTAs are scheduled ahead of the
+  // trailing-update CTAs as SMs free up.
+  const cudaStream_t user = stream;
+  int prio_lo = 0, prio_hi = 0;
+  RP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  cudaStream_t aux = nullptr, hi = nullptr;
+  RP_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, prio_lo));
+  RP_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, prio_hi));
+  std::vector<cudaEvent_t> events;
+  auto new_event = [&]() {
+    cudaEvent_t e;
+    RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events.push_back(e);
+    return e;
+  };
+  {
+    cudaEvent_t start = new_event();
+    RP_CUDA(cudaEventRecord(start, user));
+    RP_CUDA(cudaStreamWaitEvent(hi, start, 0));
+  }
+  stream = hi;
+  auto syrk_update = [&](int64_t row0, int64_t m, int64_t ncols, int64_t k0, int kb, cudaStream_t st) {
+    // C(row0.., row0..row0+ncols) -= A21(row0.., :) A21(row0..row0+ncols, :)^T, lower part
+    GemmArgs g;
+    g.opa = Op::N;
+    g.opb = Op::T;
+    g.m = m;
+    g.n = ncols;
+    g.k = kb;
+    g.alpha = -1.0;
+    g.beta = 1.0;
+    g.a = h + row0 + k0 * ld;
+    g.lda = ld;
+    g.stride_a = stride;
+    g.b = g.a;
+    g.ldb = ld;
+    g.stride_b = stride;
+    g.c = h + row0 + row0 * ld;
+    g.ldc = ld;
+    g.stride_c = stride;
+    g.batch = batch;
+    g.lower_only = true;
+    g.split_k = 1;
+    dgemm(g, st);
+  };
+  cudaEvent_t prev_rest = nullptr;  // trailing update of the previous panel (aux stream)
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
     potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
@@ -167,28 +219,33 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
       t.force_tile = 6;  // 128 x 64
       dgemm(t, stream);
     }
-    GemmArgs g;  // A22 -= A21 A21^T (lower)
-    g.opa = Op::N;
-    g.opb = Op::T;
-    g.m = rows;
-    g.n = rows;
-    g.k = kb;
-    g.alpha = -1.0;
-    g.beta = 1.0;
-    g.a = h + (k0 + kb) + k0 * ld;
-    g.lda = ld;
-    g.stride_a = stride;
-    g.b = g.a;
-    g.ldb = ld;
-    g.stride_b = stride;
-    g.c = h + (k0 + kb) + (k0 + kb) * ld;
-    g.ldc = ld;
-    g.stride_c = stride;
-    g.batch = batch;
-    g.lower_only = true;
-    g.split_k = 1;
-    dgemm(g, stream);
+    const int64_t r0 = k0 + kb;
+    const int64_t nxt = std::min<int64_t>(NB, rows), rest = rows - nxt;
+    cudaEvent_t rest_done = nullptr;
+    if (rest > 0) {  // columns beyond the next block: aux stream
+      cudaEvent_t panel_done = new_event();
+      RP_CUDA(cudaEventRecord(panel_done, stream));
+      RP_CUDA(cudaStreamWaitEvent(aux, panel_done, 0));
+      syrk_update(r0 + nxt, rest, rest, k0, kb, aux);
+      rest_done = new_event();
+      RP_CUDA(cudaEventRecord(rest_done, aux));
+    }
+    // the next block column (all rows below the diagonal) on the main stream;
+    // it also needs the previous panel's update of those columns
+    if (prev_rest) RP_CUDA(cudaStreamWaitEvent(stream, prev_rest, 0));
+    syrk_update(r0, rows, nxt, k0, kb, stream);
+    prev_rest = rest_done;
   }
+  if (prev_rest) RP_CUDA(cudaStreamWaitEvent(stream, prev_rest, 0));
+  {
+    cudaEvent_t done = new_event();
+    RP_CUDA(cudaEventRecord(done, hi));
+    RP_CUDA(cudaStreamWaitEvent(user, done, 0));
+  }
+  stream = user;
+  for (cudaEvent_t e : events) RP_CUDA(cudaEventDestroy(e));  // (released once complete)
+  RP_CUDA(cudaStreamDestroy(aux));
+  RP_CUDA(cudaStreamDestroy(hi));
   // 2) Triangular inverse in place.
   {
     // (the strict upper triangle is already zero: shifted_copies writes it so
