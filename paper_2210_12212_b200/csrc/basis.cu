@@ -63,11 +63,12 @@ __global__ void update_kernel(BasisDims d, int64_t g, Partials applied, const in
   if (bad) flags[l] = 1;
 }
 
-__global__ void seed_args_kernel(BasisDims d, const double* __restrict__ gen, double* __restrict__ args, int64_t col0) {
+__global__ void seed_args_kernel(BasisDims d, const double* __restrict__ gen, double* __restrict__ args, int64_t col0,
+                                 int64_t g) {
   const int64_t b = blockIdx.y + col0;  // problem
   const int64_t l = b / d.K, r = b - l * d.K;
-  double* out = args + (l * d.kmax * d.K + d.K + r) * d.dim;
-  const double* src = gen + b * d.dim;
+  double* out = args + (l * d.kmax * d.K + (g + 1) * d.K + r) * d.dim;
+  const double* src = gen + (g * d.L * d.K + b) * d.dim;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = src[i];
@@ -227,7 +228,13 @@ void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* 
 void seed_args(const BasisDims& d, const double* gen, double* args_im, cudaStream_t stream) {
   if (d.kmax < 2) return;
   for_col_chunks(d.dim, d.nb(), [&](dim3 grid, int64_t c0) {
-    seed_args_kernel<<<grid, 256, 0, stream>>>(d, gen, args_im, c0);
+    seed_args_kernel<<<grid, 256, 0, stream>>>(d, gen, args_im, c0, 0);
+  });
+}
+
+void seed_next_args(const BasisDims& d, int64_t g, const double* gen, double* args_im, cudaStream_t stream) {
+  for_col_chunks(d.dim, d.nb(), [&](dim3 grid, int64_t c0) {
+    seed_args_kernel<<<grid, 256, 0, stream>>>(d, gen, args_im, c0, g);
   });
 }
 

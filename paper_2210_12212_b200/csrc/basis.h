@@ -35,6 +35,9 @@ void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* 
 // args_im[l][:, K + r] = gen[:, b] (the generation-1 argument column; the
 // fused recursion epilogue writes the later ones, see gemm_f64.h).
 void seed_args(const BasisDims& d, const double* gen, double* args_im, cudaStream_t stream);
+// args_im[l][:, (g+1)*K + r] = gen[:, g*NB + b] (next generation's last argument
+// column; what the fused update epilogue writes).
+void seed_next_args(const BasisDims& d, int64_t g, const double* gen, double* args_im, cudaStream_t stream);
 
 // gen[:, j*NB+b] -= applied[l][:, j*K+r] (j < g); gen[:, g*NB+b] = -applied[l][:, g*K+r];
 // flags[l] |= any non-finite in gen[:, 0..g]; tilde[:, j*NB+b] += gen[:, j*NB+b] (j <= g).

@@ -286,6 +286,7 @@ struct rp_ctx {
   int gram_mode = -1;
   bool profile = false;
   double last_device_seconds = 0.0;  // profile: device time of the last product call
+  bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   std::string err;
 };
 
@@ -531,6 +532,17 @@ struct PrecondBatch {
       g.batch = L;
       g.col_stable = true;
       g.partials = part;
+      if (epi && !ctx->fuse_update) {
+        // split product + the standalone update kernel
+        require(out != nullptr, "preconditioner: split product needs an output buffer");
+        Partials pa;
+        g.partials = &pa;
+        dgemm(g, s);
+        BasisDims bd{epi->dim, epi->L, epi->K, epi->kmax};
+        update_gen(bd, epi->g, pa, epi->kb, epi->gen, epi->tilde, epi->flags, s);
+        if (epi->g + 1 < epi->kmax) seed_next_args(bd, epi->g, epi->gen, epi->args, s);
+        return;
+      }
       if (epi) g.split_k = 1;  // (the L-way batch fills the GPU; a fused epilogue needs no split)
       g.epilogue = epi;
       dgemm(g, s);
@@ -648,6 +660,7 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
     const int64_t stride_im = dim * kmax * K;
     DBuf<double> args(static_cast<size_t>(L * stride_im), s);
     DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);  // (used when the Gram product is split)
+    DBuf<double> applied(static_cast<size_t>(L * stride_im), s);
     if (gram.matrix && !P.woodbury) {
       // Two kernels per generation: the Gram GEMM builds the preconditioner
       // arguments in its epilogue, the preconditioner GEMM updates gen/tilde
@@ -670,10 +683,9 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
         e.kind = RecursionEpilogue::kArgs;
         gram.apply(out.gen.get(), g * NB, y.get(), &py, &e);
         e.kind = RecursionEpilogue::kUpdate;
-        P.apply(ctx, args.get(), stride_im, (g + 1) * K, nullptr, stride_im, nullptr, &e);
+        P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, nullptr, &e);
       }
     } else {
-      DBuf<double> applied(static_cast<size_t>(L * stride_im), s);
       Partials py, pa;
       for (int64_t g = 1; g < kmax; ++g) {
         gram.apply(out.gen.get(), g * NB, y.get(), &py);
@@ -1219,6 +1231,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->gram_mode = static_cast<int>(value);
     } else if (k == "profile") {
       ctx->profile = value != 0;
+    } else if (k == "fuse_update") {
+      ctx->fuse_update = value != 0;
     } else {
       throw InvalidArgument("unknown option: " + k);
     }
