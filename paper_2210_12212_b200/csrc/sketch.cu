@@ -213,6 +213,198 @@ __global__ void __launch_bounds__(256) fwht_pass(FwhtArgs f) {
   }
 }
 
+// ---- two-pass SRHT transform -------------------------------------------------
+//
+// n_pad = 2^QB * CH (CH <= 8192).  Pass 1 (fwht_top_kernel): the QB largest
+// strides -- one thread per row offset r < CH keeps the 2^QB elements
+// r + CH j in registers (sign multiply and zero padding fused into the load,
+// coalesced 8 KB segments per j).  Pass 2 (fwht_chunk_kernel): one CTA per
+// (column, CH-row chunk) does the remaining log2(CH) strides -- the four
+// largest in registers, the rest in shared memory -- and writes only the
+// sampled rows to SA.  Strides run largest first, the reference's order
+// (sketch.cpp:25-48), so every entry is bit-identical to the reference.
+constexpr int kFwhtChunkThreads = 512;
+constexpr int64_t kFwhtMaxChunk = 8192;
+
+__device__ __forceinline__ double signed_op_value(const FwhtArgs& f, int64_t c, int64_t i) {
+  const int64_t li = i - f.row0;
+  if (li < 0 || li >= f.n_loc) return 0.0;
+  return f.signs[i] * (f.trans ? f.a[c + li * f.lda] : f.a[li + c * f.lda]);
+}
+
+template <int QB>
+__global__ void __launch_bounds__(256) fwht_top_kernel(FwhtArgs f, int64_t ch) {
+  constexpr int J = 1 << QB;
+  const int64_t per_col = ch;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < per_col * f.d;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx / per_col, r = idx - c * per_col;
+    double v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = signed_op_value(f, c, r + ch * j);
+#pragma unroll
+    for (int kk = J / 2; kk >= 1; kk >>= 1)
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        if ((j & kk) == 0) {
+          const double a = v[j], b = v[j + kk];
+          v[j] = a + b;
+          v[j + kk] = a - b;
+        }
+    double* col = f.x + c * f.npad;
+#pragma unroll
+    for (int j = 0; j < J; ++j) col[r + ch * j] = v[j];
+  }
+}
+
+// from_x: the chunk comes from the pass-1 scratch; else straight from the
+// operator (n_pad <= CH: the whole transform is local).
+__global__ void __launch_bounds__(kFwhtChunkThreads) fwht_chunk_kernel(FwhtArgs f, int64_t ch, bool from_x) {
+  extern __shared__ __align__(16) double xs[];  // ch doubles
+  constexpr int kT = kFwhtChunkThreads;
+  const int ch32 = static_cast<int>(ch);
+  const int64_t chunks = f.npad / ch;
+  const int64_t c = blockIdx.x / chunks, q = blockIdx.x - c * chunks;
+  const int64_t chunk0 = q * ch;
+  const int t = threadIdx.x;
+  const int nj = ch32 >= kT ? ch32 / kT : 0;
+  if (nj >= 1) {
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nj) {
+        const int64_t i = chunk0 + t + static_cast<int64_t>(kT) * j;
+        v[j] = from_x ? f.x[c * f.npad + i] : signed_op_value(f, c, i);
+      }
+#pragma unroll
+    for (int kk = 8; kk >= 1; kk >>= 1)
+      if (kk < nj)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < nj && (j & kk) == 0) {
+            const double a = v[j], b = v[j + kk];
+            v[j] = a + b;
+            v[j + kk] = a - b;
+          }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nj) xs[t + kT * j] = v[j];
+  } else {
+    for (int e = t; e < ch32; e += kT) xs[e] = from_x ? f.x[c * f.npad + chunk0 + e] : signed_op_value(f, c, chunk0 + e);
+  }
+  __syncthreads();
+  int lh = 0;
+  const int local = nj >= 1 ? kT : ch32;  // strides below this are still to do
+  while ((2 << lh) <= local) ++lh;
+  for (--lh; lh >= 0; --lh) {
+    const int h = 1 << lh;
+#pragma unroll 4
+    for (int e = t; e < (ch32 >> 1); e += kT) {
+      const int i0 = ((e >> lh) << (lh + 1)) + (e & (h - 1));
+      const double a = xs[i0], b = xs[i0 + h];
+      xs[i0] = a + b;
+      xs[i0 + h] = a - b;
+    }
+    __syncthreads();
+  }
+  for (int k = f.boff[q] + t; k < f.boff[q + 1]; k += kT) f.sa[f.tslot[k] + c * f.m] = xs[f.tpos[k] - chunk0] * f.scale;
+}
+
+// CH = 8192 specialisation: the 13 local strides as three register passes
+// (bits 12-9, 8-5, 4-0), each a 16- or 32-point transform held by one thread,
+// with one shared-memory round trip between passes (padded layout i + i/32:
+// every access conflict-free) instead of one per stride.
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 5); }
+
+template <int N>
+__device__ __forceinline__ void fwht_regs(double (&v)[N]) {  // strides N/2 ... 1 over the register index
+#pragma unroll
+  for (int kk = N / 2; kk >= 1; kk >>= 1)
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if ((j & kk) == 0) {
+        const double a = v[j], b = v[j + kk];
+        v[j] = a + b;
+        v[j + kk] = a - b;
+      }
+}
+
+__global__ void __launch_bounds__(kFwhtChunkThreads) fwht_chunk8192_kernel(FwhtArgs f, bool from_x) {
+  extern __shared__ __align__(16) double xs[];  // fpad(8192) doubles
+  constexpr int CH = 8192;
+  const int64_t chunks = f.npad / CH;
+  const int64_t c = blockIdx.x / chunks, q = blockIdx.x - c * chunks;
+  const int64_t chunk0 = q * CH;
+  const int t = threadIdx.x;
+  {  // pass A: bits 12-9 (strides 4096 .. 512); thread t = bits 8-0
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t i = chunk0 + t + 512 * j;
+      v[j] = from_x ? f.x[c * f.npad + i] : signed_op_value(f, c, i);
+    }
+    fwht_regs<16>(v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[fpad(t + 512 * j)] = v[j];
+  }
+  __syncthreads();
+  {  // pass B: bits 8-5 (strides 256 .. 32); thread t = (bits 12-9, bits 4-0)
+    const int hi = t >> 5, lo = t & 31;
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = xs[fpad((hi << 9) | (j << 5) | lo)];
+    fwht_regs<16>(v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[fpad((hi << 9) | (j << 5) | lo)] = v[j];
+  }
+  __syncthreads();
+  if (t < 256) {  // pass C: bits 4-0 (strides 16 .. 1); thread t = bits 12-5
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = xs[fpad((t << 5) | j)];
+    fwht_regs<32>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) xs[fpad((t << 5) | j)] = v[j];
+  }
+  __syncthreads();
+  for (int k = f.boff[q] + t; k < f.boff[q + 1]; k += kFwhtChunkThreads)
+    f.sa[f.tslot[k] + c * f.m] = xs[fpad(static_cast<int>(f.tpos[k] - chunk0))] * f.scale;
+}
+
+// Dense operators with n_pad <= 2^5 * 8192 take the two-pass path.
+bool fwht2_ok(const FwhtArgs& f) { return f.npad >= 2 && f.npad <= 32 * kFwhtMaxChunk; }
+int64_t fwht2_chunk(int64_t npad) { return std::min<int64_t>(npad, kFwhtMaxChunk); }
+
+void launch_fwht2(FwhtArgs f, cudaStream_t stream) {
+  const int64_t ch = fwht2_chunk(f.npad);
+  int qb = 0;
+  while ((ch << qb) < f.npad) ++qb;
+  if (qb > 0) {
+    const int64_t work = ch * f.d;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(work, 256), 148 * 16));
+    switch (qb) {
+      case 1: fwht_top_kernel<1><<<blocks, 256, 0, stream>>>(f, ch); break;
+      case 2: fwht_top_kernel<2><<<blocks, 256, 0, stream>>>(f, ch); break;
+      case 3: fwht_top_kernel<3><<<blocks, 256, 0, stream>>>(f, ch); break;
+      case 4: fwht_top_kernel<4><<<blocks, 256, 0, stream>>>(f, ch); break;
+      default: fwht_top_kernel<5><<<blocks, 256, 0, stream>>>(f, ch); break;
+    }
+    RP_LAUNCH_CHECK();
+  }
+  if (ch == 8192) {
+    const size_t smem = static_cast<size_t>(8192 + 8192 / 32) * sizeof(double);
+    RP_CUDA(cudaFuncSetAttribute(fwht_chunk8192_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    fwht_chunk8192_kernel<<<static_cast<unsigned>(f.d * (f.npad / ch)), kFwhtChunkThreads, smem, stream>>>(f, qb > 0);
+    RP_LAUNCH_CHECK();
+    return;
+  }
+  const size_t smem = static_cast<size_t>(ch) * sizeof(double);
+  RP_CUDA(cudaFuncSetAttribute(fwht_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  fwht_chunk_kernel<<<static_cast<unsigned>(f.d * (f.npad / ch)), kFwhtChunkThreads, smem, stream>>>(f, ch, qb > 0);
+  RP_LAUNCH_CHECK();
+}
+
 void launch_fwht(FwhtArgs f, int bits, cudaStream_t stream) {
   const int S = 1 << bits;
   int logW = 0;
@@ -396,7 +588,15 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
           rem -= w;
         }
       }
-      const int last_bits = widths.back();
+      FwhtArgs probe{};
+      probe.npad = npad;
+      const bool two_pass = !op.sparse && fwht2_ok(probe);
+      // (two-pass path: targets bucketed per CH-row chunk)
+      const int last_bits = two_pass ? [&] {
+        int lb = 0;
+        while ((int64_t{1} << lb) < fwht2_chunk(npad)) ++lb;
+        return lb;
+      }() : widths.back();
       // Targets sorted by position, bucketed per block of the last pass.
       std::vector<int64_t> hrows(static_cast<size_t>(m));
       RP_CUDA(cudaMemcpyAsync(hrows.data(), rows.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToHost, stream));
@@ -423,7 +623,8 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       RP_CUDA(cudaMemcpyAsync(d_tpos.get(), tpos.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, stream));
       RP_CUDA(cudaMemcpyAsync(d_meta.get(), meta.data(), sizeof(int32_t) * meta.size(), cudaMemcpyHostToDevice,
                               stream));
-      DBuf<double> x(static_cast<size_t>(npad * d), stream);
+      DBuf<double> x;  // pass scratch (not needed when one chunk holds the whole transform)
+      if (!two_pass || npad > fwht2_chunk(npad)) x.alloc(static_cast<size_t>(npad * d), stream);
       FwhtArgs f{};
       f.x = x.get();
       f.npad = npad;
@@ -441,6 +642,11 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       f.sa = d_sa;
       f.m = m;
       const bool first_from_op = !op.sparse;
+      if (two_pass) {
+        launch_fwht2(f, stream);
+        RP_CUDA(cudaStreamSynchronize(stream));  // host target tables must outlive the copies
+        return;
+      }
       if (op.sparse) {
         zero_fill<<<grid_for(npad * d), 256, 0, stream>>>(x.get(), npad, d, npad);
         RP_LAUNCH_CHECK();
