@@ -287,6 +287,7 @@ struct rp_ctx {
   bool profile = false;
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
+  bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   std::string err;
 };
 
@@ -381,6 +382,11 @@ struct GramOp {
   // (rp_gram_apply); the recursion keeps one code path for every width so a
   // column's bits do not depend on how many problems are batched with it.
   bool allow_fused = false;
+  // Column-stable products (a column's bits independent of the batch width,
+  // the reference's matrix-vs-vector contract): on for the basis API, optional
+  // for the path (option "stable_columns"), where the split-K factor may then
+  // follow the problem's width.
+  bool col_stable = true;
   DBuf<double> G;  // D x D when matrix
   DBuf<double> tmp;
 
@@ -403,7 +409,7 @@ struct GramOp {
       g.ldb = op.d;
       g.c = Y;
       g.ldc = op.d;
-      g.col_stable = true;
+      g.col_stable = col_stable;
       g.partials = out;
       if (epi && dgemm_split(g) > 1) {
         // split-K product: the partials stay deferred and the recursion's
@@ -460,6 +466,7 @@ struct GramOp {
 struct PrecondBatch {
   int64_t m = 0, d = 0, L = 0;
   bool woodbury = false;
+  bool col_stable = true;  // (see GramOp::col_stable)
   const double* sa = nullptr;  // m x d
   std::vector<double> lambda0;
   DBuf<double> d_lambda0;
@@ -876,6 +883,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     taus.push_back(plans[l].params.alpha);
     ks.push_back(plans[l].params.k);
   }
+  P.col_stable = ctx->stable_columns;
+  gram.col_stable = ctx->stable_columns;
   if (Lo > 0) P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
   RP_CUDA(cudaEventRecord(ev.ev[2], s));
   // 5) Bases for all owned intervals at once; diverged intervals are retried
@@ -898,6 +907,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
         kr.push_back(ks[retry[j]]);
         retry_slot[retry[j]] = static_cast<int>(j);
       }
+      P2.col_stable = ctx->stable_columns;
       P2.build(ctx, sa.get(), nullptr, spec.m, dim, l0r);
       run_basis(ctx, gram, P2, cbuf.get(), K, taur, kr, run2);
       for (int v : run2.diverged) failed |= v;
@@ -1233,6 +1243,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->profile = value != 0;
     } else if (k == "fuse_update") {
       ctx->fuse_update = value != 0;
+    } else if (k == "stable_columns") {
+      ctx->stable_columns = value != 0;
     } else {
       throw InvalidArgument("unknown option: " + k);
     }

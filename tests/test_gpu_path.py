@@ -102,14 +102,25 @@ def test_matrix_basis_equals_vector_runs_bitwise(rp, ctx, oracle):  # :212-237
 
 
 def test_matrix_path_columns_equal_vector_paths(rp, ctx, oracle):
+    """With the "stable_columns" option (default on) the path's GEMMs split K
+    by K alone, so a matrix path's columns equal the vector paths bit for bit
+    (as the basis API, test_path_solver.cpp:212-237); with it off the split
+    follows the problem width and columns agree to rounding."""
     w = workloads.c1(scale=0.25)
     (oa, ocfg, ospec, orho), (ga, gcfg, gspec, grho) = _mirror(rp, oracle, w)
     B = np.asfortranarray(np.column_stack([w.b[:, 0], 2 * w.b[:, 0] + 1, np.zeros(w.b.shape[0])]))
-    joint = rp.ihs_bin_path_matrix(ga, B, gcfg, gspec, grho, ctx=ctx)
-    for col in range(3):
-        solo = rp.ihs_bin_path(ga, B[:, col].copy(), gcfg, gspec, grho, ctx=ctx)
-        for pj, ps in zip(joint.points, solo.points):
-            assert np.array_equal(pj.solution[:, col], ps.solution[:, 0])
+    for stable in (1, 0):
+        ctx.set_option("stable_columns", stable)
+        joint = rp.ihs_bin_path_matrix(ga, B, gcfg, gspec, grho, ctx=ctx)
+        for col in range(3):
+            solo = rp.ihs_bin_path(ga, B[:, col].copy(), gcfg, gspec, grho, ctx=ctx)
+            for pj, ps in zip(joint.points, solo.points):
+                if stable:
+                    assert np.array_equal(pj.solution[:, col], ps.solution[:, 0])
+                else:
+                    assert oracle.rel_error(pj.solution[:, col], ps.solution[:, 0]) < 1e-12 or \
+                        np.linalg.norm(ps.solution[:, 0]) == 0.0
+    ctx.set_option("stable_columns", 1)
 
 
 def test_single_point_path_equals_manual_pipeline(rp, ctx, oracle):  # :256-276
