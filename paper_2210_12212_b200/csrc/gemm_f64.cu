@@ -226,6 +226,160 @@ struct TileCopier {
   }
 };
 
+// GEMM epilogue shared by the cp.async and TMA kernels: accumulators -> the
+// consumer of C (store / mirror / recursion epilogue, or split-K partials).
+// Every thread of the CTA must call it (it contains CTA barriers); `active`
+// marks the compute threads (tid < C::THREADS) that hold accumulators and do
+// element work.
+template <class C, int BM, int WN, int STAGES>
+__device__ __forceinline__ void gemm_epilogue(const KParams& p, double (&acc)[C::FM][C::FN][2], double* smem, int tid,
+                                              bool active, int wm, int wn, int r8, int k4, int64_t m0, int64_t n0,
+                                              int64_t b1, int64_t b2, int64_t bidx, int sidx) {
+  // Epilogue, staged through shared memory one warp-column (BM x TN) at a
+  // time: the accumulators leave registers once, and every global access below
+  // walks rows fastest (coalesced, column-major C).  Split-K: each split
+  // publishes its partial tile; the last one to finish (tile counter) sums the
+  // partials in split order 0..S-1 -- an order independent of launch timing --
+  // and runs the consumer.
+  constexpr int SLD = BM + 2;  // conflict-free fragment stores
+  static_assert(SLD * C::TN <= STAGES * (C::A_STAGE + C::B_STAGE), "epilogue staging does not fit");
+  double* Cb = p.c + b1 * p.stride_c + b2 * p.stride_c2;
+  const int64_t mn = p.m * p.n;
+  double* W = p.split > 1 ? p.ws + bidx * p.split * mn : nullptr;
+  auto for_tile = [&](int w, auto&& fn) {  // fn(row, col, smem value) over warp-column w
+    if (!active) return;
+    for (int idx = tid; idx < BM * C::TN; idx += C::THREADS) {
+      const int rr = idx % BM, cc = idx / BM;
+      const int64_t row = m0 + rr, col = n0 + w * C::TN + cc;
+      if (row < p.m && col < p.n && !(p.lower_only && row < col)) fn(row, col, smem[cc * SLD + rr]);
+    }
+  };
+  auto stage = [&](int w) {
+    __syncthreads();
+    if (active && wn == w) {
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) smem[(j * 8 + 2 * k4 + e) * SLD + wm * C::TM + i * 8 + r8] = acc[i][j][e];
+    }
+    __syncthreads();
+  };
+  // C = reduced values of warp-column w (in smem) -> consumer.  Loads are
+  // issued U elements at a time before any store, so the L2 latency of the
+  // read-modify-write consumers overlaps.
+  constexpr int U = 4;
+  constexpr int PER = BM * C::TN;
+  __shared__ ColInfo cinfo[C::TN];
+  auto finish = [&](int w) {
+    const int64_t col0 = n0 + w * C::TN;
+    if (p.epi.kind != 0) {
+      if (tid < C::TN && col0 + tid < p.n) cinfo[tid] = column_info(p.epi, b1, col0 + tid);
+      __syncthreads();
+    }
+    if (!active) {
+      if (p.epi.kind == 0 && p.mirror) __syncthreads();
+    } else if (p.epi.kind == 0) {
+      for (int idx = tid; idx < PER; idx += C::THREADS) {
+        const int rr = idx % BM, cc = idx / BM;
+        const int64_t row = m0 + rr, col = col0 + cc;
+        if (row < p.m && col < p.n && !(p.lower_only && row < col)) {
+          double* dst = Cb + row + col * p.ldc;
+          const double v = smem[cc * SLD + rr];
+          *dst = (p.beta == 0.0) ? p.alpha * v : p.alpha * v + p.beta * (*dst);
+        }
+      }
+      if (p.mirror) {
+        __syncthreads();
+        for (int idx = tid; idx < PER; idx += C::THREADS) {
+          const int cc = idx % C::TN, rr = idx / C::TN;
+          const int64_t row = m0 + rr, col = col0 + cc;
+          if (row < p.m && col < p.n && row > col) Cb[col + row * p.ldc] = p.alpha * smem[cc * SLD + rr];
+        }
+      }
+    } else if (p.epi.kind == RecursionEpilogue::kArgs) {
+      const double* __restrict__ gen = p.epi.gen;
+      double* __restrict__ args = p.epi.args;
+      for (int base = tid; base < PER; base += U * C::THREADS) {
+        double pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+          pv[u] = 0.0;
+          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].src >= 0)
+            pv[u] = __ldcg(gen + cinfo[cc].src + m0 + rr);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n) {
+            const ColInfo ci = cinfo[cc];
+            double a = __dmul_rn(ci.s, smem[cc * SLD + rr]);
+            if (ci.src >= 0) a = __dadd_rn(a, pv[u]);
+            args[ci.dst + m0 + rr] = a;
+          }
+        }
+      }
+    } else {  // kUpdate
+      double* __restrict__ gen = p.epi.gen;
+      double* __restrict__ tilde = p.epi.tilde;
+      double* __restrict__ args = p.epi.args;
+      bool bad = false;
+      for (int base = tid; base < PER; base += U * C::THREADS) {
+        double gv[U], tv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+          gv[u] = tv[u] = 0.0;
+          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].dst >= 0) {
+            gv[u] = __ldcg(gen + cinfo[cc].dst + m0 + rr);
+            tv[u] = __ldcg(tilde + cinfo[cc].dst + m0 + rr);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].dst >= 0) {
+            const ColInfo ci = cinfo[cc];
+            const double v = smem[cc * SLD + rr];
+            const double nv = ci.s != 0.0 ? __dsub_rn(gv[u], v) : -v;
+            gen[ci.dst + m0 + rr] = nv;
+            tilde[ci.dst + m0 + rr] = __dadd_rn(tv[u], nv);
+            bad |= !isfinite(nv);
+            if (ci.src >= 0) args[ci.src + m0 + rr] = nv;
+          }
+        }
+      }
+      if (bad) p.epi.flags[b1] = 1;
+    }
+    __syncthreads();  // smem / cinfo are reused by the next warp-column
+  };
+  if (p.split > 1) {
+    if (!active) return;
+    // split-K: this split's partial tile goes straight from registers to the
+    // workspace; the sum over splits (in split order) happens in the consumer
+    // (deferred Partials) or in splitk_reduce
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int64_t row = m0 + wm * C::TM + i * 8 + r8;
+      if (row >= p.m) continue;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = n0 + wn * C::TN + j * 8 + 2 * k4 + e;
+          if (col < p.n && !(p.lower_only && row < col)) W[sidx * mn + row + col * p.m] = acc[i][j][e];
+        }
+    }
+    return;
+  }
+  for (int w = 0; w < WN; ++w) {
+    stage(w);
+    finish(w);
+  }
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
 __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
@@ -310,146 +464,7 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
     }
   }
   cp_async_wait<0>();
-
-  // Epilogue, staged through shared memory one warp-column (BM x TN) at a
-  // time: the accumulators leave registers once, and every global access below
-  // walks rows fastest (coalesced, column-major C).  Split-K: each split
-  // publishes its partial tile; the last one to finish (tile counter) sums the
-  // partials in split order 0..S-1 -- an order independent of launch timing --
-  // and runs the consumer.
-  constexpr int SLD = BM + 2;  // conflict-free fragment stores
-  static_assert(SLD * C::TN <= STAGES * (C::A_STAGE + C::B_STAGE), "epilogue staging does not fit");
-  double* Cb = p.c + b1 * p.stride_c + b2 * p.stride_c2;
-  const int64_t mn = p.m * p.n;
-  double* W = p.split > 1 ? p.ws + bidx * p.split * mn : nullptr;
-  auto for_tile = [&](int w, auto&& fn) {  // fn(row, col, smem value) over warp-column w
-    for (int idx = tid; idx < BM * C::TN; idx += C::THREADS) {
-      const int rr = idx % BM, cc = idx / BM;
-      const int64_t row = m0 + rr, col = n0 + w * C::TN + cc;
-      if (row < p.m && col < p.n && !(p.lower_only && row < col)) fn(row, col, smem[cc * SLD + rr]);
-    }
-  };
-  auto stage = [&](int w) {
-    __syncthreads();
-    if (wn == w) {
-#pragma unroll
-      for (int i = 0; i < C::FM; ++i)
-#pragma unroll
-        for (int j = 0; j < C::FN; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) smem[(j * 8 + 2 * k4 + e) * SLD + wm * C::TM + i * 8 + r8] = acc[i][j][e];
-    }
-    __syncthreads();
-  };
-  // C = reduced values of warp-column w (in smem) -> consumer.  Loads are
-  // issued U elements at a time before any store, so the L2 latency of the
-  // read-modify-write consumers overlaps.
-  constexpr int U = 4;
-  constexpr int PER = BM * C::TN;
-  __shared__ ColInfo cinfo[C::TN];
-  auto finish = [&](int w) {
-    const int64_t col0 = n0 + w * C::TN;
-    if (p.epi.kind != 0) {
-      if (tid < C::TN && col0 + tid < p.n) cinfo[tid] = column_info(p.epi, b1, col0 + tid);
-      __syncthreads();
-    }
-    if (p.epi.kind == 0) {
-      for (int idx = tid; idx < PER; idx += C::THREADS) {
-        const int rr = idx % BM, cc = idx / BM;
-        const int64_t row = m0 + rr, col = col0 + cc;
-        if (row < p.m && col < p.n && !(p.lower_only && row < col)) {
-          double* dst = Cb + row + col * p.ldc;
-          const double v = smem[cc * SLD + rr];
-          *dst = (p.beta == 0.0) ? p.alpha * v : p.alpha * v + p.beta * (*dst);
-        }
-      }
-      if (p.mirror) {
-        __syncthreads();
-        for (int idx = tid; idx < PER; idx += C::THREADS) {
-          const int cc = idx % C::TN, rr = idx / C::TN;
-          const int64_t row = m0 + rr, col = col0 + cc;
-          if (row < p.m && col < p.n && row > col) Cb[col + row * p.ldc] = p.alpha * smem[cc * SLD + rr];
-        }
-      }
-    } else if (p.epi.kind == RecursionEpilogue::kArgs) {
-      const double* __restrict__ gen = p.epi.gen;
-      double* __restrict__ args = p.epi.args;
-      for (int base = tid; base < PER; base += U * C::THREADS) {
-        double pv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
-          pv[u] = 0.0;
-          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].src >= 0)
-            pv[u] = __ldcg(gen + cinfo[cc].src + m0 + rr);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
-          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n) {
-            const ColInfo ci = cinfo[cc];
-            double a = __dmul_rn(ci.s, smem[cc * SLD + rr]);
-            if (ci.src >= 0) a = __dadd_rn(a, pv[u]);
-            args[ci.dst + m0 + rr] = a;
-          }
-        }
-      }
-    } else {  // kUpdate
-      double* __restrict__ gen = p.epi.gen;
-      double* __restrict__ tilde = p.epi.tilde;
-      double* __restrict__ args = p.epi.args;
-      bool bad = false;
-      for (int base = tid; base < PER; base += U * C::THREADS) {
-        double gv[U], tv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
-          gv[u] = tv[u] = 0.0;
-          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].dst >= 0) {
-            gv[u] = __ldcg(gen + cinfo[cc].dst + m0 + rr);
-            tv[u] = __ldcg(tilde + cinfo[cc].dst + m0 + rr);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
-          if (idx < PER && m0 + rr < p.m && col0 + cc < p.n && cinfo[cc].dst >= 0) {
-            const ColInfo ci = cinfo[cc];
-            const double v = smem[cc * SLD + rr];
-            const double nv = ci.s != 0.0 ? __dsub_rn(gv[u], v) : -v;
-            gen[ci.dst + m0 + rr] = nv;
-            tilde[ci.dst + m0 + rr] = __dadd_rn(tv[u], nv);
-            bad |= !isfinite(nv);
-            if (ci.src >= 0) args[ci.src + m0 + rr] = nv;
-          }
-        }
-      }
-      if (bad) p.epi.flags[b1] = 1;
-    }
-    __syncthreads();  // smem / cinfo are reused by the next warp-column
-  };
-  if (p.split > 1) {
-    // split-K: this split's partial tile goes straight from registers to the
-    // workspace; the sum over splits (in split order) happens in the consumer
-    // (deferred Partials) or in splitk_reduce
-#pragma unroll
-    for (int i = 0; i < C::FM; ++i) {
-      const int64_t row = m0 + wm * C::TM + i * 8 + r8;
-      if (row >= p.m) continue;
-#pragma unroll
-      for (int j = 0; j < C::FN; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t col = n0 + wn * C::TN + j * 8 + 2 * k4 + e;
-          if (col < p.n && !(p.lower_only && row < col)) W[sidx * mn + row + col * p.m] = acc[i][j][e];
-        }
-    }
-    return;
-  }
-  for (int w = 0; w < WN; ++w) {
-    stage(w);
-    finish(w);
-  }
+  gemm_epilogue<C, BM, WN, STAGES>(p, acc, smem, tid, true, wm, wn, r8, k4, m0, n0, b1, b2, bidx, sidx);
 }
 
 // Deterministic split-K reduction: partials summed in split order 0..S-1;
