@@ -10,8 +10,10 @@
 // free of shared-memory bank conflicts within each half-warp.
 #include "common.h"
 #include "gemm_f64.h"
+#include "tma_util.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -467,6 +469,128 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   gemm_epilogue<C, BM, WN, STAGES>(p, acc, smem, tid, true, wm, wn, r8, k4, m0, n0, b1, b2, bidx, sidx);
 }
 
+// TMA + mbarrier variant: one producer warp streams both operand tiles with
+// 4-D tensor boxes (inner, outer, batch, batch2) into a STAGES-deep ring;
+// the WM x WN compute warps wait on per-stage "full" barriers and release
+// stages through "empty" barriers -- no CTA-wide barrier in the main loop.
+// Boxes are 4 elements wider than the tile along the contiguous dimension,
+// which reproduces the padded shared-memory layouts of the cp.async kernel
+// (conflict-free fragment loads); the extra elements are never read.  The
+// arithmetic (k order, fragment mapping, epilogue) is the cp.async kernel's,
+// so both produce identical bits.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+__global__ void __launch_bounds__((WM * WN + 1) * 32)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, KParams p,
+                     int a_batched, int a_batched2, int b_batched, int b_batched2) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
+  extern __shared__ __align__(128) double smem_raw[];
+  // 128-byte aligned ring (TMA destinations); the launch adds 128 B of slack
+  double* smem = smem_raw + (((128u - (tma::smem_u32(smem_raw) & 127u)) & 127u) >> 3);
+  double* As = smem;
+  double* Bs = smem + STAGES * C::A_STAGE;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool compute = warp < WM * WN;
+  const int wm = warp % WM;
+  const int wn = warp / WM;
+
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
+  if (p.lower_only && m0 + BM <= n0) return;
+  const int64_t z = blockIdx.z;
+  const int64_t bidx = z / p.split;
+  const int sidx = static_cast<int>(z % p.split);
+  const int64_t b1 = bidx % p.batch, b2 = bidx / p.batch;
+  int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
+  const int64_t kend = min(p.k, kbeg + p.k_chunk);
+  if (p.tri_k) kbeg = max(kbeg, m0 & ~static_cast<int64_t>(BK - 1));
+  const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
+
+  if (tid == 0) {
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      tma::mbar_init(&full[s2], 1);
+      tma::mbar_init(&empty[s2], WM * WN);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  constexpr uint32_t kStageBytes = (C::A_STAGE + C::B_STAGE) * 8;
+  if (!compute) {
+    if (lane == 0) {
+      const int ab1 = a_batched ? static_cast<int>(b1) : 0, ab2 = a_batched2 ? static_cast<int>(b2) : 0;
+      const int bb1 = b_batched ? static_cast<int>(b1) : 0, bb2 = b_batched2 ? static_cast<int>(b2) : 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int k0 = static_cast<int>(kbeg + static_cast<int64_t>(kt) * BK);
+        tma::mbar_wait(&empty[stage], phase ^ 1);
+        tma::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+        // A: op(A) is m x k; K-major (AK): inner = k; else inner = m
+        if (AK)
+          tma::load_4d(As + stage * C::A_STAGE, &amap, k0, static_cast<int>(m0), ab1, ab2, &full[stage]);
+        else
+          tma::load_4d(As + stage * C::A_STAGE, &amap, static_cast<int>(m0), k0, ab1, ab2, &full[stage]);
+        if (BKM)
+          tma::load_4d(Bs + stage * C::B_STAGE, &bmap, k0, static_cast<int>(n0), bb1, bb2, &full[stage]);
+        else
+          tma::load_4d(Bs + stage * C::B_STAGE, &bmap, static_cast<int>(n0), k0, bb1, bb2, &full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int r8 = lane >> 2;
+    const int k4 = lane & 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kt = 0; kt < ktiles; ++kt) {
+      tma::mbar_wait(&full[stage], phase);
+      const double* as = As + stage * C::A_STAGE;
+      const double* bs = Bs + stage * C::B_STAGE;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[C::FM], bf[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) {
+          const int row = wm * C::TM + i * 8 + r8;
+          af[i] = AK ? as[row * C::A_LD + kk + k4] : as[(kk + k4) * C::A_LD + row];
+        }
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) {
+          const int col = wn * C::TN + j * 8 + r8;
+          bf[j] = BKM ? bs[col * C::B_LD + kk + k4] : bs[(kk + k4) * C::B_LD + col];
+        }
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      // (the DMMAs above consumed every fragment: the stage may be refilled)
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();  // ring drained: the stages become the epilogue's staging area
+  gemm_epilogue<C, BM, WN, STAGES>(p, acc, smem, tid, compute, wm, wn, lane >> 2, lane & 3, m0, n0, b1, b2, bidx,
+                                   sidx);
+}
+
 // Deterministic split-K reduction: partials summed in split order 0..S-1;
 // lower_only + mirror also writes the transposed element.
 __global__ void splitk_reduce(KParams p) {
@@ -517,9 +641,75 @@ double* workspace(size_t bytes, cudaStream_t stream) {
   return g_ws.ptr;
 }
 
+// ---- TMA launch path -------------------------------------------------------------
+
+bool g_tma_enabled = [] {
+  const char* e = std::getenv("RP_GEMM_TMA");
+  return !(e && e[0] == '0');
+}();
+
+// 4-D tensor map of one operand: dims (inner, outer, batch, batch2) with the
+// given box (inner is the contiguous dimension).  A batch dimension with zero
+// stride (operand shared by the batch) becomes extent 1 (coordinate 0).
+bool operand_map(CUtensorMap* map, const double* base, int64_t inner, int64_t outer, int64_t ld, int64_t s1,
+                 int64_t n1, int64_t s2, int64_t n2, int box_inner, int box_outer, int* batched1, int* batched2) {
+  auto enc = tma::encoder();
+  if (!enc) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0 || ld % 2 != 0 || s1 % 2 != 0 || s2 % 2 != 0) return false;
+  if (inner <= 0 || outer <= 0 || inner >= (int64_t{1} << 31) || outer >= (int64_t{1} << 31)) return false;
+  *batched1 = (n1 > 1 && s1 != 0) ? 1 : 0;
+  *batched2 = (n2 > 1 && s2 != 0) ? 1 : 0;
+  const int64_t span = ld * outer;  // (placeholder stride of an unused dimension)
+  const int64_t st1 = *batched1 ? s1 : span, st2 = *batched2 ? s2 : span * (*batched1 ? n1 : 1);
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer),
+                              static_cast<cuuint64_t>(*batched1 ? n1 : 1), static_cast<cuuint64_t>(*batched2 ? n2 : 1)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 8, static_cast<cuuint64_t>(st1) * 8,
+                                 static_cast<cuuint64_t>(st2) * 8};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer), 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
+  CUtensorMap amap, bmap;
+  int ab1 = 0, ab2 = 0, bb1 = 0, bb2 = 0;
+  // op(A) is m x k: K-major (AK) -> inner k, box (BK + 4) x BM; else inner m, box (BM + 4) x BK
+  const bool ok_a = AK ? operand_map(&amap, kp.a, kp.k, kp.m, kp.lda, kp.stride_a, kp.batch, kp.stride_a2, kp.batch2,
+                                     BK + 4, BM, &ab1, &ab2)
+                       : operand_map(&amap, kp.a, kp.m, kp.k, kp.lda, kp.stride_a, kp.batch, kp.stride_a2, kp.batch2,
+                                     BM + 4, BK, &ab1, &ab2);
+  if (!ok_a) return false;
+  const bool ok_b = BKM ? operand_map(&bmap, kp.b, kp.k, kp.n, kp.ldb, kp.stride_b, kp.batch, kp.stride_b2,
+                                      kp.batch2, BK + 4, BN, &bb1, &bb2)
+                        : operand_map(&bmap, kp.b, kp.n, kp.k, kp.ldb, kp.stride_b, kp.batch, kp.stride_b2,
+                                      kp.batch2, BN + 4, BK, &bb1, &bb2);
+  if (!ok_b) return false;
+  auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
+  constexpr int smem = C::SMEM_BYTES + 128;
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
+            static_cast<unsigned>(kp.batch * kp.batch2 * kp.split));
+  kern<<<grid, C::THREADS + 32, smem, stream>>>(amap, bmap, kp, ab1, ab2, bb1, bb2);
+  RP_LAUNCH_CHECK();
+  return true;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
 void launch_cfg(const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+  if constexpr (VEC == 2) {
+    if (g_tma_enabled && ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
+        launch_tma_cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>(kp, stream))
+      return;
+  }
   auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
@@ -566,6 +756,21 @@ void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
 }  // namespace
 
 int choose_split(const GemmArgs& g);
+
+namespace tma {
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+}  // namespace tma
 
 int dgemm_last_launches() { return g_last_launches; }
 
@@ -715,8 +920,10 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     // profiles/gemm_tune_r01.txt)
     // (profiles/r01_gemm_tune.txt: large-problem throughput relative to the
     // best shape; 9, 10 = BK 32 variants, kept for tuning only)
+    // (TMA kernel, the default path; the 4-warp shapes 7, 8 only pay off in
+    // the cp.async kernel)
     static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2};
-    static constexpr double kEff[] = {0.82, 0.95, 0.92, 0.93, 0.75, 0.96, 0.95, 0.90, 1.0, 0.0, 0.0};
+    static constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99};
     double best = 1e300;
     for (int t = 0; t < kNumTiles; ++t) {
       if (kTiles[t].bn == 16 && g.n > 16) continue;
