@@ -292,7 +292,7 @@ def run_ours(args, w):
     tot_s = sum(p.total_seconds for p in prof)
     peak = measure_dgemm_peak(torch)
     achieved = g_f / g_s / 1e12 if g_s > 0 else 0.0
-    roofline = {"bound": "tensor", "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, all GEMMs of the path)",
+    roofline = {"bound": "tensor", "kernel": "dgemm_tma_kernel / dgemm_kernel (FP64 DMMA m8n8k4, TMA-fed; all GEMMs of the path)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                 "traffic": None, "share_of_step": g_s / tot_s if tot_s else None,
                 "gemm_launches_per_step": g_calls / len(prof),
