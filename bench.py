@@ -292,9 +292,23 @@ def run_ours(args, w):
     tot_s = sum(p.total_seconds for p in prof)
     peak = measure_dgemm_peak(torch)
     achieved = g_f / g_s / 1e12 if g_s > 0 else 0.0
+    # DRAM traffic per launch of the representative top GEMM (the Gram product
+    # at the last generation, 1024 x 2016 x 1024) from the committed ncu
+    # --set full capture, beside that launch's algorithmic operand bytes.
+    traffic, traffic_note = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_gemm_tma.json")) as f:
+            rec = json.load(f)[0]
+        mb = float(rec["dram__bytes_read.sum"].split()[0]) + float(rec["dram__bytes_write.sum"].split()[0])
+        traffic = mb * 1e6
+        traffic_note = ("bytes per launch of %s (ncu, profiles/r01_ncu_gemm_tma.json); algorithmic "
+                        "operand bytes of that launch 8*(1024*1024 + 1024*2016 + 4*1024*2016) = 90 MB "
+                        "(split-K partials included)" % rec["kernel"][:60])
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": "dgemm_tma_kernel / dgemm_kernel (FP64 DMMA m8n8k4, TMA-fed; all GEMMs of the path)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                "traffic": None, "share_of_step": g_s / tot_s if tot_s else None,
+                "traffic": traffic, "traffic_note": traffic_note, "share_of_step": g_s / tot_s if tot_s else None,
                 "gemm_launches_per_step": g_calls / len(prof),
                 "gemm_flops_per_step": g_f / len(prof),
                 "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul fp64) measured in this run; "
