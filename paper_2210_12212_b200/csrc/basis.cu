@@ -93,15 +93,14 @@ __global__ void compose_kernel(BasisDims d, const double* __restrict__ tilde, co
   }
 }
 
-__global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, int64_t stride,
-                                     const double* __restrict__ args, const double* __restrict__ t3,
-                                     const double* __restrict__ lambda0, double* __restrict__ out) {
+__global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, const double* __restrict__ args,
+                                     int64_t s_args, const double* __restrict__ t3, int64_t s_t3,
+                                     const double* __restrict__ lambda0, double* __restrict__ out, int64_t s_out) {
   const int64_t per = dim * cols;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < per * L;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t l = idx / per, e = idx % per;
-    const int64_t o = l * stride + e;
-    out[o] = __ddiv_rn(__dsub_rn(args[o], t3[o]), lambda0[l]);
+    out[l * s_out + e] = __ddiv_rn(__dsub_rn(args[l * s_args + e], t3[l * s_t3 + e]), lambda0[l]);
   }
 }
 
@@ -253,9 +252,11 @@ void compose(const BasisDims& d, const double* tilde, const double* d_tau, const
   });
 }
 
-void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,
-                   const double* d_lambda0, double* out, cudaStream_t stream) {
-  woodbury_tail_kernel<<<grid_for(dim * cols * L), 256, 0, stream>>>(dim, cols, L, stride, args, t3, d_lambda0, out);
+void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t s_args, const double* args, int64_t s_t3,
+                   const double* t3, const double* d_lambda0, int64_t s_out, double* out, cudaStream_t stream) {
+  if (dim <= 0 || cols <= 0 || L <= 0) return;
+  woodbury_tail_kernel<<<grid_for(dim * cols * L), 256, 0, stream>>>(dim, cols, L, args, s_args, t3, s_t3, d_lambda0,
+                                                                     out, s_out);
   RP_LAUNCH_CHECK();
 }
 

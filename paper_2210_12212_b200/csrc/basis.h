@@ -51,9 +51,11 @@ void update_gen(const BasisDims& d, int64_t g, const Partials& applied, const in
 void compose(const BasisDims& d, const double* tilde, const double* d_tau, const int* d_k, const double* d_lambda,
              const int* d_interval, int64_t T, double* x, cudaStream_t stream);
 
-// out = (args - t3) / lambda0_l, interval-major (Woodbury preconditioner tail).
-void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t stride, const double* args, const double* t3,
-                   const double* d_lambda0, double* out, cudaStream_t stream);
+// out_l = (args_l - t3_l) / lambda0_l for l < L (Woodbury preconditioner tail);
+// each operand is dim x cols contiguous per interval at its own interval
+// stride (s_args = 0 broadcasts one input).
+void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t s_args, const double* args, int64_t s_t3,
+                   const double* t3, const double* d_lambda0, int64_t s_out, double* out, cudaStream_t stream);
 
 // Loss pieces (path_solver.cpp:425-454).  For output column j of R
 // (rows x cols, ld ldr): out[j] = sum_r (R[r, j] - B[r, j % K])^2 (B may be

@@ -36,6 +36,7 @@
 #include "operator.h"
 #include "ridgepath_b200.h"
 #include "sketch.h"
+#include "sparse_gram.h"
 
 namespace rpb {
 
@@ -221,6 +222,8 @@ struct OperatorStore {
   DBuf<int32_t> csr_col, csc_row;
   DBuf<double> csr_val, csc_val;
   int64_t nnz = 0;
+  // per-panel CSC of the primal / dual operator (sparse Gram passes), built lazily
+  PanelCsc panels_primal, panels_dual;
 
   // Primal operator M = A (rows local).
   OpView primal() const {
@@ -288,6 +291,8 @@ struct rp_ctx {
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
+  int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
+  int64_t csr_chunk = 64;            // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 64)
   std::string err;
 };
 
@@ -428,10 +433,26 @@ struct GramOp {
       allreduce(ctx, Y, op.d * cols);  // fused single pass over the operator
       return;
     }
+    if (op.sparse) {
+      // L2-blocked two passes per row panel (sparse_gram.cu): bit-identical to
+      // apply followed by apply_transpose, without the n x cols intermediate
+      sparse_gram(op.csr_off, op.csr_col, op.csr_val, panel_csc(ctx, op), W, op.d, cols, Y, op.d, ctx->csr_chunk, s);
+      allreduce(ctx, Y, op.d * cols);
+      return;
+    }
     const size_t need = static_cast<size_t>(op.n_loc * cols);
     if (tmp.size() < need) tmp.alloc(need, s);
     op_apply(ctx, op, W, cols, tmp.get());
     op_apply_t(ctx, op, tmp.get(), cols, Y, true);
+  }
+
+  static const PanelCsc& panel_csc(rp_ctx* ctx, const OpView& op) {
+    OperatorStore& st = ctx->op;
+    PanelCsc& pc = op.csr_off == st.csr_off.get() ? st.panels_primal : st.panels_dual;
+    if (!pc.matches(op.n_loc, op.d, op.nnz, ctx->csr_panel_rows))
+      build_panel_csc(op.csr_off, op.csr_col, op.csr_val, op.n_loc, op.d, op.nnz, ctx->csr_panel_rows, pc,
+                      ctx->stream);
+    return pc;
   }
 
   void build_matrix() {
@@ -555,21 +576,31 @@ struct PrecondBatch {
       dgemm(g, s);
       return;
     }
-    DBuf<double> t1(static_cast<size_t>(L * m * cols), s), t2(static_cast<size_t>(L * m * cols), s);
+    // Woodbury: SA is shared by every interval, so the two SA products run as
+    // single GEMMs over all L * cols columns (SA streamed once per call); only
+    // the m x m middle factor is batched per interval.  A broadcast input is
+    // multiplied by SA once.
+    const bool bcast = sin == 0;
+    const double* src = in;
+    DBuf<double> inb;
+    if (!bcast && sin != d * cols) {
+      inb.alloc(static_cast<size_t>(L * d * cols), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(in + l * sin, d, cols, d, inb.get() + l * d * cols, d, s);
+      src = inb.get();
+    }
+    const int64_t n1 = bcast ? cols : L * cols;
+    DBuf<double> t1(static_cast<size_t>(m * n1), s), t2(static_cast<size_t>(L * m * cols), s);
     DBuf<double> t3(static_cast<size_t>(L * d * cols), s);
-    GemmArgs g1;  // t1_l = SA in_l
+    GemmArgs g1;  // t1 = SA [in_0 .. in_{L-1}]
     g1.m = m;
-    g1.n = cols;
+    g1.n = n1;
     g1.k = d;
     g1.a = sa;
     g1.lda = m;
-    g1.b = in;
+    g1.b = src;
     g1.ldb = d;
-    g1.stride_b = sin;
     g1.c = t1.get();
     g1.ldc = m;
-    g1.stride_c = m * cols;
-    g1.batch = L;
     g1.col_stable = true;
     dgemm(g1, s);
     GemmArgs g2;  // t2_l = W_l t1_l
@@ -581,45 +612,28 @@ struct PrecondBatch {
     g2.stride_a = m * m;
     g2.b = t1.get();
     g2.ldb = m;
-    g2.stride_b = m * cols;
+    g2.stride_b = bcast ? 0 : m * cols;
     g2.c = t2.get();
     g2.ldc = m;
     g2.stride_c = m * cols;
     g2.batch = L;
     g2.col_stable = true;
     dgemm(g2, s);
-    GemmArgs g3;  // t3_l = SA^T t2_l
+    GemmArgs g3;  // t3 = SA^T [t2_0 .. t2_{L-1}]
     g3.opa = Op::T;
     g3.m = d;
-    g3.n = cols;
+    g3.n = L * cols;
     g3.k = m;
     g3.a = sa;
     g3.lda = m;
     g3.b = t2.get();
     g3.ldb = m;
-    g3.stride_b = m * cols;
     g3.c = t3.get();
     g3.ldc = d;
-    g3.stride_c = d * cols;
-    g3.batch = L;
     g3.col_stable = true;
     dgemm(g3, s);
-    // out_l = (in_l - t3_l) / l0_l   (in may be broadcast: materialize per l)
-    if (sin == 0) {
-      DBuf<double> inb(static_cast<size_t>(L * d * cols), s);
-      for (int64_t l = 0; l < L; ++l) copy_cols(in, d, cols, d, inb.get() + l * d * cols, d, s);
-      DBuf<double> o(static_cast<size_t>(L * d * cols), s);
-      woodbury_tail(d, cols, L, d * cols, inb.get(), t3.get(), d_lambda0.get(), o.get(), s);
-      for (int64_t l = 0; l < L; ++l) copy_cols(o.get() + l * d * cols, d, cols, d, out + l * sout, d, s);
-    } else if (sin == d * cols && sout == d * cols) {
-      woodbury_tail(d, cols, L, d * cols, in, t3.get(), d_lambda0.get(), out, s);
-    } else {
-      DBuf<double> o(static_cast<size_t>(L * d * cols), s);
-      DBuf<double> inb(static_cast<size_t>(L * d * cols), s);
-      for (int64_t l = 0; l < L; ++l) copy_cols(in + l * sin, d, cols, d, inb.get() + l * d * cols, d, s);
-      woodbury_tail(d, cols, L, d * cols, inb.get(), t3.get(), d_lambda0.get(), o.get(), s);
-      for (int64_t l = 0; l < L; ++l) copy_cols(o.get() + l * d * cols, d, cols, d, out + l * sout, d, s);
-    }
+    // out_l = (in_l - t3_l) / l0_l
+    woodbury_tail(d, cols, L, sin, in, d * cols, t3.get(), d_lambda0.get(), sout, out, s);
   }
 };
 
@@ -1245,6 +1259,12 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->fuse_update = value != 0;
     } else if (k == "stable_columns") {
       ctx->stable_columns = value != 0;
+    } else if (k == "csr_panel_rows") {
+      require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
+      ctx->csr_panel_rows = value;
+    } else if (k == "csr_chunk") {
+      require(value >= 1 && value <= 64, "csr_chunk must be in [1, 64]");
+      ctx->csr_chunk = value;
     } else {
       throw InvalidArgument("unknown option: " + k);
     }

@@ -1,0 +1,46 @@
+// Sparse Gram product Y = M^T (M W) for a CSR operator, L2-blocked
+// (reference: gram_apply for CsrMatrix = apply then apply_transpose,
+// ref/proj/core/src/matrix.cpp:140-172).
+//
+// The operator's local rows are cut into panels of `panel_rows` rows and the
+// right-hand columns into chunks of <= 64.  Per (chunk, panel):
+//   pass 1  Y_p = M_p W_c            (warp per row, gathers rows of the
+//                                     row-major W_c, which stays in L2)
+//   pass 2  Z  = Z + M_p^T Y_p       (warp per column through the panel's own
+//                                     CSC, gathers rows of Y_p from L2)
+// so the n x cols intermediate M W never reaches HBM.  Pass 2 continues each
+// column's running sum across panels in ascending row order, which is exactly
+// the order of the reference's apply_transpose (out.row(c) += v * x.row(r),
+// rows ascending): the result is bit-identical to the unblocked two-pass
+// product and independent of the panel and chunk sizes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.h"
+
+namespace rpb {
+
+// CSC of every row panel of a CSR matrix (n local rows, d columns): entries of
+// panel p, column j are [off[p*d + j], off[p*d + j + 1]), rows ascending.
+struct PanelCsc {
+  int64_t n = 0, d = 0, nnz = 0, panel_rows = 0, panels = 0;
+  DBuf<int64_t> off;  // panels * d + 1
+  DBuf<int32_t> row;  // nnz, local row index
+  DBuf<double> val;   // nnz
+  bool matches(int64_t n_, int64_t d_, int64_t nnz_, int64_t pr) const {
+    return panels > 0 && n == n_ && d == d_ && nnz == nnz_ && panel_rows == pr;
+  }
+};
+
+// Build the panel CSC on the device (stable radix sort of (panel, column) keys).
+void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, int64_t n, int64_t d,
+                     int64_t nnz, int64_t panel_rows, PanelCsc& out, cudaStream_t s);
+
+// Y (d x cols, column-major, ld ldy) = M^T (M W), W (d x cols, column-major, ld ldw).
+void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelCsc& pc,
+                 const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s);
+
+}  // namespace rpb

@@ -358,3 +358,25 @@ def test_path_losses_match_oracle(rp, ctx, oracle):
                          rp.SketchSpec("gaussian", 80, 120, 1, 5), rp.RhoBounds.manual(1.0, 1e-5), ctx=ctx)
     for p in dpath.points:
         assert p.train_loss == pytest.approx(oracle.losses(aw, bw, p.solution[:, 0], p.lam)[0], rel=1e-12)
+
+
+def test_dual_csr_path_matches_oracle(rp, ctx, oracle):
+    """dual_path on a CSR operator (path_solver.cpp:329-351): the dual Gram
+    A A^T runs through the panel sparse passes on the transposed structure."""
+    rng = np.random.default_rng(21)
+    n, d = 60, 300
+    dense = np.where(rng.random((n, d)) < 0.1, rng.standard_normal((n, d)), 0.0)
+    b = rng.standard_normal(n)
+    c = oracle.Csr.from_dense(dense)
+    gc = rp.Csr(c.rows, c.cols, c.offsets, c.indices, c.values)
+    grid = oracle.log_grid(1e-1, 1e1, 12)
+    ref = oracle.dual_path(c, b, oracle.PathConfig(1e-1, 1e1, grid, 1e-6, None),
+                           oracle.SketchSpec("countsketch", 40, d, 1, 4), oracle.RhoBounds.manual(1.0, 1e-5))
+    try:
+        ctx.set_option("csr_panel_rows", 37)
+        got = rp.dual_path(gc, b, rp.PathConfig(1e-1, 1e1, list(grid), 1e-6), rp.SketchSpec("countsketch", 40, d, 1, 4),
+                           rp.RhoBounds.manual(1.0, 1e-5), ctx=ctx)
+    finally:
+        ctx.set_option("csr_panel_rows", 65536)
+    worst, npts = _worst(got.points, ref.points, oracle)
+    assert npts == len(grid) and worst < TOL

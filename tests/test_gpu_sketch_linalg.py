@@ -145,3 +145,37 @@ def test_narrow_passes(rp, ctx, oracle, n, d, k):
     for j in range(k):
         assert np.array_equal(rp.gram_apply(a, w[:, j].copy(), ctx=ctx), g_all[:, j])
         assert np.array_equal(rp.apply_transpose(a, y[:, j].copy(), ctx=ctx), t_all[:, j])
+
+
+@pytest.mark.parametrize("panel,chunk", [(65536, 64), (7, 64), (64, 5), (1, 1), (100, 33), (1000, 17)])
+def test_csr_panel_gram_bitwise(rp, ctx, oracle, panel, chunk):
+    """The L2-blocked sparse Gram (sparse_gram.cu) continues each column's
+    running sum across row panels, so it equals apply followed by
+    apply_transpose (matrix.cpp:168-172) bit for bit, whatever the panel and
+    chunk sizes; empty rows and empty columns included."""
+    rng = np.random.default_rng(11)
+    n, d = 523, 71
+    dense = np.where(rng.random((n, d)) < 0.08, rng.standard_normal((n, d)), 0.0)
+    dense[17] = 0.0  # empty row
+    dense[:, 5] = 0.0  # empty column
+    oc, gc = _csr(rp, oracle, dense)
+    x = rng.standard_normal((d, 150))  # > 2 chunks of 64
+    two_pass = rp.apply_transpose(gc, rp.apply(gc, x, ctx=ctx), ctx=ctx)
+    try:
+        ctx.set_option("csr_panel_rows", panel)
+        ctx.set_option("csr_chunk", chunk)
+        got = rp.gram_apply(gc, x, ctx=ctx)
+        assert np.array_equal(got, two_pass)
+        assert oracle.rel_error(got, oracle.gram_apply(oc, x)) < 1e-14
+        # a single column through the same kernels
+        assert np.array_equal(rp.gram_apply(gc, x[:, 3].copy(), ctx=ctx), two_pass[:, 3])
+    finally:
+        ctx.set_option("csr_panel_rows", 65536)
+        ctx.set_option("csr_chunk", 64)
+
+
+def test_csr_panel_gram_empty_matrix(rp, ctx, oracle):
+    dense = np.zeros((40, 9))
+    oc, gc = _csr(rp, oracle, dense)
+    got = rp.gram_apply(gc, np.ones((9, 3)), ctx=ctx)
+    assert np.array_equal(got, np.zeros((9, 3)))
