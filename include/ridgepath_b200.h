@@ -223,6 +223,38 @@ RP_API int32_t rp_auto_interval_count(double lambda_min, double lambda_max);
 RP_API rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_intervals, double* edges_out,
                             int32_t* count_out);
 
+/* ---- plug-in envelope (derive_rho, tools/ridgepath_main.cpp:218-279) ------
+ * The reference CLI derives (rho1, rho2) from the sketched spectrum when
+ * --rho1/--rho2 are absent: sketch A, thin SVD of SA, effective dimension at
+ * lambda0 = sqrt(lambda_min * lambda_max), then the family's envelope
+ * (spectrum.cpp:87-169).  rp_derive_rho does the same on the device for the
+ * context's operator (transpose_op = 1: A^T, the dual route) without an SVD:
+ * ||D||_F^2 = tr(H (H + lambda0 I)^{-1}) and s_max^2 = lambda_max(H) by
+ * Lanczos, H = SA^T SA or SA SA^T.  Identity sketches return identity bounds
+ * without sketching, as the reference does. */
+typedef struct {
+  double effective_dimension; /* d_e at lambda0 */
+  double sigma_max_sq;        /* s_max(SA)^2 */
+  double dnorm_sq;            /* s_max^2 / (s_max^2 + lambda0) */
+  double lambda0;
+  int32_t lanczos_steps;
+} rp_spectrum_info;
+
+RP_API rp_status rp_derive_rho(rp_ctx* ctx, const rp_sketch_spec* spec, int transpose_op, double lambda_min,
+                               double lambda_max, rp_rho_bounds* out, rp_spectrum_info* info);
+/* effective_dimension (spectrum.hpp:51-52; spectrum.cpp:87-103), host. */
+RP_API rp_status rp_effective_dimension(const double* sigma, int64_t count, double lambda0, double* out);
+/* rho_gaussian (spectrum.cpp:105-128); m <= 0 = std::nullopt.  success_probability
+ * may be NULL; it is set to NaN when m is absent. */
+RP_API rp_status rp_rho_gaussian(double rho, double eta, double dnorm_sq, int64_t m, rp_rho_bounds* out,
+                                 double* success_probability);
+/* rho_srht (spectrum.cpp:130-148); n <= 0 = std::nullopt; recommended_m (nullable) = -1 when absent. */
+RP_API rp_status rp_rho_srht(double rho, double dnorm_sq, int64_t n, double de, rp_rho_bounds* out,
+                             int64_t* recommended_m);
+/* rho_sjlt (spectrum.cpp:150-169); alpha <= 0 = std::nullopt; recommendations = -1 when absent. */
+RP_API rp_status rp_rho_sjlt(double eps, double alpha, double delta, double de, rp_rho_bounds* out,
+                             int64_t* recommended_m, int32_t* recommended_s);
+
 /* ---- draw contract (rng.hpp / sketch.cpp draw loops), device-generated ---- */
 RP_API rp_status rp_draw_u64(rp_ctx* ctx, uint64_t seed, uint64_t skip, int64_t count, uint64_t* out, int where);
 RP_API rp_status rp_draw_uniform01(rp_ctx* ctx, uint64_t seed, int64_t count, double* out, int where);

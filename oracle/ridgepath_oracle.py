@@ -408,6 +408,106 @@ class RateParams:
     k: int = 1
 
 
+def effective_dimension(sigma, lambda0: float) -> float:
+    """spectrum.cpp:87-103: ||D||_F^2 / ||D||_2^2 with D_ii^2 = s^2 / (s^2 + lambda0)."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    _require(sigma.shape[0] > 0, "effective_dimension: empty spectrum")
+    _require(lambda0 >= 0.0, "effective_dimension: negative shift")
+    fro = 0.0
+    top = 0.0
+    for s in sigma.tolist():
+        _require(s >= 0.0, "effective_dimension: negative singular value")
+        if s == 0.0:
+            continue
+        dii_sq = s * s / (s * s + lambda0)
+        fro += dii_sq
+        top = max(top, dii_sq)
+    _require(top > 0.0, "effective_dimension: all-zero spectrum")
+    return fro / top
+
+
+def rho_gaussian(rho: float, eta: float, dnorm_sq: float, m=None):
+    """spectrum.cpp:105-128 -> (RhoBounds, success_probability or None)."""
+    _require(0.0 < rho < 1.0, "rho_gaussian: rho not in (0,1)")
+    eta_cap = (1.0 - math.sqrt(rho)) * (1.0 - math.sqrt(rho)) / 4.0
+    _require(0.0 < eta < eta_cap, "rho_gaussian: eta outside (0, (1-sqrt(rho))^2/4)")
+    _require(0.0 < dnorm_sq <= 1.0, "rho_gaussian: ||D||^2 must lie in (0,1]")
+    sq_eta = math.sqrt(eta)
+    c_eta = math.pow((1.0 + sq_eta) / (1.0 - sq_eta), 2.0)
+    up = (1.0 + math.sqrt(rho)) * (1.0 + sq_eta)
+    down = 1.0 - math.sqrt(c_eta * rho)
+    b = RhoBounds(1.0 - dnorm_sq + dnorm_sq * up * up, 1.0 - dnorm_sq + dnorm_sq * down * down, "gaussian")
+    b.validate()
+    prob = None
+    if m is not None:
+        prob = 1.0 - 16.0 * math.exp(-eta * eta * rho * float(m) / 2.0)
+    return b, prob
+
+
+def rho_srht(rho: float, dnorm_sq: float, n_and_de=None):
+    """spectrum.cpp:130-148 -> (RhoBounds, recommended_m or None)."""
+    _require(0.0 < rho < 1.0, "rho_srht: rho not in (0,1)")
+    _require(dnorm_sq > 0.0, "rho_srht: ||D||^2 must be positive")
+    _require(dnorm_sq * rho < 1.0, "rho_srht: ||D||^2 * rho must be below 1")
+    b = RhoBounds(1.0 + dnorm_sq * rho, 1.0 - dnorm_sq * rho, "srht")
+    rec = None
+    if n_and_de is not None:
+        n, de = n_and_de
+        _require(n >= 1 and de >= 1.0, "rho_srht: bad (n, d_e)")
+        c = 16.0 / 3.0 * math.pow(1.0 + math.sqrt(8.0 * math.log(de * float(n)) / de), 2.0)
+        rec = int(math.ceil(c * de * math.log(de) / rho))
+    return b, rec
+
+
+def rho_sjlt(eps: float, alpha_delta_de=None):
+    """spectrum.cpp:150-169 -> (RhoBounds, recommended_m or None, recommended_s or None)."""
+    _require(0.0 < eps < 0.5, "rho_sjlt: eps not in (0, 1/2)")
+    b = RhoBounds(1.0 + eps, 1.0 - eps, "sjlt")
+    rec_m = rec_s = None
+    if alpha_delta_de is not None:
+        alpha, delta, de = alpha_delta_de
+        _require(alpha > 2.0, "rho_sjlt: alpha must exceed 2")
+        _require(0.0 < delta < 0.5, "rho_sjlt: delta not in (0, 1/2)")
+        _require(de >= 1.0, "rho_sjlt: d_e must be >= 1")
+        log_alpha = math.log(de / delta) / math.log(alpha)
+        rec_s = int(math.ceil(log_alpha / eps))
+        rec_m = int(math.ceil(alpha * de * log_alpha / (eps * eps)))
+    return b, rec_m, rec_s
+
+
+def derive_rho(spec: "SketchSpec", a, lambda_min: float, lambda_max: float):
+    """tools/ridgepath_main.cpp:218-279 (the CLI's plug-in envelope): sketch A,
+    thin SVD of SA, effective dimension at lambda0 = sqrt(lo*hi), then the
+    family's bound.  Returns (RhoBounds, info dict)."""
+    if spec.kind == "identity":
+        return RhoBounds.identity(), {}
+    sa = sketch_apply(spec, a)
+    _, sigma, _ = thin_svd(sa)
+    lambda0 = math.sqrt(lambda_min * lambda_max)
+    de = effective_dimension(sigma, lambda0)
+    top = float(sigma[0]) * float(sigma[0])
+    dnorm_sq = top / (top + lambda0)
+    m = float(spec.m)
+    bounds = RhoBounds.identity()
+    if spec.kind == "gaussian":
+        rho = min(0.95, de / m)
+        eta = 0.5 * (1.0 - math.sqrt(rho)) * (1.0 - math.sqrt(rho)) / 4.0
+        bounds, _ = rho_gaussian(rho, eta, dnorm_sq, spec.m)
+    elif spec.kind == "srht":
+        c = 16.0 / 3.0 * math.pow(1.0 + math.sqrt(8.0 * math.log(de * float(spec.n)) / de), 2.0)
+        rho = c * de * max(1.0, math.log(de)) / m
+        rho = min(rho, 0.95 / max(dnorm_sq, 1e-12))
+        rho = min(max(rho, 1e-6), 0.95)
+        bounds, _ = rho_srht(rho, dnorm_sq)
+    elif spec.kind in ("countsketch", "sjlt"):
+        alpha, delta = 4.0, 0.1
+        log_term = math.log(max(de / delta, 1.5)) / math.log(alpha)
+        eps = math.sqrt(alpha * de * log_term / m)
+        eps = min(max(eps, 1e-6), 0.49)
+        bounds, _, _ = rho_sjlt(eps, (alpha, delta, de))
+    return bounds, dict(effective_dimension=de, sigma_max_sq=top, dnorm_sq=dnorm_sq, lambda0=lambda0)
+
+
 def log_grid(lambda_min: float, lambda_max: float, count: int) -> List[float]:
     """spectrum.cpp:38-53."""
     _require(count >= 1, "log_grid: count must be >= 1")

@@ -37,6 +37,7 @@
 #include "ridgepath_b200.h"
 #include "sketch.h"
 #include "sparse_gram.h"
+#include "spectrum.h"
 
 namespace rpb {
 
@@ -292,7 +293,7 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
-  int64_t csr_chunk = 64;            // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 64)
+  int64_t csr_chunk = 128;           // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 128)
   std::string err;
 };
 
@@ -1263,7 +1264,7 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
     } else if (k == "csr_chunk") {
-      require(value >= 1 && value <= 64, "csr_chunk must be in [1, 64]");
+      require(value >= 1 && value <= 128, "csr_chunk must be in [1, 128]");
       ctx->csr_chunk = value;
     } else {
       throw InvalidArgument("unknown option: " + k);
@@ -1670,6 +1671,90 @@ rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_in
         edges_out[2 * i] = sp[i].first;
         edges_out[2 * i + 1] = sp[i].second;
       }
+  });
+}
+
+// ---- plug-in envelope (derive_rho, ridgepath_main.cpp:218-279) -------------------
+
+static void to_c_rho(const RhoResult& r, rp_rho_bounds* out) {
+  out->rho1 = r.rho1;
+  out->rho2 = r.rho2;
+  out->provenance = r.provenance;
+}
+
+rp_status rp_derive_rho(rp_ctx* ctx, const rp_sketch_spec* specp, int transpose_op, double lambda_min,
+                        double lambda_max, rp_rho_bounds* out, rp_spectrum_info* info) {
+  if (!ctx || !out) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const SketchSpecC spec = to_spec(specp);
+    require(lambda_min > 0.0 && lambda_max >= lambda_min, "derive_rho: bad lambda range");
+    rp_spectrum_info inf{};
+    const double lambda0 = std::sqrt(lambda_min * lambda_max);
+    inf.lambda0 = lambda0;
+    if (spec.kind == RP_SKETCH_IDENTITY) {
+      to_c_rho(RhoResult{}, out);
+      if (info) *info = inf;
+      return;
+    }
+    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    validate_spec(spec);
+    require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
+    cudaStream_t s = ctx->stream;
+    DBuf<double> sa(static_cast<size_t>(spec.m * op.d), s);
+    sketch_apply(spec, op, sa.get(), s);
+    allreduce(ctx, sa.get(), spec.m * op.d);
+    const SketchedSpectrum sp = sketched_spectrum(sa.get(), spec.m, op.d, lambda0, s);
+    double de = 0.0, dn = 0.0;
+    const RhoResult r = envelope_from_spectrum(spec.kind, spec.m, spec.n, sp, lambda0, &de, &dn);
+    to_c_rho(r, out);
+    inf.effective_dimension = de;
+    inf.sigma_max_sq = sp.sigma_max_sq;
+    inf.dnorm_sq = dn;
+    inf.lanczos_steps = sp.lanczos_steps;
+    if (info) *info = inf;
+  });
+}
+
+rp_status rp_effective_dimension(const double* sigma, int64_t count, double lambda0, double* out) {
+  return guarded(nullptr, [&] {
+    require(out != nullptr && (sigma != nullptr || count == 0), "effective_dimension: null buffer");
+    *out = effective_dimension(sigma, count, lambda0);
+  });
+}
+
+rp_status rp_rho_gaussian(double rho, double eta, double dnorm_sq, int64_t m, rp_rho_bounds* out,
+                          double* success_probability) {
+  return guarded(nullptr, [&] {
+    require(out != nullptr, "rho_gaussian: null output");
+    std::optional<int64_t> mm;
+    if (m > 0) mm = m;
+    const RhoResult r = rho_gaussian(rho, eta, dnorm_sq, mm);
+    to_c_rho(r, out);
+    if (success_probability) *success_probability = r.success_probability ? *r.success_probability : std::nan("");
+  });
+}
+
+rp_status rp_rho_srht(double rho, double dnorm_sq, int64_t n, double de, rp_rho_bounds* out, int64_t* recommended_m) {
+  return guarded(nullptr, [&] {
+    require(out != nullptr, "rho_srht: null output");
+    std::optional<std::pair<int64_t, double>> nd;
+    if (n > 0) nd = std::make_pair(n, de);
+    const RhoResult r = rho_srht(rho, dnorm_sq, nd);
+    to_c_rho(r, out);
+    if (recommended_m) *recommended_m = r.recommended_m ? *r.recommended_m : -1;
+  });
+}
+
+rp_status rp_rho_sjlt(double eps, double alpha, double delta, double de, rp_rho_bounds* out, int64_t* recommended_m,
+                      int32_t* recommended_s) {
+  return guarded(nullptr, [&] {
+    require(out != nullptr, "rho_sjlt: null output");
+    std::optional<std::tuple<double, double, double>> adde;
+    if (alpha > 0.0) adde = std::make_tuple(alpha, delta, de);
+    const RhoResult r = rho_sjlt(eps, adde);
+    to_c_rho(r, out);
+    if (recommended_m) *recommended_m = r.recommended_m ? *r.recommended_m : -1;
+    if (recommended_s) *recommended_s = r.recommended_s ? *r.recommended_s : -1;
   });
 }
 

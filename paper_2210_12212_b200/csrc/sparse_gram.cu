@@ -221,7 +221,7 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelCsc& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s) {
   if (cols <= 0 || pc.d <= 0) return;
-  chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, 64));
+  chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, 128));
   const int64_t cmax = std::min(chunk, cols);
   DBuf<double> wr(static_cast<size_t>(pc.d * cmax), s), z(static_cast<size_t>(pc.d * cmax), s);
   DBuf<double> yp(static_cast<size_t>(std::max<int64_t>(1, std::min(pc.panel_rows, pc.n)) * cmax), s);
@@ -232,8 +232,10 @@ void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* c
       fill(z.get(), pc.d * cc, 0.0, s);
     } else if (cc <= 32) {
       run_chunk<1>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
-    } else {
+    } else if (cc <= 64) {
       run_chunk<2>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+    } else {
+      run_chunk<4>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
     }
     transpose(z.get(), cc, pc.d, cc, Y + c0 * ldy, ldy, s);  // back to column-major
   }

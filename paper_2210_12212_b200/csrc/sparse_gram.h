@@ -3,7 +3,7 @@
 // ref/proj/core/src/matrix.cpp:140-172).
 //
 // The operator's local rows are cut into panels of `panel_rows` rows and the
-// right-hand columns into chunks of <= 64.  Per (chunk, panel):
+// right-hand columns into chunks of <= 128.  Per (chunk, panel):
 //   pass 1  Y_p = M_p W_c            (warp per row, gathers rows of the
 //                                     row-major W_c, which stays in L2)
 //   pass 2  Z  = Z + M_p^T Y_p       (warp per column through the panel's own

@@ -64,6 +64,11 @@ class _Rho(ctypes.Structure):
     _fields_ = [("rho1", ctypes.c_double), ("rho2", ctypes.c_double), ("provenance", ctypes.c_int32)]
 
 
+class _SpectrumInfo(ctypes.Structure):
+    _fields_ = [("effective_dimension", ctypes.c_double), ("sigma_max_sq", ctypes.c_double),
+                ("dnorm_sq", ctypes.c_double), ("lambda0", ctypes.c_double), ("lanczos_steps", ctypes.c_int32)]
+
+
 class _Rate(ctypes.Structure):
     _fields_ = [("lambda0", ctypes.c_double), ("alpha", ctypes.c_double), ("kappa", ctypes.c_double),
                 ("contraction", ctypes.c_double), ("k", ctypes.c_int32)]
@@ -138,6 +143,12 @@ SIGNATURES = {
     "rp_count_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
     "rp_srht_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
     "rp_mt_selfcheck": ([_U64, _U64], _INT),
+    "rp_derive_rho": ([_P, ctypes.POINTER(_SketchSpec), _INT, _D, _D, ctypes.POINTER(_Rho),
+                       ctypes.POINTER(_SpectrumInfo)], _INT),
+    "rp_effective_dimension": ([_P, _I64, _D, _P], _INT),
+    "rp_rho_gaussian": ([_D, _D, _D, _I64, ctypes.POINTER(_Rho), _P], _INT),
+    "rp_rho_srht": ([_D, _D, _I64, _D, ctypes.POINTER(_Rho), _P], _INT),
+    "rp_rho_sjlt": ([_D, _D, _D, _D, ctypes.POINTER(_Rho), _P, _P], _INT),
 }
 
 
@@ -321,6 +332,63 @@ def tune_interval(lambda_lo, lambda_hi, rho: RhoBounds, sigma_d=None, eps=1e-6) 
     _check(lib().rp_tune_interval(lambda_lo, lambda_hi, ctypes.byref(rho.c()),
                                   ctypes.cast(ctypes.byref(sd), _P) if sd is not None else None, eps, ctypes.byref(r)))
     return RateParams(r.lambda0, r.alpha, r.kappa, r.contraction, r.k)
+
+
+def _rho_py(r: "_Rho") -> RhoBounds:
+    return RhoBounds(r.rho1, r.rho2, RHO_PROVENANCE[r.provenance])
+
+
+def effective_dimension(sigma, lambda0: float) -> float:
+    """spectrum.cpp:87-103 (host)."""
+    sig = np.ascontiguousarray(np.asarray(sigma, dtype=np.float64).reshape(-1))
+    out = ctypes.c_double(0.0)
+    _check(lib().rp_effective_dimension(_ptr(sig) if sig.size else None, sig.size, float(lambda0),
+                                        ctypes.cast(ctypes.byref(out), _P)))
+    return out.value
+
+
+def rho_gaussian(rho, eta, dnorm_sq, m=None):
+    """spectrum.cpp:105-128 -> (RhoBounds, success_probability or None)."""
+    r, p = _Rho(), ctypes.c_double(0.0)
+    _check(lib().rp_rho_gaussian(rho, eta, dnorm_sq, int(m) if m is not None else 0, ctypes.byref(r),
+                                 ctypes.cast(ctypes.byref(p), _P)))
+    return _rho_py(r), (p.value if m is not None else None)
+
+
+def rho_srht(rho, dnorm_sq, n_and_de=None):
+    """spectrum.cpp:130-148 -> (RhoBounds, recommended_m or None)."""
+    r, rec = _Rho(), _I64(0)
+    n, de = n_and_de if n_and_de is not None else (0, 0.0)
+    _check(lib().rp_rho_srht(rho, dnorm_sq, int(n), float(de), ctypes.byref(r), ctypes.cast(ctypes.byref(rec), _P)))
+    return _rho_py(r), (rec.value if n_and_de is not None else None)
+
+
+def rho_sjlt(eps, alpha_delta_de=None):
+    """spectrum.cpp:150-169 -> (RhoBounds, recommended_m or None, recommended_s or None)."""
+    r, rm, rs = _Rho(), _I64(0), _I32(0)
+    alpha, delta, de = alpha_delta_de if alpha_delta_de is not None else (0.0, 0.0, 0.0)
+    _check(lib().rp_rho_sjlt(eps, float(alpha), float(delta), float(de), ctypes.byref(r), ctypes.cast(ctypes.byref(rm), _P),
+                             ctypes.cast(ctypes.byref(rs), _P)))
+    if alpha_delta_de is None:
+        return _rho_py(r), None, None
+    return _rho_py(r), rm.value, rs.value
+
+
+def derive_rho(spec: "SketchSpec", a, lambda_min: float, lambda_max: float, ctx: Optional["Context"] = None,
+               transpose_op: bool = False):
+    """The CLI's plug-in envelope (tools/ridgepath_main.cpp:218-279) on the
+    device: returns (RhoBounds, info dict).  Identity sketches return identity
+    bounds without sketching."""
+    ctx = ctx or default_context()
+    if spec.kind != "identity":
+        ctx.set_operator(a)
+    r, info = _Rho(), _SpectrumInfo()
+    ctx.check(lib().rp_derive_rho(ctx.handle, ctypes.byref(spec.c()), int(bool(transpose_op)), float(lambda_min),
+                                  float(lambda_max), ctypes.byref(r), ctypes.byref(info)))
+    if spec.kind == "identity":
+        return _rho_py(r), {}
+    return _rho_py(r), dict(effective_dimension=info.effective_dimension, sigma_max_sq=info.sigma_max_sq,
+                            dnorm_sq=info.dnorm_sq, lambda0=info.lambda0, lanczos_steps=info.lanczos_steps)
 
 
 def auto_interval_count(lambda_min, lambda_max) -> int:

@@ -111,3 +111,38 @@ def test_no_cpu_fallback_without_device(rp):
         pytest.skip("a CUDA device is present")
     with pytest.raises(Exception):
         rp.Context(0)
+
+
+def test_envelope_host_functions_bit_identical(rp, oracle):
+    """effective_dimension / rho_gaussian / rho_srht / rho_sjlt (spectrum.cpp:87-169)
+    through the C ABI equal the oracle's restatement bit for bit and keep the
+    reference's argument checks (test_spectrum.cpp:9-106)."""
+    rng = np.random.default_rng(8)
+    for _ in range(200):
+        sig = np.sort(rng.random(int(rng.integers(1, 40))) * 10)[::-1]
+        if rng.random() < 0.3:
+            sig[-3:] = 0.0
+        lam = float(10 ** rng.uniform(-4, 3))
+        if not sig.any():
+            continue
+        assert rp.effective_dimension(sig, lam) == oracle.effective_dimension(sig, lam)
+        rho = float(rng.uniform(0.01, 0.9))
+        eta = float(rng.uniform(0.001, 0.99)) * (1 - math.sqrt(rho)) ** 2 / 4
+        dn = float(rng.uniform(0.01, 1.0))
+        m = int(rng.integers(10, 10000))
+        (a, pa), (b, pb) = rp.rho_gaussian(rho, eta, dn, m), oracle.rho_gaussian(rho, eta, dn, m)
+        assert (a.rho1, a.rho2, a.provenance, pa) == (b.rho1, b.rho2, b.provenance, pb)
+        de = float(rng.uniform(1, 500))
+        (a, ra), (b, rb) = rp.rho_srht(rho, dn, (m, de)), oracle.rho_srht(rho, dn, (m, de))
+        assert (a.rho1, a.rho2, a.provenance, ra) == (b.rho1, b.rho2, b.provenance, rb)
+        eps = float(rng.uniform(0.001, 0.49))
+        a, ma, sa = rp.rho_sjlt(eps, (4.0, 0.1, de))
+        b, mb, sb = oracle.rho_sjlt(eps, (4.0, 0.1, de))
+        assert (a.rho1, a.rho2, a.provenance, ma, sa) == (b.rho1, b.rho2, b.provenance, mb, sb)
+    assert rp.effective_dimension([2.0, 1.0], 3.0) == pytest.approx(23.0 / 16.0)
+    assert rp.rho_sjlt(0.25, (4.0, 0.1, 100.0))[1:] == (31891, 20)
+    assert rp.rho_gaussian(0.25, 0.01, 1.0)[1] is None
+    for bad in (lambda: rp.effective_dimension(np.zeros(3), 1.0), lambda: rp.rho_gaussian(0.25, 0.2, 1.0),
+                lambda: rp.rho_srht(0.9, 1.2), lambda: rp.rho_sjlt(0.6), lambda: rp.effective_dimension([-1.0], 1.0)):
+        with pytest.raises(ValueError):
+            bad()

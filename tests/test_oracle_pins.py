@@ -304,3 +304,63 @@ def test_gram_is_composition(oracle):  # test_matrix_core.cpp:68-76
     assert np.array_equal(oracle.gram_apply(m, x), oracle.apply_transpose(m, oracle.apply(m, x)))
     lower = np.array([[1.0, 0.0], [1.0, 1.0]])
     assert oracle.gram_apply(lower, np.ones(2)).tolist() == [3.0, 2.0]
+
+
+# ---- derive_rho pieces: spectrum.cpp:87-169 against test_spectrum.cpp:9-106 ----
+
+def test_effective_dimension_kats(oracle):  # test_spectrum.cpp:9-38
+    assert oracle.effective_dimension([1.0, 1.0], 1.0) == pytest.approx(2.0)
+    assert oracle.effective_dimension([2.0, 1.0], 3.0) == pytest.approx(23.0 / 16.0)
+    assert oracle.effective_dimension([3.0, 0.0], 1.0) == pytest.approx(1.0)
+    with pytest.raises(ValueError):
+        oracle.effective_dimension([0.0, 0.0, 0.0], 1.0)
+    sigma = [5.0, 2.0, 1.0, 0.5]
+    prev = oracle.effective_dimension(sigma, 0.0)
+    assert prev == pytest.approx(4.0)
+    for shift in (0.1, 1.0, 10.0, 100.0):
+        cur = oracle.effective_dimension(sigma, shift)
+        assert 1.0 <= cur <= prev + 1e-12
+        prev = cur
+
+
+def test_rho_envelope_kats(oracle):  # test_spectrum.cpp:40-106
+    b, _ = oracle.rho_gaussian(0.25, 0.01, 1.0)
+    assert b.rho1 == pytest.approx(2.7225, rel=1e-12)
+    assert b.rho2 == pytest.approx(49.0 / 324.0, rel=1e-14)
+    b, _ = oracle.rho_gaussian(0.25, 0.01, 1e-12)
+    assert b.rho1 == pytest.approx(1.0, rel=1e-9) and b.rho2 == pytest.approx(1.0, rel=1e-9)
+    b, _ = oracle.rho_gaussian(0.04, 0.04, 0.5)
+    assert b.rho1 == pytest.approx(1.5368, rel=1e-12) and b.rho2 == pytest.approx(0.745, rel=1e-12)
+    _, p = oracle.rho_gaussian(0.25, 0.01, 1.0, 8000)
+    assert p == pytest.approx(1.0 - 16.0 * math.exp(-0.01 * 0.01 * 0.25 * 4000.0))
+    for bad in ((0.25, 0.2, 1.0), (1.5, 0.01, 1.0)):
+        with pytest.raises(ValueError):
+            oracle.rho_gaussian(*bad)
+    b, _ = oracle.rho_srht(0.5, 1.0)
+    assert (b.rho1, b.rho2) == (1.5, 0.5)
+    b, _ = oracle.rho_srht(0.2, 0.8)
+    assert b.rho1 == pytest.approx(1.16, rel=1e-12) and b.rho2 == pytest.approx(0.84, rel=1e-12)
+    _, rec = oracle.rho_srht(0.5, 1.0, (1024, 50.0))
+    c = 16.0 / 3.0 * (1.0 + math.sqrt(8.0 * math.log(50.0 * 1024.0) / 50.0)) ** 2
+    assert rec == math.ceil(c * 50.0 * math.log(50.0) / 0.5)
+    with pytest.raises(ValueError):
+        oracle.rho_srht(0.9, 1.2)
+    b, _, _ = oracle.rho_sjlt(0.25)
+    assert (b.rho1, b.rho2) == (1.25, 0.75)
+    _, rm, rs = oracle.rho_sjlt(0.25, (4.0, 0.1, 100.0))
+    assert rs == 20 and rm == 31891
+    with pytest.raises(ValueError):
+        oracle.rho_sjlt(0.6)
+
+
+def test_derive_rho_oracle_families(oracle):
+    """derive_rho (ridgepath_main.cpp:218-279) on a small problem: every family
+    yields a valid envelope; identity short-circuits without sketching."""
+    a = oracle.random_dense(600, 20, 3) / np.sqrt(np.arange(1, 21))
+    for kind, m, s in (("gaussian", 120, 1), ("srht", 120, 1), ("countsketch", 120, 1), ("sjlt", 120, 3)):
+        b, info = oracle.derive_rho(oracle.SketchSpec(kind, m, 600, s, 7), a, 1e-3, 1e2)
+        b.validate()
+        assert b.provenance == ("sjlt" if kind == "countsketch" else kind)
+        assert 1.0 <= info["effective_dimension"] <= 20.0
+    b, info = oracle.derive_rho(oracle.SketchSpec("identity", 600, 600, 1, 0), a, 1e-3, 1e2)
+    assert (b.rho1, b.rho2, b.provenance, info) == (1.0, 1.0, "identity", {})

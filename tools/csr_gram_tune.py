@@ -32,23 +32,23 @@ def main():
     x = torch.randn(d * cols, dtype=torch.float64, device="cuda")
     y = torch.empty(d * cols, dtype=torch.float64, device="cuda")
     ref = None
-    for panel in (16384, 32768, 65536, 131072):
-        for chunk in (16, 32, 48, 64):
-            ctx.set_option("csr_panel_rows", panel)
-            ctx.set_option("csr_chunk", chunk)
+    combos = [(p, c) for p in (32768, 65536, 131072, 262144) for c in (64, 96, 128)]
+    for panel, chunk in combos:
+        ctx.set_option("csr_panel_rows", panel)
+        ctx.set_option("csr_chunk", chunk)
+        rp.gram_apply_raw(ctx, x.data_ptr(), cols, y.data_ptr())
+        if ref is None:
+            ref = y.clone()
+        assert torch.equal(ref, y), "blocking changed the bits"
+        ctx.set_option("profile", 1)
+        ts = []
+        for _ in range(3):
             rp.gram_apply_raw(ctx, x.data_ptr(), cols, y.data_ptr())
-            if ref is None:
-                ref = y.clone()
-            assert torch.equal(ref, y), "blocking changed the bits"
-            ctx.set_option("profile", 1)
-            ts = []
-            for _ in range(3):
-                rp.gram_apply_raw(ctx, x.data_ptr(), cols, y.data_ptr())
-                ts.append(rp.last_device_seconds(ctx))
-            ctx.set_option("profile", 0)
-            t = statistics.median(ts)
-            print(f"panel {panel:7d} chunk {chunk:3d}: {t*1e3:8.2f} ms  {t/cols*1e6:7.2f} us/col  "
-                  f"gather {2*nnz*8*cols/t/1e12:6.2f} TB/s", flush=True)
+            ts.append(rp.last_device_seconds(ctx))
+        ctx.set_option("profile", 0)
+        t = statistics.median(ts)
+        print(f"panel {panel:7d} chunk {chunk:3d}: {t*1e3:8.2f} ms  {t/cols*1e6:7.2f} us/col  "
+              f"gather {2*nnz*8*cols/t/1e12:6.2f} TB/s", flush=True)
 
 
 if __name__ == "__main__":
