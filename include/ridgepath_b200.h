@@ -223,6 +223,23 @@ RP_API int32_t rp_auto_interval_count(double lambda_min, double lambda_max);
 RP_API rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_intervals, double* edges_out,
                             int32_t* count_out);
 
+/* ---- comparison baselines (baselines.hpp; baselines.cpp:80-226) ----------
+ * warm_cg_path, warm_ihs_path and direct_path on the context's operator with a
+ * vector b (n entries; the local rows when row-sharded).  x_out is d x T
+ * column-major in grid order.  iterations / seconds (host, T entries each,
+ * nullable) are PathPoint::iterations / ::seconds; setup_total (host, 2
+ * entries, nullable) receives RegPathResult setup_seconds and total_seconds.
+ * Iteration caps and divergence raise RP_ESOLVER (SolverError) as in the
+ * reference; direct_path's failed Cholesky is RP_ESOLVER too.  svd_path (a
+ * thin SVD of A itself) is not provided. */
+RP_API rp_status rp_warm_cg_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
+                                 int32_t* iterations, double* seconds, double* setup_total);
+RP_API rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, const rp_sketch_spec* spec,
+                                  const rp_rho_bounds* rho, double* x_out, int where, int32_t* iterations,
+                                  double* seconds, double* setup_total);
+RP_API rp_status rp_direct_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
+                                double* seconds, double* setup_total);
+
 /* ---- plug-in envelope (derive_rho, tools/ridgepath_main.cpp:218-279) ------
  * The reference CLI derives (rho1, rho2) from the sketched spectrum when
  * --rho1/--rho2 are absent: sketch A, thin SVD of SA, effective dimension at

@@ -733,6 +733,7 @@ class PathPoint:
     lam: float
     solution: np.ndarray
     seconds: float = 0.0
+    iterations: int = 0
 
 
 @dataclass
@@ -826,6 +827,123 @@ def ihs_basis_matrix(a, b: np.ndarray, p: Preconditioner, tau: float, k: int) ->
 
 def ihs_compose_matrix(basis: BinomialBasis, lam: float) -> np.ndarray:
     return compose_horner(basis, basis.tau * lam)
+
+
+# --------------------------------------------------------------------------
+# Comparison baselines (baselines.hpp; baselines.cpp:51-226)
+# --------------------------------------------------------------------------
+
+def _descending_order(grid):
+    """baselines.cpp:40-47 (std::sort with '>' -- ties are never present in a
+    validated grid except repeated lambdas, kept in index order here)."""
+    return sorted(range(len(grid)), key=lambda i: -grid[i])
+
+
+def svd_path(a, b: np.ndarray, config: PathConfig) -> RegPathResult:
+    """baselines.cpp:51-78: one thin SVD of A, a diagonal solve per lambda."""
+    config.validate()
+    _require(b.shape[0] == _rows(a), "svd_path: dimension mismatch")
+    dense = a.to_dense() if is_csr(a) else a
+    u, s, vt = thin_svd(dense)
+    utb = u.T @ b
+    pts = [PathPoint(lam, vt.T @ (s * utb / (s * s + lam))) for lam in config.lambdas]
+    return RegPathResult("svd", pts)
+
+
+def direct_path(a, b: np.ndarray, config: PathConfig) -> RegPathResult:
+    """baselines.cpp:80-118: A^T A once, Cholesky of A^T A + lambda I per lambda."""
+    config.validate()
+    _require(b.shape[0] == _rows(a), "direct_path: dimension mismatch")
+    d = _cols(a)
+    gram = apply_transpose(a, apply(a, np.eye(d))) if is_csr(a) else a.T @ a
+    atb = apply_transpose(a, b)
+    pts = []
+    for lam in config.lambdas:
+        sh = gram + lam * np.eye(d)
+        try:
+            lo = np.linalg.cholesky(sh)
+        except np.linalg.LinAlgError:
+            raise SolverError("direct_path: Cholesky factorization failed")
+        y = np.linalg.solve(lo, atb)
+        pts.append(PathPoint(lam, np.linalg.solve(lo.T, y)))
+    return RegPathResult("direct", pts)
+
+
+def warm_cg_path(a, b: np.ndarray, config: PathConfig) -> RegPathResult:
+    """baselines.cpp:120-162: CG on (A^T A + lambda I) x = A^T b, swept from the
+    largest lambda down with warm starts; stop at ||r|| <= eps ||A^T b||; cap 10 d."""
+    config.validate()
+    _require(b.shape[0] == _rows(a), "warm_cg_path: dimension mismatch")
+    atb = apply_transpose(a, b)
+    rhs_norm = float(np.linalg.norm(atb))
+    d = _cols(a)
+    cap = 10 * d
+    tol = config.epsilon * (rhs_norm if rhs_norm > 0.0 else 1.0)
+    pts = [None] * len(config.lambdas)
+    x = np.zeros(d)
+    for idx in _descending_order(config.lambdas):
+        lam = config.lambdas[idx]
+        r = atb - gram_apply(a, x) - lam * x
+        p = r.copy()
+        rr = float(r @ r)
+        iters = 0
+        while math.sqrt(rr) > tol:
+            if iters >= cap:
+                raise SolverError("warm_cg_path: iteration cap (10 d) reached")
+            q = gram_apply(a, p) + lam * p
+            alpha = rr / float(p @ q)
+            x = x + alpha * p
+            r = r - alpha * q
+            rr_next = float(r @ r)
+            p = r + (rr_next / rr) * p
+            rr = rr_next
+            iters += 1
+        pts[idx] = PathPoint(lam, x.copy(), iterations=iters)
+    return RegPathResult("cg", pts)
+
+
+def warm_ihs_path(a, b: np.ndarray, config: PathConfig, spec: SketchSpec, rho: RhoBounds) -> RegPathResult:
+    """baselines.cpp:164-224: warm-started preconditioned iterations per lambda
+    with the shift pinned to the active lambda, step 2 / (1/rho1 + 1/rho2),
+    stop at ||grad|| <= eps ||A^T b||, cap 1000, one tau/2 retry."""
+    config.validate()
+    rho.validate()
+    _require(b.shape[0] == _rows(a), "warm_ihs_path: dimension mismatch")
+    _require(spec.n == _rows(a), "warm_ihs_path: spec.n must equal A.rows")
+    sa = sketch_apply(spec, a)
+    pre = Preconditioner.build_from_svd(thin_svd(sa), sa.shape[0], sa.shape[1], config.lambdas[-1])
+    atb = apply_transpose(a, b)
+    rhs_norm = float(np.linalg.norm(atb))
+    tau_nominal = 2.0 / (1.0 / rho.rho1 + 1.0 / rho.rho2)
+    tol = config.epsilon * (rhs_norm if rhs_norm > 0.0 else 1.0)
+    cap = 1000
+    pts = [None] * len(config.lambdas)
+    x = np.zeros(_cols(a))
+    for idx in _descending_order(config.lambdas):
+        lam = config.lambdas[idx]
+        pre = pre.reshift(lam)
+        tau = tau_nominal
+        xs = x.copy()
+        iters = 0
+        retried = False
+        while True:
+            grad = gram_apply(a, xs) + lam * xs - atb
+            if float(np.linalg.norm(grad)) <= tol:
+                break
+            if iters >= cap:
+                raise SolverError("warm_ihs_path: iteration cap reached")
+            xs = xs - tau * pre.apply(grad)
+            iters += 1
+            if not np.all(np.isfinite(xs)):
+                if retried:
+                    raise SolverError("warm_ihs_path: diverged twice, even at tau/2")
+                retried = True
+                tau /= 2.0
+                xs = x.copy()
+                iters = 0
+        x = xs
+        pts[idx] = PathPoint(lam, x.copy(), iterations=iters)
+    return RegPathResult("ihs", pts)
 
 
 def losses(a, b, x, lam, a_test=None, b_test=None):

@@ -38,6 +38,7 @@
 #include "sketch.h"
 #include "sparse_gram.h"
 #include "spectrum.h"
+#include "vecops.h"
 
 namespace rpb {
 
@@ -293,6 +294,7 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
+  int64_t csr_one_panel_bytes = 48 << 20;  // option "csr_one_panel_bytes": M W up to this size runs as one panel
   int64_t csr_chunk = 128;           // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 128)
   std::string err;
 };
@@ -437,7 +439,13 @@ struct GramOp {
     if (op.sparse) {
       // L2-blocked two passes per row panel (sparse_gram.cu): bit-identical to
       // apply followed by apply_transpose, without the n x cols intermediate
-      sparse_gram(op.csr_off, op.csr_col, op.csr_val, panel_csc(ctx, op), W, op.d, cols, Y, op.d, ctx->csr_chunk, s);
+      // (a narrow product whose whole M W fits in L2 runs as one panel on the
+      // operator's plain CSC: same bits, no panel structure needed)
+      const bool one_panel =
+          static_cast<double>(op.n_loc) * static_cast<double>(cols) * 8.0 <= static_cast<double>(ctx->csr_one_panel_bytes);
+      const PanelView pv = one_panel ? single_panel(op.n_loc, op.d, op.csc_off, op.csc_row, op.csc_val)
+                                     : view_of(panel_csc(ctx, op));
+      sparse_gram(op.csr_off, op.csr_col, op.csr_val, pv, W, op.d, cols, Y, op.d, ctx->csr_chunk, s);
       allreduce(ctx, Y, op.d * cols);
       return;
     }
@@ -534,6 +542,23 @@ struct PrecondBatch {
     inv_owned.alloc(static_cast<size_t>(L * nn * nn), s);
     inv = inv_owned.get();
     spd_inverse_batched(h.get(), nn, nn, nn * nn, L, inv_owned.get(), nn, nn * nn, s);
+  }
+
+  // A one-shift view of shift l (no copy of the factor).
+  PrecondBatch single(rp_ctx* ctx, int64_t l) const {
+    PrecondBatch v;
+    v.m = m;
+    v.d = d;
+    v.L = 1;
+    v.woodbury = woodbury;
+    v.col_stable = col_stable;
+    v.sa = sa;
+    v.lambda0 = {lambda0[static_cast<size_t>(l)]};
+    v.d_lambda0.alloc(1, ctx->stream);
+    RP_CUDA(cudaMemcpyAsync(v.d_lambda0.get(), v.lambda0.data(), sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    v.inv = inv + l * n() * n();
+    return v;
   }
 
   // out_l (d x cols) = P_l in_l for l < L; in/out strided by `sin`/`sout`
@@ -1263,6 +1288,9 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "csr_panel_rows") {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
+    } else if (k == "csr_one_panel_bytes") {
+      require(value >= 0, "csr_one_panel_bytes must be >= 0");
+      ctx->csr_one_panel_bytes = value;
     } else if (k == "csr_chunk") {
       require(value >= 1 && value <= 128, "csr_chunk must be in [1, 128]");
       ctx->csr_chunk = value;
@@ -1671,6 +1699,321 @@ rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t num_in
         edges_out[2 * i] = sp[i].first;
         edges_out[2 * i + 1] = sp[i].second;
       }
+  });
+}
+
+// ---- comparison baselines (baselines.cpp:80-226) --------------------------------
+//
+// The reference's speed/accuracy baselines for the IHS-BIN path, run on the
+// same device operator.  warm_cg / warm_ihs are sequential per lambda (warm
+// starts along the descending sweep); their per-iteration Gram product is the
+// narrow fused pass (gram_pass.cu) for dense operators and the one-panel
+// sparse pass for CSR.  Scalars stay on the device; the host reads the one
+// convergence scalar per iteration.
+
+namespace rpb {
+
+std::vector<size_t> descending_order(const std::vector<double>& grid) {  // baselines.cpp:40-47
+  std::vector<size_t> idx(grid.size());
+  std::iota(idx.begin(), idx.end(), size_t{0});
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t i, size_t j) { return grid[i] > grid[j]; });
+  return idx;
+}
+
+struct BaselineRun {
+  std::vector<int32_t> iterations;
+  std::vector<double> seconds;
+  double setup_seconds = 0.0, total_seconds = 0.0;
+};
+
+double read_scalar(const double* dev, cudaStream_t s) {
+  double v = 0.0;
+  RP_CUDA(cudaMemcpyAsync(&v, dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+double host_seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// warm_cg_path (baselines.cpp:120-162); x_out: d x T on the device.
+void run_warm_cg(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out, BaselineRun& run) {
+  cudaStream_t s = ctx->stream;
+  const auto t_total = std::chrono::steady_clock::now();
+  const OpView op = ctx->op.primal();
+  const int64_t d = op.d;
+  GramOp gram;
+  gram.ctx = ctx;
+  gram.op = op;
+  gram.allow_fused = true;
+  DBuf<double> atb(static_cast<size_t>(d), s), x(static_cast<size_t>(d), s), r(static_cast<size_t>(d), s),
+      p(static_cast<size_t>(d), s), q(static_cast<size_t>(d), s), g(static_cast<size_t>(d), s),
+      part(kDotParts, s), sc(4, s);
+  op_apply_t(ctx, op, b, 1, atb.get(), true);
+  vec_dot(atb.get(), atb.get(), d, part.get(), sc.get(), s);
+  const double rhs_norm = std::sqrt(read_scalar(sc.get(), s));
+  run.setup_seconds = host_seconds_since(t_total);
+  const int64_t cap = 10 * d;
+  const double tol = cfg.epsilon * (rhs_norm > 0.0 ? rhs_norm : 1.0);
+  const size_t T = cfg.lambdas.size();
+  run.iterations.assign(T, 0);
+  run.seconds.assign(T, 0.0);
+  fill(x.get(), d, 0.0, s);
+  for (size_t idx : descending_order(cfg.lambdas)) {
+    const double lam = cfg.lambdas[idx];
+    const auto t_eval = std::chrono::steady_clock::now();
+    gram.apply(x.get(), 1, g.get());
+    cg_init(atb.get(), g.get(), x.get(), lam, d, r.get(), p.get(), s);
+    vec_dot(r.get(), r.get(), d, part.get(), sc.get(), s);
+    double rr = read_scalar(sc.get(), s);
+    int slot = 0;  // sc[0] / sc[2] hold rr and rr_next in turn, sc[1] = p.q
+    int32_t iters = 0;
+    while (std::sqrt(rr) > tol) {
+      if (iters >= cap) throw SolverFailure("warm_cg_path: iteration cap (10 d) reached");
+      double* rr_dev = sc.get() + slot;
+      double* rr_next_dev = sc.get() + (2 - slot);
+      gram.apply(p.get(), 1, g.get());
+      cg_q(g.get(), p.get(), lam, d, q.get(), s);
+      vec_dot(p.get(), q.get(), d, part.get(), sc.get() + 1, s);
+      cg_update(x.get(), r.get(), p.get(), q.get(), rr_dev, sc.get() + 1, d, s);
+      vec_dot(r.get(), r.get(), d, part.get(), rr_next_dev, s);
+      cg_direction(p.get(), r.get(), rr_next_dev, rr_dev, d, s);
+      rr = read_scalar(rr_next_dev, s);
+      slot = 2 - slot;
+      ++iters;
+    }
+    RP_CUDA(cudaMemcpyAsync(x_out + static_cast<int64_t>(idx) * d, x.get(), sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    run.iterations[idx] = iters;
+    run.seconds[idx] = host_seconds_since(t_eval);
+  }
+  run.total_seconds = host_seconds_since(t_total);
+}
+
+// warm_ihs_path (baselines.cpp:164-224); x_out: d x T on the device.
+void run_warm_ihs(rp_ctx* ctx, const double* b, const PathCfg& cfg, const SketchSpecC& spec, const Rho& rho,
+                  double* x_out, BaselineRun& run) {
+  cudaStream_t s = ctx->stream;
+  const auto t_total = std::chrono::steady_clock::now();
+  const OpView op = ctx->op.primal();
+  const int64_t d = op.d;
+  DBuf<double> sa(static_cast<size_t>(spec.m * d), s);
+  sketch_apply(spec, op, sa.get(), s);
+  allreduce(ctx, sa.get(), spec.m * d);
+  GramOp gram;
+  gram.ctx = ctx;
+  gram.op = op;
+  gram.allow_fused = true;
+  DBuf<double> atb(static_cast<size_t>(d), s), x(static_cast<size_t>(d), s), xs(static_cast<size_t>(d), s),
+      g(static_cast<size_t>(d), s), grad(static_cast<size_t>(d), s), pg(static_cast<size_t>(d), s),
+      part(kDotParts, s), sc(2, s);
+  DBuf<int> flag(1, s);
+  op_apply_t(ctx, op, b, 1, atb.get(), true);
+  vec_dot(atb.get(), atb.get(), d, part.get(), sc.get(), s);
+  const double rhs_norm = std::sqrt(read_scalar(sc.get(), s));
+  // P for the swept shifts, factored in batches (reshift per lambda, :189)
+  const std::vector<size_t> order = descending_order(cfg.lambdas);
+  const int64_t nn = spec.m < d ? spec.m : d;
+  const int64_t per_batch =
+      std::max<int64_t>(1, std::min<int64_t>(64, (int64_t{1} << 31) / std::max<int64_t>(1, nn * nn * 8)));
+  run.setup_seconds = host_seconds_since(t_total);
+  const double tau_nominal = 2.0 / (1.0 / rho.rho1 + 1.0 / rho.rho2);
+  const double tol = cfg.epsilon * (rhs_norm > 0.0 ? rhs_norm : 1.0);
+  const int cap = 1000;
+  const size_t T = cfg.lambdas.size();
+  run.iterations.assign(T, 0);
+  run.seconds.assign(T, 0.0);
+  fill(x.get(), d, 0.0, s);
+  PrecondBatch P;
+  P.col_stable = true;
+  int64_t batch0 = -1;
+  for (size_t pos = 0; pos < T; ++pos) {
+    const size_t idx = order[pos];
+    const double lam = cfg.lambdas[idx];
+    const auto t_eval = std::chrono::steady_clock::now();
+    if (batch0 < 0 || static_cast<int64_t>(pos) >= batch0 + P.L) {
+      batch0 = static_cast<int64_t>(pos);
+      std::vector<double> shifts;
+      for (size_t q = pos; q < T && static_cast<int64_t>(shifts.size()) < per_batch; ++q)
+        shifts.push_back(cfg.lambdas[order[q]]);
+      P.build(ctx, sa.get(), nullptr, spec.m, d, shifts);
+    }
+    const PrecondBatch Pl = P.single(ctx, static_cast<int64_t>(pos) - batch0);
+    double tau = tau_nominal;
+    RP_CUDA(cudaMemcpyAsync(xs.get(), x.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+    int32_t iters = 0;
+    bool retried = false;
+    while (true) {
+      gram.apply(xs.get(), 1, g.get());
+      ihs_grad(g.get(), xs.get(), lam, atb.get(), d, grad.get(), s);
+      vec_dot(grad.get(), grad.get(), d, part.get(), sc.get(), s);
+      struct {
+        double nrm2;
+        int bad;
+      } h{};
+      RP_CUDA(cudaMemcpyAsync(&h.nrm2, sc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+      RP_CUDA(cudaMemcpyAsync(&h.bad, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+      RP_CUDA(cudaStreamSynchronize(s));
+      if (h.bad) {  // the previous step left a non-finite iterate (:201-208)
+        if (retried) throw SolverFailure("warm_ihs_path: diverged twice, even at tau/2");
+        retried = true;
+        tau /= 2.0;
+        RP_CUDA(cudaMemcpyAsync(xs.get(), x.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+        RP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+        iters = 0;
+        continue;
+      }
+      if (std::sqrt(h.nrm2) <= tol) break;
+      if (iters >= cap) throw SolverFailure("warm_ihs_path: iteration cap reached");
+      Pl.apply(ctx, grad.get(), d, 1, pg.get(), d);
+      ihs_step(xs.get(), pg.get(), tau, d, flag.get(), s);
+      ++iters;
+    }
+    RP_CUDA(cudaMemcpyAsync(x.get(), xs.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(x_out + static_cast<int64_t>(idx) * d, x.get(), sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    run.iterations[idx] = iters;
+    run.seconds[idx] = host_seconds_since(t_eval);
+  }
+  run.total_seconds = host_seconds_since(t_total);
+}
+
+// direct_path (baselines.cpp:80-118): G = A^T A once, then (G + lambda I)^{-1} A^T b
+// for batches of lambdas (batched Cholesky + triangular inverse on the tensor cores).
+void run_direct(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out, BaselineRun& run) {
+  cudaStream_t s = ctx->stream;
+  const auto t_total = std::chrono::steady_clock::now();
+  const OpView op = ctx->op.primal();
+  const int64_t d = op.d;
+  require(static_cast<double>(d) * d * 8.0 <= 32.0 * (1ull << 30), "direct_path: A^T A exceeds 32 GiB");
+  DBuf<double> G;
+  if (!op.sparse) {
+    GramOp gram;
+    gram.ctx = ctx;
+    gram.op = op;
+    gram.build_matrix();
+    G = std::move(gram.G);
+  } else {  // apply_transpose(a, apply(a, I)) (baselines.cpp:93), in column blocks
+    G.alloc(static_cast<size_t>(d * d), s);
+    GramOp gram;
+    gram.ctx = ctx;
+    gram.op = op;
+    const int64_t blk = std::min<int64_t>(d, 1024);
+    DBuf<double> eye(static_cast<size_t>(d * blk), s);
+    for (int64_t c0 = 0; c0 < d; c0 += blk) {
+      const int64_t cb = std::min(blk, d - c0);
+      identity_block(eye.get(), d, cb, c0, s);
+      gram.apply(eye.get(), cb, G.get() + c0 * d);
+    }
+  }
+  DBuf<double> atb(static_cast<size_t>(d), s);
+  op_apply_t(ctx, op, b, 1, atb.get(), true);
+  RP_CUDA(cudaStreamSynchronize(s));
+  run.setup_seconds = host_seconds_since(t_total);
+  const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(T, (int64_t{1} << 31) / std::max<int64_t>(1, d * d * 8)));
+  run.iterations.assign(static_cast<size_t>(T), 0);
+  run.seconds.assign(static_cast<size_t>(T), 0.0);
+  DBuf<double> h(static_cast<size_t>(per * d * d), s), inv(static_cast<size_t>(per * d * d), s),
+      shifts(static_cast<size_t>(per), s);
+  for (int64_t t0 = 0; t0 < T; t0 += per) {
+    const auto t_eval = std::chrono::steady_clock::now();
+    const int64_t tc = std::min(per, T - t0);
+    RP_CUDA(cudaMemcpyAsync(shifts.get(), cfg.lambdas.data() + t0, sizeof(double) * tc, cudaMemcpyHostToDevice, s));
+    shifted_copies(G.get(), d, shifts.get(), tc, h.get(), s);
+    try {
+      spd_inverse_batched(h.get(), d, d, d * d, tc, inv.get(), d, d * d, s);
+    } catch (const FactorFailure&) {
+      throw SolverFailure("direct_path: Cholesky factorization failed");
+    }
+    GemmArgs gx;  // x_t = (G + lambda_t I)^{-1} A^T b
+    gx.m = d;
+    gx.n = 1;
+    gx.k = d;
+    gx.a = inv.get();
+    gx.lda = d;
+    gx.stride_a = d * d;
+    gx.b = atb.get();
+    gx.ldb = d;
+    gx.stride_b = 0;
+    gx.c = x_out + t0 * d;
+    gx.ldc = d;
+    gx.stride_c = d;
+    gx.batch = tc;
+    dgemm(gx, s);
+    RP_CUDA(cudaStreamSynchronize(s));
+    const double secs = host_seconds_since(t_eval) / static_cast<double>(tc);
+    for (int64_t t = t0; t < t0 + tc; ++t) run.seconds[static_cast<size_t>(t)] = secs;
+  }
+  run.total_seconds = host_seconds_since(t_total);
+}
+
+void finish_baseline(const BaselineRun& run, int32_t* iterations, double* seconds, double* setup_total) {
+  if (iterations) std::copy(run.iterations.begin(), run.iterations.end(), iterations);
+  if (seconds) std::copy(run.seconds.begin(), run.seconds.end(), seconds);
+  if (setup_total) {
+    setup_total[0] = run.setup_seconds;
+    setup_total[1] = run.total_seconds;
+  }
+}
+
+}  // namespace rpb
+
+rp_status rp_warm_cg_path(rp_ctx* ctx, const double* b, const rp_path_config* cfgp, double* x_out, int where,
+                          int32_t* iterations, double* seconds, double* setup_total) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const PathCfg cfg = to_cfg(cfgp);
+    cfg.validate();
+    const OpView op = ctx->op.primal();
+    InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
+    OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
+    BaselineRun run;
+    run_warm_cg(ctx, bb.ptr, cfg, out.dev, run);
+    out.finish();
+    finish_baseline(run, iterations, seconds, setup_total);
+  });
+}
+
+rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_config* cfgp, const rp_sketch_spec* specp,
+                           const rp_rho_bounds* rhop, double* x_out, int where, int32_t* iterations, double* seconds,
+                           double* setup_total) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const PathCfg cfg = to_cfg(cfgp);
+    cfg.validate();
+    const Rho rho = to_rho(rhop);
+    rho_validate(rho);
+    const SketchSpecC spec = to_spec(specp);
+    const OpView op = ctx->op.primal();
+    require(spec.n == op.n_global, "warm_ihs_path: spec.n must equal A.rows");
+    validate_spec(spec);
+    InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
+    OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
+    BaselineRun run;
+    run_warm_ihs(ctx, bb.ptr, cfg, spec, rho, out.dev, run);
+    out.finish();
+    finish_baseline(run, iterations, seconds, setup_total);
+  });
+}
+
+rp_status rp_direct_path(rp_ctx* ctx, const double* b, const rp_path_config* cfgp, double* x_out, int where,
+                         double* seconds, double* setup_total) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const PathCfg cfg = to_cfg(cfgp);
+    cfg.validate();
+    const OpView op = ctx->op.primal();
+    InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
+    OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
+    BaselineRun run;
+    run_direct(ctx, bb.ptr, cfg, out.dev, run);
+    out.finish();
+    finish_baseline(run, nullptr, seconds, setup_total);
   });
 }
 

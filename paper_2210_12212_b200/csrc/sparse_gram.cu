@@ -181,14 +181,14 @@ __global__ void __launch_bounds__(256) pass2_kernel(const int64_t* __restrict__ 
 }
 
 template <int CPL>
-void run_chunk(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelCsc& pc,
+void run_chunk(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                const double* wr, int cc, double* yp, double* z, cudaStream_t s) {
   for (int64_t p = 0; p < pc.panels; ++p) {
     const int64_t row0 = p * pc.panel_rows;
     const int64_t rows = std::min(pc.panel_rows, pc.n - row0);
     pass1_kernel<CPL><<<grid_for(rows * 32), 256, 0, s>>>(csr_off, csr_col, csr_val, row0, rows, wr, cc, yp);
     RP_LAUNCH_CHECK();
-    pass2_kernel<CPL><<<grid_for(pc.d * 32), 256, 0, s>>>(pc.off.get() + p * pc.d, pc.row.get(), pc.val.get(), pc.d,
+    pass2_kernel<CPL><<<grid_for(pc.d * 32), 256, 0, s>>>(pc.off + p * pc.d, pc.row, pc.val, pc.d,
                                                           row0, yp, cc, z, p == 0);
     RP_LAUNCH_CHECK();
   }
@@ -218,7 +218,7 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
     build_impl<uint64_t>(csr_off, csr_col, csr_val, n, d, nnz, panel_rows, out, s);
 }
 
-void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelCsc& pc,
+void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s) {
   if (cols <= 0 || pc.d <= 0) return;
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, 128));

@@ -35,12 +35,28 @@ struct PanelCsc {
   }
 };
 
+// Non-owning view of a panel CSC.  The operator's plain CSC (d + 1 offsets,
+// rows ascending per column) is the one-panel case.
+struct PanelView {
+  int64_t n = 0, d = 0, panel_rows = 0, panels = 0;
+  const int64_t* off = nullptr;
+  const int32_t* row = nullptr;
+  const double* val = nullptr;
+};
+inline PanelView view_of(const PanelCsc& pc) {
+  return PanelView{pc.n, pc.d, pc.panel_rows, pc.panels, pc.off.get(), pc.row.get(), pc.val.get()};
+}
+inline PanelView single_panel(int64_t n, int64_t d, const int64_t* csc_off, const int32_t* csc_row,
+                              const double* csc_val) {
+  return PanelView{n, d, n > 0 ? n : 1, 1, csc_off, csc_row, csc_val};
+}
+
 // Build the panel CSC on the device (stable radix sort of (panel, column) keys).
 void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, int64_t n, int64_t d,
                      int64_t nnz, int64_t panel_rows, PanelCsc& out, cudaStream_t s);
 
 // Y (d x cols, column-major, ld ldy) = M^T (M W), W (d x cols, column-major, ld ldw).
-void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelCsc& pc,
+void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s);
 
 }  // namespace rpb

@@ -9,6 +9,7 @@
 #include "common.h"
 #include "factor.h"
 #include "gemm_f64.h"
+#include "vecops.h"
 
 namespace rpb {
 
@@ -135,33 +136,6 @@ RhoResult envelope_from_spectrum(int kind, int64_t m_rows, int64_t n_rows, const
 
 namespace {
 
-constexpr int kRedBlocks = 296;  // fixed: the reduction order never depends on the device
-
-// part[b] = sum over the b-th fixed slice of x[i] * y[i] (i < count), fixed order.
-__global__ void dot_partials_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t count,
-                                    double* __restrict__ part) {
-  __shared__ double sh[256];
-  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = blockIdx.x * per, hi = min(count, lo + per);
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc = __fma_rn(x[i], y[i], acc);
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
-}
-
-__global__ void sum_partials_kernel(const double* __restrict__ part, int count, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < count; ++i) s += part[i];
-    *out = s;
-  }
-}
-
 // v_out = w / sqrt(nrm2); also stores beta = sqrt(nrm2).
 __global__ void normalize_kernel(const double* __restrict__ w, int64_t n, const double* __restrict__ nrm2,
                                  double* __restrict__ v_out, double* __restrict__ beta) {
@@ -188,13 +162,6 @@ __global__ void start_kernel(double* __restrict__ v, int64_t n) {
 
 unsigned blocks_for(int64_t work) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16)));
-}
-
-void dot(const double* x, const double* y, int64_t count, double* part, double* out, cudaStream_t s) {
-  dot_partials_kernel<<<kRedBlocks, 256, 0, s>>>(x, y, count, part);
-  RP_LAUNCH_CHECK();
-  sum_partials_kernel<<<1, 32, 0, s>>>(part, kRedBlocks, out);
-  RP_LAUNCH_CHECK();
 }
 
 // Largest eigenvalue of the symmetric tridiagonal (a[0..k), b[0..k-1)) by
@@ -254,14 +221,14 @@ SketchedSpectrum sketched_spectrum(const double* sa, int64_t m, int64_t d, doubl
     g.mirror = true;
     dgemm(g, s);
   }
-  DBuf<double> part(kRedBlocks, s), scal(4, s);
+  DBuf<double> part(kDotParts, s), scal(4, s);
   // ||D||_F^2 = tr(H (H + l0 I)^{-1}) = <H, (H + l0 I)^{-1}>_F  (both symmetric)
   {
     DBuf<double> l0(1, s), hs(static_cast<size_t>(N * N), s), inv(static_cast<size_t>(N * N), s);
     RP_CUDA(cudaMemcpyAsync(l0.get(), &lambda0, sizeof(double), cudaMemcpyHostToDevice, s));
     shifted_copies(H.get(), N, l0.get(), 1, hs.get(), s);
     spd_inverse_batched(hs.get(), N, N, N * N, 1, inv.get(), N, N * N, s);
-    dot(H.get(), inv.get(), N * N, part.get(), scal.get(), s);
+    vec_dot(H.get(), inv.get(), N * N, part.get(), scal.get(), s);
     RP_CUDA(cudaMemcpyAsync(&out.sum_dii_sq, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     RP_CUDA(cudaStreamSynchronize(s));
   }
@@ -319,7 +286,7 @@ SketchedSpectrum sketched_spectrum(const double* sa, int64_t m, int64_t d, doubl
       up.ldc = N;
       dgemm(up, s);
     }
-    dot(w.get(), w.get(), N, part.get(), scal.get(), s);
+    vec_dot(w.get(), w.get(), N, part.get(), scal.get(), s);
     normalize_kernel<<<blocks_for(N), 256, 0, s>>>(w.get(), N, scal.get(), V.get() + (j + 1) * N, scal.get() + 1);
     RP_LAUNCH_CHECK();
     double bj = 0.0;

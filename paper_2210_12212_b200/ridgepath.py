@@ -143,6 +143,10 @@ SIGNATURES = {
     "rp_count_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
     "rp_srht_draws": ([_P, ctypes.POINTER(_SketchSpec), _P, _P, _INT], _INT),
     "rp_mt_selfcheck": ([_U64, _U64], _INT),
+    "rp_warm_cg_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P, _P], _INT),
+    "rp_warm_ihs_path": ([_P, _P, ctypes.POINTER(_PathConfig), ctypes.POINTER(_SketchSpec), ctypes.POINTER(_Rho), _P,
+                          _INT, _P, _P, _P], _INT),
+    "rp_direct_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
     "rp_derive_rho": ([_P, ctypes.POINTER(_SketchSpec), _INT, _D, _D, ctypes.POINTER(_Rho),
                        ctypes.POINTER(_SpectrumInfo)], _INT),
     "rp_effective_dimension": ([_P, _I64, _D, _P], _INT),
@@ -304,6 +308,7 @@ class PathPoint:
     seconds: float = 0.0
     train_loss: float = 0.0  # 0.5 ||A x - b||^2 + 0.5 lam ||x||^2  (path_solver.cpp:425-439)
     test_loss: Optional[float] = None  # 0.5 ||A_test x - b_test||^2 when a test set is given
+    iterations: int = 0  # inner iterations (the iterative baselines, baselines.cpp:25-38)
 
 
 @dataclass
@@ -759,6 +764,67 @@ def dual_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, sigma_
     if spec.n != _cols(a):
         raise ValueError("dual_path: spec.n must equal A.cols (the dual operator is A^T)")
     return _run_path(True, a, b, config, spec, rho, sigma_d, ctx, a_test=a_test, b_test=b_test)
+
+
+# ---------------------------------------------------------------------------
+# Comparison baselines (baselines.hpp; baselines.cpp:80-226)
+# ---------------------------------------------------------------------------
+
+
+def _baseline(name, fn, a, b, config: PathConfig, ctx, a_test, b_test, *extra, iterative=True) -> RegPathResult:
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    b = np.asarray(b)
+    if b.ndim != 1 and not (b.ndim == 2 and b.shape[1] == 1):
+        raise ValueError(f"{name}_path: b must be a vector")
+    b1 = _f64(b.reshape(-1))
+    if b1.shape[0] != _rows(a):
+        raise ValueError(f"{name}_path: dimension mismatch")
+    T = len(config.lambdas)
+    d = _cols(a)
+    out = np.empty(d * max(T, 1))
+    cfg, keep = config.c()
+    iters = np.zeros(max(T, 1), dtype=np.int32)
+    secs = np.zeros(max(T, 1))
+    st = np.zeros(2)
+    args = [ctx.handle, _ptr(b1), ctypes.byref(cfg), *extra, _ptr(out), RP_HOST]
+    args += [_ptr(iters), _ptr(secs), _ptr(st)] if iterative else [_ptr(secs), _ptr(st)]
+    ctx.check(fn(*args))
+    del keep
+    lam = np.asarray(config.lambdas, dtype=np.float64)
+    b2 = b1.reshape(-1, 1)
+    train = _losses_flat(ctx, b2, 1, T, out, lam) if T else np.empty(0)
+    test = None
+    if a_test is not None and b_test is not None and T:
+        bt = _f64(np.asarray(b_test).reshape(-1, 1))
+        if _cols(a_test) != d or bt.shape[0] != _rows(a_test):
+            raise ValueError("losses: test dimension mismatch")
+        ctx.set_operator(a_test)
+        test = _losses_flat(ctx, bt, 1, T, out, None)
+        ctx.set_operator(a)
+    pts = [PathPoint(float(config.lambdas[t]), out[t * d:(t + 1) * d].reshape(d, 1).copy(), seconds=float(secs[t]),
+                     train_loss=float(train[t]), test_loss=float(test[t]) if test is not None else None,
+                     iterations=int(iters[t])) for t in range(T)]
+    return RegPathResult(name, pts, float(st[0]), float(st[1]))
+
+
+def warm_cg_path(a, b, config: PathConfig, ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
+    """baselines.hpp: CG on the normal equations, descending warm-started sweep."""
+    return _baseline("cg", lib().rp_warm_cg_path, a, b, config, ctx, a_test, b_test)
+
+
+def warm_ihs_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, ctx: Optional[Context] = None,
+                  a_test=None, b_test=None) -> RegPathResult:
+    """baselines.hpp: warm-started sketched Newton iterations per lambda."""
+    if spec.n != _rows(a):
+        raise ValueError("warm_ihs_path: spec.n must equal A.rows")
+    return _baseline("ihs", lib().rp_warm_ihs_path, a, b, config, ctx, a_test, b_test, ctypes.byref(spec.c()),
+                     ctypes.byref(rho.c()))
+
+
+def direct_path(a, b, config: PathConfig, ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
+    """baselines.hpp: A^T A once, (A^T A + lambda I)^{-1} A^T b per lambda."""
+    return _baseline("direct", lib().rp_direct_path, a, b, config, ctx, a_test, b_test, iterative=False)
 
 
 # ---------------------------------------------------------------------------

@@ -374,9 +374,11 @@ def test_dual_csr_path_matches_oracle(rp, ctx, oracle):
                            oracle.SketchSpec("countsketch", 40, d, 1, 4), oracle.RhoBounds.manual(1.0, 1e-5))
     try:
         ctx.set_option("csr_panel_rows", 37)
+        ctx.set_option("csr_one_panel_bytes", 0)
         got = rp.dual_path(gc, b, rp.PathConfig(1e-1, 1e1, list(grid), 1e-6), rp.SketchSpec("countsketch", 40, d, 1, 4),
                            rp.RhoBounds.manual(1.0, 1e-5), ctx=ctx)
     finally:
         ctx.set_option("csr_panel_rows", 65536)
+        ctx.set_option("csr_one_panel_bytes", 48 << 20)
     worst, npts = _worst(got.points, ref.points, oracle)
     assert npts == len(grid) and worst < TOL

@@ -147,8 +147,9 @@ def test_narrow_passes(rp, ctx, oracle, n, d, k):
         assert np.array_equal(rp.apply_transpose(a, y[:, j].copy(), ctx=ctx), t_all[:, j])
 
 
-@pytest.mark.parametrize("panel,chunk", [(65536, 64), (7, 64), (64, 5), (1, 1), (100, 33), (1000, 17)])
-def test_csr_panel_gram_bitwise(rp, ctx, oracle, panel, chunk):
+@pytest.mark.parametrize("panel,chunk,one", [(65536, 64, 0), (7, 64, 0), (64, 5, 0), (1, 1, 0), (100, 33, 0),
+                                             (1000, 17, 0), (7, 128, 1 << 40), (7, 100, 0)])
+def test_csr_panel_gram_bitwise(rp, ctx, oracle, panel, chunk, one):
     """The L2-blocked sparse Gram (sparse_gram.cu) continues each column's
     running sum across row panels, so it equals apply followed by
     apply_transpose (matrix.cpp:168-172) bit for bit, whatever the panel and
@@ -164,6 +165,7 @@ def test_csr_panel_gram_bitwise(rp, ctx, oracle, panel, chunk):
     try:
         ctx.set_option("csr_panel_rows", panel)
         ctx.set_option("csr_chunk", chunk)
+        ctx.set_option("csr_one_panel_bytes", one)
         got = rp.gram_apply(gc, x, ctx=ctx)
         assert np.array_equal(got, two_pass)
         assert oracle.rel_error(got, oracle.gram_apply(oc, x)) < 1e-14
@@ -171,7 +173,8 @@ def test_csr_panel_gram_bitwise(rp, ctx, oracle, panel, chunk):
         assert np.array_equal(rp.gram_apply(gc, x[:, 3].copy(), ctx=ctx), two_pass[:, 3])
     finally:
         ctx.set_option("csr_panel_rows", 65536)
-        ctx.set_option("csr_chunk", 64)
+        ctx.set_option("csr_chunk", 128)
+        ctx.set_option("csr_one_panel_bytes", 48 << 20)
 
 
 def test_csr_panel_gram_empty_matrix(rp, ctx, oracle):
