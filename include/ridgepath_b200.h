@@ -240,6 +240,44 @@ RP_API rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_co
 RP_API rp_status rp_direct_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
                                 double* seconds, double* setup_total);
 
+/* ---- adaptive sketch dimension (adaptive.hpp; adaptive.cpp:19-137) --------
+ * AdaptiveConfig / AdaptiveStep / AdaptiveResult; m_initial, m_cap = 0 select
+ * the reference defaults max(16, d/64) and d.  The trace holds every step
+ * (trace_len); the first trace_cap entries are copied to `trace` (nullable).
+ * x0 (nullable, d entries) and x_out (d entries) live on `where`. */
+typedef struct {
+  double gamma1;   /* backtracking factor (0.5) */
+  double gamma2;   /* sufficient-decrease fraction (1e-4) */
+  double gamma3;   /* stall threshold (0.9) */
+  double epsilon;  /* progress tolerance (1e-8) */
+  int64_t m_initial;
+  int64_t m_cap;
+  int32_t iteration_cap; /* (200) */
+} rp_adaptive_config;
+
+typedef struct {
+  int64_t m;
+  double f_before;
+  double f_after;
+  double step;
+  double progress;
+  int32_t doubled;
+} rp_adaptive_step;
+
+typedef struct {
+  int64_t m;
+  int32_t iterations;
+  int32_t doublings;
+  int32_t converged;
+  int32_t stalled_at_cap;
+  int64_t trace_len;
+} rp_adaptive_result;
+
+RP_API rp_status rp_adaptive_sketch_dim(rp_ctx* ctx, const double* b, double lambda_min, const rp_adaptive_config* cfg,
+                                        const rp_sketch_spec* spec_template, const double* x0, double* x_out,
+                                        int where, rp_adaptive_result* result, rp_adaptive_step* trace,
+                                        int64_t trace_cap);
+
 /* ---- plug-in envelope (derive_rho, tools/ridgepath_main.cpp:218-279) ------
  * The reference CLI derives (rho1, rho2) from the sketched spectrum when
  * --rho1/--rho2 are absent: sketch A, thin SVD of SA, effective dimension at

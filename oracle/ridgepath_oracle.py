@@ -946,6 +946,133 @@ def warm_ihs_path(a, b: np.ndarray, config: PathConfig, spec: SketchSpec, rho: R
     return RegPathResult("ihs", pts)
 
 
+# --------------------------------------------------------------------------
+# Adaptive sketch dimension (adaptive.hpp; adaptive.cpp:19-137)
+# --------------------------------------------------------------------------
+
+@dataclass
+class AdaptiveConfig:
+    gamma1: float = 0.5
+    gamma2: float = 1e-4
+    gamma3: float = 0.9
+    epsilon: float = 1e-8
+    m_initial: int = 0
+    m_cap: int = 0
+    iteration_cap: int = 200
+
+    def initial_m(self, d):
+        return self.m_initial if self.m_initial > 0 else max(16, d // 64)
+
+    def cap_m(self, d):
+        return self.m_cap if self.m_cap > 0 else d
+
+    def validate(self, d):
+        """adaptive.cpp:19-28."""
+        _require(0.0 < self.gamma1 < 1.0, "adaptive: gamma1 not in (0,1)")
+        _require(0.0 < self.gamma2 < 1.0, "adaptive: gamma2 not in (0,1)")
+        _require(0.0 < self.gamma3 < 1.0, "adaptive: gamma3 not in (0,1)")
+        _require(self.epsilon > 0.0, "adaptive: epsilon must be positive")
+        _require(self.initial_m(d) >= 1, "adaptive: m_initial must be >= 1")
+        _require(self.cap_m(d) <= d, "adaptive: m_cap must not exceed d")
+        _require(self.initial_m(d) <= self.cap_m(d), "adaptive: m_initial above m_cap")
+        _require(self.iteration_cap >= 1, "adaptive: iteration cap must be >= 1")
+
+
+@dataclass
+class AdaptiveStep:
+    m: int
+    f_before: float
+    f_after: float
+    step: float
+    progress: float
+    doubled: bool
+
+
+@dataclass
+class AdaptiveResult:
+    m: int
+    x: np.ndarray
+    iterations: int = 0
+    doublings: int = 0
+    converged: bool = False
+    stalled_at_cap: bool = False
+    trace: List[AdaptiveStep] = field(default_factory=list)
+
+
+def armijo_step(f, x, direction, dir_dot_grad, gamma1, gamma2) -> float:
+    """adaptive.cpp:39-51."""
+    _require(dir_dot_grad > 0.0, "armijo: direction is not a descent direction")
+    fx = f(x)
+    step = 1.0
+    for _ in range(51):
+        if f(x - step * direction) <= fx - gamma2 * step * dir_dot_grad:
+            return step
+        step *= gamma1
+    raise SolverError("armijo: no acceptable step within 50 backtracks")
+
+
+def adaptive_sketch_dim(a, b, lambda_min: float, config: AdaptiveConfig, spec_template: SketchSpec,
+                        x0=None) -> AdaptiveResult:
+    """adaptive.cpp:53-135: sketched Newton steps at lambda_min with Armijo
+    steps, doubling m (fresh seed per doubling) when d.grad stalls."""
+    _require(lambda_min > 0.0, "adaptive: lambda_min must be positive")
+    _require(b.shape[0] == _rows(a), "adaptive: dimension mismatch")
+    d = _cols(a)
+    config.validate(d)
+    atb = apply_transpose(a, b)
+
+    def objective(x):
+        r = apply(a, x) - b
+        return 0.5 * float(r @ r) + 0.5 * lambda_min * float(x @ x)
+
+    def gradient(x):
+        return gram_apply(a, x) + lambda_min * x - atb
+
+    res = AdaptiveResult(config.initial_m(d), np.array(x0, dtype=np.float64) if x0 is not None else np.zeros(d))
+    m_cap = config.cap_m(d)
+
+    def make_pre(m, resample):
+        seed = (spec_template.seed + 0x9E3779B97F4A7C15 * resample) % (1 << 64)
+        spec = SketchSpec(spec_template.kind, m, spec_template.n, spec_template.s, seed)
+        if spec.kind == "identity":
+            spec.m = spec.n
+        if spec.kind == "sjlt" and spec.m % spec.s != 0:
+            spec.m += spec.s - spec.m % spec.s
+        return Preconditioner.build(sketch_apply(spec, a), lambda_min)
+
+    pre = make_pre(res.m, 0)
+    grad = gradient(res.x)
+    direction = pre.apply(grad)
+    progress = float(direction @ grad)
+    loop_guard = 0
+    while progress >= config.epsilon:
+        loop_guard += 1
+        if res.iterations >= config.iteration_cap or loop_guard > 4 * config.iteration_cap:
+            break
+        step = armijo_step(objective, res.x, direction, progress, config.gamma1, config.gamma2)
+        x_next = res.x - step * direction
+        grad_next = gradient(x_next)
+        dir_next = pre.apply(grad_next)
+        progress_next = float(dir_next @ grad_next)
+        rec = AdaptiveStep(res.m, objective(res.x), objective(x_next), step, progress, False)
+        if progress_next >= config.gamma3 * progress and res.m < m_cap:
+            res.m = min(2 * res.m, m_cap)
+            res.doublings += 1
+            rec.doubled = True
+            pre = make_pre(res.m, res.doublings)
+            grad = gradient(res.x)
+            direction = pre.apply(grad)
+            progress = float(direction @ grad)
+        else:
+            res.x = x_next
+            grad, direction, progress = grad_next, dir_next, progress_next
+            res.iterations += 1
+        res.trace.append(rec)
+    res.converged = progress < config.epsilon
+    res.stalled_at_cap = (not res.converged) and res.m >= m_cap
+    return res
+
+
 def losses(a, b, x, lam, a_test=None, b_test=None):
     """path_solver.cpp:425-438."""
     resid = apply(a, x) - b

@@ -1952,6 +1952,133 @@ void run_direct(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out,
   run.total_seconds = host_seconds_since(t_total);
 }
 
+// adaptive_sketch_dim (adaptive.cpp:53-135): sketched Newton steps at
+// lambda_min with Armijo backtracking, doubling m under a fresh seed when the
+// progress measure d.grad stalls.  Every vector lives on the device; the
+// objective is one pass over the operator plus two dots.
+void run_adaptive(rp_ctx* ctx, const double* b, double lambda_min, const rp_adaptive_config& cfg,
+                  const SketchSpecC& tmpl, const double* x0, double* x_out, rp_adaptive_result& res,
+                  std::vector<rp_adaptive_step>& trace) {
+  cudaStream_t s = ctx->stream;
+  const OpView op = ctx->op.primal();
+  const int64_t d = op.d, nl = op.n_loc;
+  // AdaptiveConfig::validate / initial_m / cap_m (adaptive.cpp:19-37)
+  const int64_t m0 = cfg.m_initial > 0 ? cfg.m_initial : std::max<int64_t>(16, d / 64);
+  const int64_t m_cap = cfg.m_cap > 0 ? cfg.m_cap : d;
+  require(lambda_min > 0.0, "adaptive: lambda_min must be positive");
+  require(cfg.gamma1 > 0.0 && cfg.gamma1 < 1.0, "adaptive: gamma1 not in (0,1)");
+  require(cfg.gamma2 > 0.0 && cfg.gamma2 < 1.0, "adaptive: gamma2 not in (0,1)");
+  require(cfg.gamma3 > 0.0 && cfg.gamma3 < 1.0, "adaptive: gamma3 not in (0,1)");
+  require(cfg.epsilon > 0.0, "adaptive: epsilon must be positive");
+  require(m0 >= 1, "adaptive: m_initial must be >= 1");
+  require(m_cap <= d, "adaptive: m_cap must not exceed d");
+  require(m0 <= m_cap, "adaptive: m_initial above m_cap");
+  require(cfg.iteration_cap >= 1, "adaptive: iteration cap must be >= 1");
+  require(tmpl.n == op.n_global, "sketch_apply: spec.n must match A.rows");
+  GramOp gram;
+  gram.ctx = ctx;
+  gram.op = op;
+  gram.allow_fused = true;
+  auto vec = [&](int64_t n) { return DBuf<double>(static_cast<size_t>(std::max<int64_t>(n, 1)), s); };
+  DBuf<double> atb = vec(d), x = vec(d), xt = vec(d), xn = vec(d), g = vec(d), grad = vec(d), gradn = vec(d),
+               dir = vec(d), dirn = vec(d), r = vec(nl), part(kDotParts, s), sc(4, s);
+  DBuf<int> flag(1, s);
+  op_apply_t(ctx, op, b, 1, atb.get(), true);
+  auto dot = [&](const double* u, const double* v, int64_t n, bool reduce) {
+    vec_dot(u, v, n, part.get(), sc.get(), s);
+    if (reduce) allreduce(ctx, sc.get(), 1);
+    return read_scalar(sc.get(), s);
+  };
+  auto objective = [&](const double* xv) {  // 0.5 ||A x - b||^2 + 0.5 lambda ||x||^2
+    op_apply(ctx, op, xv, 1, r.get());
+    residual_in_place(r.get(), b, nl, s);
+    const double rr = dot(r.get(), r.get(), nl, true);
+    const double xx = dot(xv, xv, d, false);
+    return 0.5 * rr + 0.5 * lambda_min * xx;
+  };
+  auto gradient = [&](const double* xv, double* out) {  // gram_apply(a, x) + lambda x - atb
+    gram.apply(xv, 1, g.get());
+    ihs_grad(g.get(), xv, lambda_min, atb.get(), d, out, s);
+  };
+  auto axpy_to = [&](const double* xv, double step, const double* dv, double* out) {  // out = x - step d
+    RP_CUDA(cudaMemcpyAsync(out, xv, sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+    ihs_step(out, dv, step, d, flag.get(), s);
+  };
+  PrecondBatch P;
+  DBuf<double> sa;
+  auto make_pre = [&](int64_t m, int resample) {
+    SketchSpecC spec = tmpl;
+    spec.m = m;
+    spec.seed = tmpl.seed + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(resample);
+    if (spec.kind == kIdentity) spec.m = spec.n;
+    if (spec.kind == kSjlt && spec.m % spec.s != 0) spec.m += spec.s - spec.m % spec.s;
+    validate_spec(spec);
+    sa.alloc(static_cast<size_t>(spec.m * d), s);
+    sketch_apply(spec, op, sa.get(), s);
+    allreduce(ctx, sa.get(), spec.m * d);
+    P.build(ctx, sa.get(), nullptr, spec.m, d, {lambda_min});
+  };
+  res = rp_adaptive_result{};
+  res.m = m0;
+  if (x0)
+    RP_CUDA(cudaMemcpyAsync(x.get(), x0, sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+  else
+    fill(x.get(), d, 0.0, s);
+  make_pre(res.m, 0);
+  gradient(x.get(), grad.get());
+  P.apply(ctx, grad.get(), d, 1, dir.get(), d);
+  double progress = dot(dir.get(), grad.get(), d, false);
+  int loop_guard = 0;
+  while (progress >= cfg.epsilon) {
+    if (res.iterations >= cfg.iteration_cap || ++loop_guard > 4 * cfg.iteration_cap) break;
+    // armijo_step (adaptive.cpp:39-51)
+    require(progress > 0.0, "armijo: direction is not a descent direction");
+    const double fx = objective(x.get());
+    double step = 1.0;
+    bool found = false;
+    for (int j = 0; j <= 50; ++j) {
+      axpy_to(x.get(), step, dir.get(), xt.get());
+      if (objective(xt.get()) <= fx - cfg.gamma2 * step * progress) {
+        found = true;
+        break;
+      }
+      step *= cfg.gamma1;
+    }
+    if (!found) throw SolverFailure("armijo: no acceptable step within 50 backtracks");
+    axpy_to(x.get(), step, dir.get(), xn.get());
+    gradient(xn.get(), gradn.get());
+    P.apply(ctx, gradn.get(), d, 1, dirn.get(), d);
+    const double progress_next = dot(dirn.get(), gradn.get(), d, false);
+    rp_adaptive_step rec{};
+    rec.m = res.m;
+    rec.f_before = objective(x.get());
+    rec.f_after = objective(xn.get());
+    rec.step = step;
+    rec.progress = progress;
+    if (progress_next >= cfg.gamma3 * progress && res.m < m_cap) {
+      res.m = std::min(2 * res.m, m_cap);
+      ++res.doublings;
+      rec.doubled = 1;
+      make_pre(res.m, res.doublings);
+      gradient(x.get(), grad.get());
+      P.apply(ctx, grad.get(), d, 1, dir.get(), d);
+      progress = dot(dir.get(), grad.get(), d, false);
+    } else {
+      std::swap(x, xn);
+      std::swap(grad, gradn);
+      std::swap(dir, dirn);
+      progress = progress_next;
+      ++res.iterations;
+    }
+    trace.push_back(rec);
+  }
+  res.converged = progress < cfg.epsilon ? 1 : 0;
+  res.stalled_at_cap = (!res.converged && res.m >= m_cap) ? 1 : 0;
+  res.trace_len = static_cast<int64_t>(trace.size());
+  RP_CUDA(cudaMemcpyAsync(x_out, x.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+}
+
 void finish_baseline(const BaselineRun& run, int32_t* iterations, double* seconds, double* setup_total) {
   if (iterations) std::copy(run.iterations.begin(), run.iterations.end(), iterations);
   if (seconds) std::copy(run.seconds.begin(), run.seconds.end(), seconds);
@@ -1998,6 +2125,25 @@ rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_config* c
     run_warm_ihs(ctx, bb.ptr, cfg, spec, rho, out.dev, run);
     out.finish();
     finish_baseline(run, iterations, seconds, setup_total);
+  });
+}
+
+rp_status rp_adaptive_sketch_dim(rp_ctx* ctx, const double* b, double lambda_min, const rp_adaptive_config* cfg,
+                                 const rp_sketch_spec* spec_template, const double* x0, double* x_out, int where,
+                                 rp_adaptive_result* result, rp_adaptive_step* trace, int64_t trace_cap) {
+  if (!ctx || !cfg || !result) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const SketchSpecC tmpl = to_spec(spec_template);
+    const OpView op = ctx->op.primal();
+    require(trace_cap >= 0, "adaptive: negative trace capacity");
+    InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
+    InBuf xb(x0, x0 ? static_cast<size_t>(op.d) : 0, where, ctx->stream);
+    OutBuf out(x_out, static_cast<size_t>(op.d), where, ctx->stream);
+    std::vector<rp_adaptive_step> tr;
+    run_adaptive(ctx, bb.ptr, lambda_min, *cfg, tmpl, x0 ? xb.ptr : nullptr, out.dev, *result, tr);
+    out.finish();
+    if (trace)
+      for (int64_t i = 0; i < std::min<int64_t>(trace_cap, static_cast<int64_t>(tr.size())); ++i) trace[i] = tr[i];
   });
 }
 

@@ -100,7 +100,17 @@ __global__ void identity_block_kernel(double* __restrict__ out, int64_t d, int64
   }
 }
 
+__global__ void residual_kernel(double* __restrict__ r, const double* __restrict__ b, int64_t n) {
+  RP_GRID_STRIDE(i, n) r[i] = __dsub_rn(r[i], b[i]);
+}
+
 }  // namespace
+
+void residual_in_place(double* r, const double* b, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  residual_kernel<<<blocks_for(n), 256, 0, s>>>(r, b, n);
+  RP_LAUNCH_CHECK();
+}
 
 void identity_block(double* out, int64_t d, int64_t cols, int64_t c0, cudaStream_t s) {
   identity_block_kernel<<<blocks_for(d * cols), 256, 0, s>>>(out, d, cols, c0);

@@ -69,6 +69,22 @@ class _SpectrumInfo(ctypes.Structure):
                 ("dnorm_sq", ctypes.c_double), ("lambda0", ctypes.c_double), ("lanczos_steps", ctypes.c_int32)]
 
 
+class _AdaptiveConfig(ctypes.Structure):
+    _fields_ = [("gamma1", ctypes.c_double), ("gamma2", ctypes.c_double), ("gamma3", ctypes.c_double),
+                ("epsilon", ctypes.c_double), ("m_initial", ctypes.c_int64), ("m_cap", ctypes.c_int64),
+                ("iteration_cap", ctypes.c_int32)]
+
+
+class _AdaptiveStep(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("f_before", ctypes.c_double), ("f_after", ctypes.c_double),
+                ("step", ctypes.c_double), ("progress", ctypes.c_double), ("doubled", ctypes.c_int32)]
+
+
+class _AdaptiveResult(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("iterations", ctypes.c_int32), ("doublings", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("stalled_at_cap", ctypes.c_int32), ("trace_len", ctypes.c_int64)]
+
+
 class _Rate(ctypes.Structure):
     _fields_ = [("lambda0", ctypes.c_double), ("alpha", ctypes.c_double), ("kappa", ctypes.c_double),
                 ("contraction", ctypes.c_double), ("k", ctypes.c_int32)]
@@ -147,6 +163,8 @@ SIGNATURES = {
     "rp_warm_ihs_path": ([_P, _P, ctypes.POINTER(_PathConfig), ctypes.POINTER(_SketchSpec), ctypes.POINTER(_Rho), _P,
                           _INT, _P, _P, _P], _INT),
     "rp_direct_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
+    "rp_adaptive_sketch_dim": ([_P, _P, _D, ctypes.POINTER(_AdaptiveConfig), ctypes.POINTER(_SketchSpec), _P, _P, _INT,
+                                ctypes.POINTER(_AdaptiveResult), _P, _I64], _INT),
     "rp_derive_rho": ([_P, ctypes.POINTER(_SketchSpec), _INT, _D, _D, ctypes.POINTER(_Rho),
                        ctypes.POINTER(_SpectrumInfo)], _INT),
     "rp_effective_dimension": ([_P, _I64, _D, _P], _INT),
@@ -825,6 +843,72 @@ def warm_ihs_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, ct
 def direct_path(a, b, config: PathConfig, ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
     """baselines.hpp: A^T A once, (A^T A + lambda I)^{-1} A^T b per lambda."""
     return _baseline("direct", lib().rp_direct_path, a, b, config, ctx, a_test, b_test, iterative=False)
+
+
+# ---------------------------------------------------------------------------
+# Adaptive sketch dimension (adaptive.hpp; adaptive.cpp:19-137)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class AdaptiveConfig:
+    """adaptive.hpp AdaptiveConfig (m_initial / m_cap 0 = the reference defaults)."""
+    gamma1: float = 0.5
+    gamma2: float = 1e-4
+    gamma3: float = 0.9
+    epsilon: float = 1e-8
+    m_initial: int = 0
+    m_cap: int = 0
+    iteration_cap: int = 200
+
+    def c(self):
+        return _AdaptiveConfig(self.gamma1, self.gamma2, self.gamma3, self.epsilon, int(self.m_initial),
+                               int(self.m_cap), int(self.iteration_cap))
+
+
+@dataclass
+class AdaptiveStep:
+    m: int
+    f_before: float
+    f_after: float
+    step: float
+    progress: float
+    doubled: bool
+
+
+@dataclass
+class AdaptiveResult:
+    m: int
+    x: np.ndarray
+    iterations: int = 0
+    doublings: int = 0
+    converged: bool = False
+    stalled_at_cap: bool = False
+    trace: List[AdaptiveStep] = field(default_factory=list)
+
+
+def adaptive_sketch_dim(a, b, lambda_min: float, config: AdaptiveConfig, spec_template: "SketchSpec", x0=None,
+                        ctx: Optional[Context] = None) -> AdaptiveResult:
+    """adaptive_sketch_dim (adaptive.hpp) on the device."""
+    ctx = ctx or default_context()
+    ctx.set_operator(a)
+    b1 = _f64(np.asarray(b).reshape(-1))
+    if b1.shape[0] != _rows(a):
+        raise ValueError("adaptive: dimension mismatch")
+    d = _cols(a)
+    x = np.empty(d)
+    xv = _f64(np.asarray(x0).reshape(-1)) if x0 is not None else None
+    if xv is not None and xv.shape[0] != d:
+        raise ValueError("adaptive: x0 dimension mismatch")
+    res = _AdaptiveResult()
+    cap = 4 * int(config.iteration_cap) + 8
+    tr = (_AdaptiveStep * cap)()
+    ctx.check(lib().rp_adaptive_sketch_dim(ctx.handle, _ptr(b1), float(lambda_min), ctypes.byref(config.c()),
+                                           ctypes.byref(spec_template.c()), _ptr(xv) if xv is not None else None,
+                                           _ptr(x), RP_HOST, ctypes.byref(res), ctypes.cast(tr, _P), cap))
+    steps = [AdaptiveStep(t.m, t.f_before, t.f_after, t.step, t.progress, bool(t.doubled))
+             for t in tr[:min(cap, res.trace_len)]]
+    return AdaptiveResult(res.m, x, res.iterations, res.doublings, bool(res.converged), bool(res.stalled_at_cap), steps)
 
 
 # ---------------------------------------------------------------------------

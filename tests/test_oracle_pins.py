@@ -429,3 +429,63 @@ def test_baselines_oracle_agree_pairwise(oracle):  # test_baselines.cpp:133-151
         for j in range(i + 1, 4):
             for p, q in zip(allp[i].points, allp[j].points):
                 assert oracle.rel_error(p.solution, q.solution) < 10 * tol
+
+
+# ---- adaptive sketch dimension: adaptive.cpp against test_adaptive.cpp ----
+
+def _tspec(oracle, kind, n, seed):
+    return oracle.SketchSpec(kind, n if kind == "identity" else 1, n, 1, seed)
+
+
+def test_armijo_oracle_kats(oracle):  # test_adaptive.cpp:25-63
+    f = lambda x: 0.5 * float(x @ x)  # noqa: E731
+    assert oracle.armijo_step(f, np.ones(1), np.ones(1), 1.0, 0.5, 1e-4) == pytest.approx(1.0)
+    g = lambda x: 50.0 * float(x @ x)  # noqa: E731
+    j = next(j for j in range(51) if g(np.full(1, 1.0 - 0.5 ** j)) <= g(np.ones(1)) - 1e-4 * 0.5 ** j * 100.0)
+    assert oracle.armijo_step(g, np.ones(1), np.ones(1), 100.0, 0.5, 1e-4) == pytest.approx(0.5 ** j)
+    with pytest.raises(ValueError):
+        oracle.armijo_step(f, np.ones(1), np.ones(1), -1.0, 0.5, 1e-4)
+    # test_adaptive.cpp:57-62 expects SolverError for a constant objective, but
+    # in double arithmetic fx - gamma2 * step * 1 rounds to fx once
+    # 1e-4 * 2^-j drops below half an ulp of 1 (j = 41), so the code at
+    # adaptive.cpp:44-48 accepts that step; the oracle follows the code
+    j = next(j for j in range(51) if 1.0 <= 1.0 - 1e-4 * 0.5 ** j * 1.0)
+    assert j == 41
+    assert oracle.armijo_step(lambda x: 1.0, np.ones(1), np.ones(1), 1.0, 0.5, 1e-4) == 0.5 ** j
+    with pytest.raises(oracle.SolverError):  # a rising objective never qualifies
+        oracle.armijo_step(lambda x: 1.0 + float(np.abs(x - 1).sum()), np.ones(1), np.ones(1), 1.0, 0.5, 1e-4)
+
+
+def test_adaptive_oracle_kats(oracle):  # test_adaptive.cpp:65-171
+    a, b = _ab(oracle, 1, 20, 6)
+    xs = oracle.ridge_solve_oracle(a, b, 0.7)
+    r = oracle.adaptive_sketch_dim(a, b, 0.7, oracle.AdaptiveConfig(epsilon=1e-6, m_initial=4),
+                                   _tspec(oracle, "gaussian", 20, 3), xs)
+    assert (r.iterations, r.m, r.converged) == (0, 4, True)
+    a, b = _ab(oracle, 2, 40, 10)
+    cfg = oracle.AdaptiveConfig(epsilon=1e-10, m_initial=8)
+    r = oracle.adaptive_sketch_dim(a, b, 1.0, cfg, _tspec(oracle, "identity", 40, 5))
+    assert r.doublings == 0 and r.converged and r.m == 8 and r.iterations <= cfg.iteration_cap
+    prev = math.inf
+    for st in r.trace:
+        if st.doubled:
+            continue
+        assert st.f_after <= st.f_before - cfg.gamma2 * st.step * st.progress + 1e-15
+        assert st.f_before <= prev + 1e-12
+        prev = st.f_after
+    raw, b = _ab(oracle, 7, 64, 20)
+    q, _ = np.linalg.qr(raw)
+    r = oracle.adaptive_sketch_dim(5.0 * q, b, 0.01, oracle.AdaptiveConfig(epsilon=1e-8, m_initial=1),
+                                   _tspec(oracle, "gaussian", 64, 11))
+    assert r.doublings >= 1 and r.m <= 20
+    assert all(s1.m <= s2.m for s1, s2 in zip(r.trace, r.trace[1:]))
+    a, b = _ab(oracle, 21, 30, 8)
+    cfg = oracle.AdaptiveConfig(epsilon=1e-9, m_initial=2)
+    r1 = oracle.adaptive_sketch_dim(a, b, 0.5, cfg, _tspec(oracle, "countsketch", 30, 77))
+    r2 = oracle.adaptive_sketch_dim(a, b, 0.5, cfg, _tspec(oracle, "countsketch", 30, 77))
+    assert (r1.m, r1.iterations, r1.doublings) == (r2.m, r2.iterations, r2.doublings)
+    assert np.array_equal(r1.x, r2.x)
+    with pytest.raises(ValueError):
+        oracle.AdaptiveConfig(gamma1=1.5).validate(10)
+    with pytest.raises(ValueError):
+        oracle.AdaptiveConfig(m_cap=20).validate(10)
