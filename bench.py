@@ -286,6 +286,7 @@ def run_ours(args, w):
     ctx.set_option("profile", 1)
     prof = [step() for _ in range(max(1, min(args.steps, 3)))]
     ctx.set_option("profile", 0)
+    l_sec, l_flops, l_bytes = rp.last_gemm_profile(ctx)  # per launch, last profiled step
     g_s = sum(p.gemm_seconds for p in prof)
     g_f = sum(p.gemm_flops for p in prof)
     g_calls = sum(p.gemm_calls for p in prof)
@@ -306,11 +307,27 @@ def run_ours(args, w):
                         "(split-K partials included)" % rec["kernel"][:60])
     except Exception:
         pass
+    # Per-launch binding roof: the recursion's early generations are skinny
+    # (N = g+1 columns) and HBM-bound, the late ones DMMA-bound, so each
+    # launch is held to max(flops / tensor peak, bytes / HBM peak).
+    hbm_peak = 6449.1
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = float(json.load(f).get("hbm_gbs", hbm_peak))
+    except Exception:
+        pass
+    bound_t = sum(max(fl / (peak * 1e12), by / (hbm_peak * 1e9)) for fl, by in zip(l_flops, l_bytes)) if peak else 0.0
+    n_hbm = sum(1 for fl, by in zip(l_flops, l_bytes) if peak and by / (hbm_peak * 1e9) > fl / (peak * 1e12))
+    binding = {"frac": bound_t / float(sum(l_sec)) if len(l_sec) else None, "launches": int(len(l_sec)),
+               "hbm_bound_launches": int(n_hbm), "hbm_peak_gbs": hbm_peak,
+               "note": "sum over the GEMM launches of one step of max(flops/tensor peak, operand bytes/HBM peak) "
+                       "divided by their summed device time"}
     roofline = {"bound": "tensor", "kernel": "dgemm_tma_kernel / dgemm_kernel (FP64 DMMA m8n8k4, TMA-fed; all GEMMs of the path)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                 "traffic": traffic, "traffic_note": traffic_note, "share_of_step": g_s / tot_s if tot_s else None,
                 "gemm_launches_per_step": g_calls / len(prof),
                 "gemm_flops_per_step": g_f / len(prof),
+                "binding_roof": binding,
                 "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul fp64) measured in this run; "
                                "MEASURED_PEAKS.json has no FP64 figure; DMMA issue peak measured 37.1 TFLOP/s "
                                "(profiles/fp64_peaks_r01.txt)"}

@@ -140,6 +140,13 @@ RP_API rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value);
 RP_API int64_t rp_launch_count(void);
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) -------------------- */
+/* Per-GEMM records of the last path call made with option "profile" = 1:
+ * device seconds (CUDA events on the call's stream), algorithmic flops and
+ * algorithmic operand bytes, in launch order.  *count = number of records;
+ * the first `cap` are copied (any output pointer may be NULL). */
+RP_API rp_status rp_last_gemm_profile(rp_ctx* ctx, double* seconds, double* flops, double* bytes, int64_t cap,
+                                      int64_t* count);
+
 RP_API rp_status rp_comm_unique_id(void* id128);
 RP_API rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128);
 

@@ -804,6 +804,20 @@ void GemmProfiler::resolve(double* seconds, double* flops, int64_t* calls) {
   *calls = static_cast<int64_t>(recs.size());
 }
 
+void GemmProfiler::launches(std::vector<double>& seconds, std::vector<double>& flops,
+                            std::vector<double>& bytes) const {
+  seconds.clear();
+  flops.clear();
+  bytes.clear();
+  for (const auto& r : recs) {
+    float ms = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+    seconds.push_back(ms * 1e-3);
+    flops.push_back(r.flops);
+    bytes.push_back(r.bytes);
+  }
+}
+
 void dgemm(const GemmArgs& g, cudaStream_t stream) {
   if (!g_prof || g.m == 0 || g.n == 0) {
     dgemm_impl(g, stream);
@@ -816,6 +830,15 @@ void dgemm(const GemmArgs& g, cudaStream_t stream) {
   const double mn = g.lower_only ? 0.5 * static_cast<double>(g.m) * static_cast<double>(g.n + 1)
                                  : static_cast<double>(g.m) * static_cast<double>(g.n);
   r.flops = 2.0 * mn * static_cast<double>(g.k) * batch;
+  {
+    const double m = static_cast<double>(g.m), n = static_cast<double>(g.n), k = static_cast<double>(g.k);
+    const double a_copies = g.stride_a == 0 && g.stride_a2 == 0 ? 1.0 : batch;
+    const double b_copies = g.stride_b == 0 && g.stride_b2 == 0 ? 1.0 : batch;
+    const double a_bytes = 8.0 * m * k * a_copies;
+    const double b_bytes = g.b == g.a && g.lower_only ? 0.0 : 8.0 * k * n * b_copies;  // SYRK reads A once
+    const double c_bytes = 8.0 * mn * batch * (g.beta != 0.0 ? 2.0 : 1.0);
+    r.bytes = a_bytes + b_bytes + c_bytes;
+  }
   RP_CUDA(cudaEventRecord(r.start, stream));
   dgemm_impl(g, stream);
   RP_CUDA(cudaEventRecord(r.stop, stream));

@@ -109,11 +109,14 @@ struct GemmProfiler {
   struct Rec {
     cudaEvent_t start, stop;
     double flops;
+    double bytes;  // algorithmic operand bytes: A and B read once, C written (and read when beta != 0)
   };
   std::vector<Rec> recs;
   ~GemmProfiler();
   // Synchronizes on the last event and returns (seconds, flops, calls).
   void resolve(double* seconds, double* flops, int64_t* calls);
+  // Per-launch (seconds, flops, bytes), in launch order (after resolve).
+  void launches(std::vector<double>& seconds, std::vector<double>& flops, std::vector<double>& bytes) const;
 };
 void set_gemm_profiler(GemmProfiler* p);
 

@@ -293,6 +293,7 @@ struct rp_ctx {
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
+  std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
   int64_t csr_one_panel_bytes = 48 << 20;  // option "csr_one_panel_bytes": M W up to this size runs as one panel
   int64_t csr_chunk = 128;           // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 128)
@@ -1033,7 +1034,10 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     tm->linear_seconds = ev.secs(1, 5);
     tm->gram_seconds = ev.secs(5, 6);
     tm->precond_seconds = ev.secs(6, 2);
-    if (prof) prof->resolve(&tm->gemm_seconds, &tm->gemm_flops, &tm->gemm_calls);
+    if (prof) {
+      prof->resolve(&tm->gemm_seconds, &tm->gemm_flops, &tm->gemm_calls);
+      prof->launches(ctx->prof_seconds, ctx->prof_flops, ctx->prof_bytes);
+    }
   }
   (void)host_t0;
 }
@@ -1296,6 +1300,20 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->csr_chunk = value;
     } else {
       throw InvalidArgument("unknown option: " + k);
+    }
+  });
+}
+
+rp_status rp_last_gemm_profile(rp_ctx* ctx, double* seconds, double* flops, double* bytes, int64_t cap,
+                               int64_t* count) {
+  if (!ctx || !count) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const int64_t n = static_cast<int64_t>(ctx->prof_seconds.size());
+    *count = n;
+    for (int64_t i = 0; i < std::min(n, cap); ++i) {
+      if (seconds) seconds[i] = ctx->prof_seconds[i];
+      if (flops) flops[i] = ctx->prof_flops[i];
+      if (bytes) bytes[i] = ctx->prof_bytes[i];
     }
   });
 }

@@ -165,6 +165,7 @@ SIGNATURES = {
     "rp_direct_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
     "rp_adaptive_sketch_dim": ([_P, _P, _D, ctypes.POINTER(_AdaptiveConfig), ctypes.POINTER(_SketchSpec), _P, _P, _INT,
                                 ctypes.POINTER(_AdaptiveResult), _P, _I64], _INT),
+    "rp_last_gemm_profile": ([_P, _P, _P, _P, _I64, _P], _INT),
     "rp_derive_rho": ([_P, ctypes.POINTER(_SketchSpec), _INT, _D, _D, ctypes.POINTER(_Rho),
                        ctypes.POINTER(_SpectrumInfo)], _INT),
     "rp_effective_dimension": ([_P, _I64, _D, _P], _INT),
@@ -1031,6 +1032,17 @@ def path_raw(ctx: Context, b_ptr: int, K: int, config: PathConfig, spec: SketchS
 def gram_apply_raw(ctx: Context, x_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
     """rp_gram_apply on raw pointers: out = A^T (A x) for the context's operator."""
     ctx.check(lib().rp_gram_apply(ctx.handle, _P(x_ptr), ncols, _P(out_ptr), where))
+
+
+def last_gemm_profile(ctx: Context):
+    """Per-GEMM (seconds, flops, bytes) arrays of the last profiled path call."""
+    cnt = _I64(0)
+    ctx.check(lib().rp_last_gemm_profile(ctx.handle, None, None, None, 0, ctypes.cast(ctypes.byref(cnt), _P)))
+    n = cnt.value
+    sec, fl, by = np.zeros(max(n, 1)), np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    ctx.check(lib().rp_last_gemm_profile(ctx.handle, _ptr(sec), _ptr(fl), _ptr(by), n,
+                                         ctypes.cast(ctypes.byref(cnt), _P)))
+    return sec[:n], fl[:n], by[:n]
 
 
 def last_device_seconds(ctx: Context) -> float:
