@@ -374,7 +374,7 @@ def run_ours(args, w):
         x_host = torch.empty((T * K * d,), dtype=torch.float64).pin_memory()
 
         def e2e_step():
-            rp.set_dense_rows_host(ctx, n, r0, nl, d, a_host.data_ptr() + 8 * r0, n)
+            rp.set_dense_rows_host(ctx, n, r0, nl, d, a_host.data_ptr() + 8 * r0, n, stream=True)
             rp.path_raw(ctx, b_host.data_ptr(), K, cfg, spec, rho, x_host.data_ptr(), rp.RP_HOST)
 
         e2e_step()

@@ -54,7 +54,16 @@ typedef enum {
   RP_ENOMEM = 7
 } rp_status;
 
-enum { RP_HOST = 0, RP_DEVICE = 1 };
+enum { RP_HOST = 0, RP_DEVICE = 1, RP_HOST_STREAM = 2 };
+/* RP_HOST_STREAM (rp_set_dense / rp_set_dense_rows / rp_set_dense_cols only):
+ * the operator is uploaded asynchronously, in column chunks on an internal
+ * copy stream, and the call returns at once.  The next call that reads the
+ * operator waits for it -- rp_ihs_bin_path on a dense primal operator with an
+ * SRHT / CountSketch / SJLT / identity sketch instead consumes the chunks as
+ * they land (sketch columns, A^T b rows and Gram-matrix block rows), so the
+ * PCIe transfer overlaps that work.  The host buffer must stay valid and
+ * unmodified until that next call returns; pinned memory is needed for the
+ * overlap (pageable memory degrades to a synchronous copy). */
 
 /* SketchKind, sketch.hpp:10 (same order). */
 typedef enum {

@@ -209,6 +209,59 @@ void nccl_check(ncclResult_t r, const char* what) {
 // Context
 // ---------------------------------------------------------------------------
 
+// Chunked asynchronous upload of a host operator (RP_HOST_STREAM).  Chunks
+// are enqueued on the context's copy stream a few at a time (`enqueue`), so
+// the small host<->device copies the consumer issues meanwhile are never
+// queued behind the whole transfer; one event per chunk.
+struct Upload {
+  std::vector<cudaEvent_t> ev;   // per chunk (created up front, recorded when enqueued)
+  int64_t chunk = 0;             // columns per chunk
+  int64_t next = 0;              // first chunk not yet enqueued
+  const double* src = nullptr;   // host source (column-major, leading dim lda)
+  int64_t lda = 0, rows = 0, cols = 0;
+  double* dst = nullptr;         // device destination (leading dim rows)
+  cudaStream_t copy = nullptr;
+  Upload() = default;
+  Upload(const Upload&) = delete;
+  Upload& operator=(const Upload&) = delete;
+  Upload(Upload&& o) noexcept { *this = std::move(o); }
+  Upload& operator=(Upload&& o) noexcept {
+    if (this != &o) {
+      release();
+      ev = std::move(o.ev);
+      chunk = o.chunk;
+      next = o.next;
+      src = o.src;
+      lda = o.lda;
+      rows = o.rows;
+      cols = o.cols;
+      dst = o.dst;
+      copy = o.copy;
+      o.ev.clear();
+      o.next = 0;
+    }
+    return *this;
+  }
+  ~Upload() { release(); }
+  void release() {
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+  int64_t chunks() const { return static_cast<int64_t>(ev.size()); }
+  // Enqueue chunks [next, min(upto, chunks)).
+  void enqueue(int64_t upto) {
+    for (; next < std::min<int64_t>(upto, chunks()); ++next) {
+      const int64_t c0 = next * chunk, cc = std::min(chunk, cols - c0);
+      if (cc > 0 && rows > 0)
+        RP_CUDA(cudaMemcpy2DAsync(dst + c0 * rows, sizeof(double) * rows, src + c0 * lda, sizeof(double) * lda,
+                                  sizeof(double) * rows, static_cast<size_t>(cc), cudaMemcpyHostToDevice, copy));
+      RP_CUDA(cudaEventRecord(ev[static_cast<size_t>(next)], copy));
+    }
+  }
+};
+
+constexpr int64_t kUploadDepth = 2;  // chunks kept in flight ahead of the consumer
+
 struct OperatorStore {
   bool set = false;
   bool sparse = false;
@@ -226,6 +279,7 @@ struct OperatorStore {
   int64_t nnz = 0;
   // per-panel CSC of the primal / dual operator (sparse Gram passes), built lazily
   PanelCsc panels_primal, panels_dual;
+  Upload up;  // pending chunked upload (RP_HOST_STREAM)
 
   // Primal operator M = A (rows local).
   OpView primal() const {
@@ -285,6 +339,7 @@ struct rp_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -293,6 +348,7 @@ struct rp_ctx {
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
+  int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
   std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
   int64_t csr_one_panel_bytes = 48 << 20;  // option "csr_one_panel_bytes": M W up to this size runs as one panel
@@ -320,6 +376,23 @@ struct DeviceGuard {
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+// Order the context's stream after a pending chunked upload (every generic
+// reader of the operator goes through op_primal / op_dual).
+void wait_upload(rp_ctx* ctx) {
+  Upload& up = ctx->op.up;
+  if (up.ev.empty()) return;
+  up.enqueue(up.chunks());
+  RP_CUDA(cudaStreamWaitEvent(ctx->stream, up.ev.back(), 0));
+}
+OpView op_primal(rp_ctx* ctx) {
+  wait_upload(ctx);
+  return ctx->op.primal();
+}
+OpView op_dual(rp_ctx* ctx) {
+  wait_upload(ctx);
+  return ctx->op.dual();
+}
 
 void allreduce(rp_ctx* ctx, double* buf, int64_t count) {
   if (ctx->world <= 1 || count <= 0) return;
@@ -463,6 +536,32 @@ struct GramOp {
       build_panel_csc(op.csr_off, op.csr_col, op.csr_val, op.n_loc, op.d, op.nnz, ctx->csr_panel_rows, pc,
                       ctx->stream);
     return pc;
+  }
+
+  // Streamed build (RP_HOST_STREAM uploads): block rows of the lower triangle
+  // as the operator's column chunks land, then mirror and all-reduce.
+  void begin_matrix() {
+    require(!op.sparse && !op.trans, "gram matrix rows need a dense primal operator");
+    G.alloc(static_cast<size_t>(op.d * op.d), ctx->stream);
+  }
+  void matrix_rows(int64_t c0, int64_t c1) {  // G[c0:c1, 0:c1] = M[:, c0:c1]^T M[:, 0:c1]
+    GemmArgs g;
+    g.opa = Op::T;
+    g.m = c1 - c0;
+    g.n = c1;
+    g.k = op.n_loc;
+    g.a = op.a + c0 * op.ld;
+    g.lda = op.ld;
+    g.b = op.a;
+    g.ldb = op.ld;
+    g.c = G.get() + c0;
+    g.ldc = op.d;
+    dgemm(g, ctx->stream);
+  }
+  void end_matrix() {
+    mirror_lower(G.get(), op.d, op.d, ctx->stream);
+    allreduce(ctx, G.get(), op.d * op.d);
+    matrix = true;
   }
 
   void build_matrix() {
@@ -753,14 +852,22 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
 struct InBuf {
   const double* ptr = nullptr;
   DBuf<double> owned;
-  InBuf(const double* p, size_t count, int where, cudaStream_t s) {
+  InBuf(const double* p, size_t count, int where, cudaStream_t s, bool zero_copy = false) {
     if (where == RP_DEVICE || count == 0) {
       ptr = p;
-    } else {
-      owned.alloc(count, s);
-      RP_CUDA(cudaMemcpyAsync(owned.get(), p, count * sizeof(double), cudaMemcpyHostToDevice, s));
-      ptr = owned.get();
+      return;
     }
+    owned.alloc(count, s);
+    ptr = owned.get();
+    if (zero_copy) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer) {
+        copy_mapped(static_cast<const double*>(at.devicePointer), static_cast<int64_t>(count), owned.get(), s);
+        return;
+      }
+      cudaGetLastError();
+    }
+    RP_CUDA(cudaMemcpyAsync(owned.get(), p, count * sizeof(double), cudaMemcpyHostToDevice, s));
   }
 };
 
@@ -853,7 +960,12 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   cfg.validate();
   rho_validate(rho);
   require(K >= 1, "path: empty right-hand side");
-  const OpView op = dual ? ctx->op.dual() : ctx->op.primal();
+  // A dense primal operator still landing in chunks (RP_HOST_STREAM) is
+  // consumed chunk by chunk below; every other case waits for the upload.
+  const bool stream_in = !dual && ctx->op.set && !ctx->op.sparse && ctx->op.shard != 2 &&
+                         ctx->op.up.chunks() > 1 && ctx->op.up.next < ctx->op.up.chunks() &&
+                         spec.kind != kGaussian;
+  const OpView op = stream_in ? ctx->op.primal() : (dual ? op_dual(ctx) : op_primal(ctx));
   // ihs_bin_path: spec.n == A.rows; dual_path: spec.n == A.cols (path_solver.cpp:294, 333-334)
   require(spec.n == op.n_global, dual ? "dual_path: spec.n must equal A.cols (the dual operator is A^T)"
                                       : "ihs_bin_path: spec.n must equal A.rows");
@@ -862,45 +974,81 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   // Host -> device copy of b (timed as copy).
   double copy_secs = 0.0;
   auto tc0 = std::chrono::steady_clock::now();
-  InBuf b(b_in, static_cast<size_t>(b_rows * K), where, s);
+  // (while an upload streams, a pinned host b is read by a kernel through its
+  // mapped address instead of queueing a copy behind the transfer)
+  InBuf b(b_in, static_cast<size_t>(b_rows * K), where, s, stream_in);
   if (where == RP_HOST) RP_CUDA(cudaStreamSynchronize(s));
   copy_secs += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count();
 
   Events ev(8);
   RP_CUDA(cudaEventRecord(ev.ev[0], s));
-  // 1) Sketch (once), summed over ranks.
-  DBuf<double> sa(static_cast<size_t>(spec.m * dim), s);
-  sketch_apply(spec, op, sa.get(), s);
-  allreduce(ctx, sa.get(), spec.m * dim);
-  RP_CUDA(cudaEventRecord(ev.ev[1], s));
   // 2) Plans (host, bit-identical to the reference).
   const auto plans = plan_intervals(cfg, rho, sigma_d);
   const int64_t L = static_cast<int64_t>(plans.size());
-  // 3) Linear term: c = M^T b (primal) or c = b (dual).
-  DBuf<double> cbuf(static_cast<size_t>(dim * K), s);
-  if (!dual) {
-    op_apply_t(ctx, op, b.ptr, K, cbuf.get(), true);
-  } else {
-    copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
-  }
-  RP_CUDA(cudaEventRecord(ev.ev[5], s));
   // Gram operator: pass over M, or G = M^T M when cheaper.
   GramOp gram;
   gram.ctx = ctx;
   gram.op = op;
   int kmax = 2;
   for (const auto& p : plans) kmax = std::max(kmax, p.params.k);
+  bool use_matrix = false;
   {
     const double cols_total = static_cast<double>(L * K) * (static_cast<double>(kmax) * (kmax - 1) / 2.0);
     const double nnz = op.sparse ? static_cast<double>(op.nnz) : static_cast<double>(op.n_loc) * op.d;
     const double pass = 4.0 * nnz * cols_total;
     const double matrix = static_cast<double>(op.n_loc) * op.d * op.d + 2.0 * op.d * op.d * cols_total;
-    bool use_matrix = !op.sparse && matrix < pass && static_cast<double>(op.d) * op.d * 8.0 <= 16.0 * (1 << 30);
+    use_matrix = !op.sparse && matrix < pass && static_cast<double>(op.d) * op.d * 8.0 <= 16.0 * (1 << 30);
     if (ctx->gram_mode == 0) use_matrix = false;
     if (ctx->gram_mode == 1) {
       require(!op.sparse, "gram_mode=1 needs a dense operator");
       use_matrix = true;
     }
+  }
+  DBuf<double> sa(static_cast<size_t>(spec.m * dim), s);
+  DBuf<double> cbuf(static_cast<size_t>(dim * K), s);
+  if (stream_in) {
+    // Chunked consumption of the upload: as column block [c0, c1) of A lands,
+    // sketch its columns, form rows c0..c1 of c = A^T b and block row
+    // G[c0:c1, 0:c1] of the Gram matrix (lower part; mirrored at the end).
+    const Upload& up = ctx->op.up;
+    DBuf<double> ctmp(static_cast<size_t>(std::min<int64_t>(up.chunk, dim) * K), s);
+    if (use_matrix) gram.begin_matrix();
+    Upload& upm = ctx->op.up;
+    const bool planned = spec.kind == kCountSketch || spec.kind == kSjlt || spec.kind == kSrht;
+    SketchPlan plan;  // draws / SRHT tables once, applied per column block
+    if (planned) sketch_plan(spec, op, plan, s);
+    for (size_t j = 0; j < up.ev.size(); ++j) {
+      const int64_t c0 = static_cast<int64_t>(j) * up.chunk, cc = std::min(up.chunk, dim - c0);
+      upm.enqueue(static_cast<int64_t>(j) + kUploadDepth);
+      RP_CUDA(cudaStreamWaitEvent(s, up.ev[j], 0));
+      OpView sub = op;
+      sub.a = op.a + c0 * op.ld;
+      sub.d = cc;
+      if (planned)
+        sketch_apply_planned(plan, sub, sa.get() + c0 * spec.m, s);
+      else
+        sketch_apply(spec, sub, sa.get() + c0 * spec.m, s);
+      op_apply_t(ctx, sub, b.ptr, K, ctmp.get(), false);
+      copy_cols(ctmp.get(), cc, K, cc, cbuf.get() + c0, dim, s);
+      if (use_matrix) gram.matrix_rows(c0, c0 + cc);
+    }
+    allreduce(ctx, sa.get(), spec.m * dim);
+    RP_CUDA(cudaEventRecord(ev.ev[1], s));
+    allreduce(ctx, cbuf.get(), dim * K);
+    RP_CUDA(cudaEventRecord(ev.ev[5], s));
+    if (use_matrix) gram.end_matrix();
+  } else {
+    // 1) Sketch (once), summed over ranks.
+    sketch_apply(spec, op, sa.get(), s);
+    allreduce(ctx, sa.get(), spec.m * dim);
+    RP_CUDA(cudaEventRecord(ev.ev[1], s));
+    // 3) Linear term: c = M^T b (primal) or c = b (dual).
+    if (!dual) {
+      op_apply_t(ctx, op, b.ptr, K, cbuf.get(), true);
+    } else {
+      copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
+    }
+    RP_CUDA(cudaEventRecord(ev.ev[5], s));
     if (use_matrix) gram.build_matrix();
   }
   RP_CUDA(cudaEventRecord(ev.ev[6], s));
@@ -1159,6 +1307,7 @@ void set_csr_impl(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, 
       }
   }
   OperatorStore& o = ctx->op;
+  wait_upload(ctx);
   o = OperatorStore();
   o.sparse = true;
   o.n = shard == 2 ? n_global : n_global;
@@ -1191,6 +1340,7 @@ void set_dense_impl(rp_ctx* ctx, int64_t n, int64_t d, int shard, int64_t off0, 
   require(lda >= std::max<int64_t>(rows, 1), "dense: leading dimension too small");
   cudaStream_t s = ctx->stream;
   OperatorStore& o = ctx->op;
+  wait_upload(ctx);  // the old buffer is freed on this stream: after its upload
   o = OperatorStore();
   o.sparse = false;
   o.n = n;
@@ -1201,6 +1351,30 @@ void set_dense_impl(rp_ctx* ctx, int64_t n, int64_t d, int shard, int64_t off0, 
   if (where == RP_DEVICE) {
     o.a = a;
     o.lda = lda;
+  } else if (where == RP_HOST_STREAM) {
+    // Column chunks of ~upload_chunk_bytes (32 MiB) on the copy stream, one event each.
+    o.owned.alloc(static_cast<size_t>(std::max<int64_t>(rows * cols, 1)), s);
+    if (!ctx->copy) RP_CUDA(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    cudaEvent_t alloc_done;
+    RP_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
+    RP_CUDA(cudaEventRecord(alloc_done, s));
+    RP_CUDA(cudaStreamWaitEvent(ctx->copy, alloc_done, 0));
+    RP_CUDA(cudaEventDestroy(alloc_done));
+    const int64_t chunk = std::max<int64_t>(1, ctx->upload_chunk_bytes / std::max<int64_t>(1, rows * 8));
+    Upload& up = o.up;
+    up.chunk = chunk;
+    up.src = a;
+    up.lda = lda;
+    up.rows = rows;
+    up.cols = cols;
+    up.dst = o.owned.get();
+    up.copy = ctx->copy;
+    up.next = 0;
+    up.ev.resize(static_cast<size_t>(std::max<int64_t>(1, ceil_div(cols, chunk))));
+    for (auto& e : up.ev) RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    up.enqueue(1);  // the consumer keeps kUploadDepth chunks in flight from here on
+    o.a = o.owned.get();
+    o.lda = std::max<int64_t>(rows, 1);
   } else {
     o.owned.alloc(static_cast<size_t>(std::max<int64_t>(rows * cols, 1)), s);
     RP_CUDA(cudaMemcpy2DAsync(o.owned.get(), sizeof(double) * rows, a, sizeof(double) * lda, sizeof(double) * rows,
@@ -1254,8 +1428,10 @@ void rp_destroy(rp_ctx* ctx) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
+    if (!ctx->op.up.ev.empty()) cudaStreamWaitEvent(ctx->stream, ctx->op.up.ev.back(), 0);
     cudaStreamSynchronize(ctx->stream);
     ctx->op = OperatorStore();
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     cudaSetDevice(prev);
@@ -1292,6 +1468,9 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "csr_panel_rows") {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
+    } else if (k == "upload_chunk_bytes") {
+      require(value >= 1, "upload_chunk_bytes must be >= 1");
+      ctx->upload_chunk_bytes = value;
     } else if (k == "csr_one_panel_bytes") {
       require(value >= 0, "csr_one_panel_bytes must be >= 0");
       ctx->csr_one_panel_bytes = value;
@@ -1409,7 +1588,7 @@ struct DeviceTimer {
 rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(ncols >= 0, "apply: dimension mismatch");
     InBuf in(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
     OutBuf out(y, static_cast<size_t>(op.n_loc * ncols), where, ctx->stream);
@@ -1421,7 +1600,7 @@ rp_status rp_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* y, int w
 rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double* x, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(ncols >= 0, "apply_transpose: dimension mismatch");
     InBuf in(y, static_cast<size_t>(op.n_loc * ncols), where, ctx->stream);
     OutBuf out(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
@@ -1435,7 +1614,7 @@ rp_status rp_apply_transpose(rp_ctx* ctx, const double* y, int64_t ncols, double
 rp_status rp_gram_apply(rp_ctx* ctx, const double* x, int64_t ncols, double* outp, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(ncols >= 0, "gram_apply: dimension mismatch");
     InBuf in(x, static_cast<size_t>(op.d * ncols), where, ctx->stream);
     OutBuf out(outp, static_cast<size_t>(op.d * ncols), where, ctx->stream);
@@ -1460,7 +1639,7 @@ rp_status rp_losses(rp_ctx* ctx, const double* b, int64_t K, int64_t T, const do
                     double* lossp, int where) {
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(K >= 1 && T >= 0, "losses: dimension mismatch");
     cudaStream_t s = ctx->stream;
     InBuf xb(x, static_cast<size_t>(op.d * K * T), where, s);
@@ -1489,7 +1668,7 @@ rp_status rp_sketch_apply(rp_ctx* ctx, const rp_sketch_spec* specp, int transpos
   if (!ctx) return RP_EINVAL;
   return guarded(ctx, [&] {
     const SketchSpecC spec = to_spec(specp);
-    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    const OpView op = transpose_op ? op_dual(ctx) : op_primal(ctx);
     validate_spec(spec);
     require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
     OutBuf out(sa, static_cast<size_t>(spec.m * op.d), where, ctx->stream);
@@ -1618,7 +1797,7 @@ rp_status rp_ihs_basis(rp_ctx* ctx, const rp_precond* p, const double* b, int64_
     require(K >= 1, "ihs_basis_matrix: empty right-hand side");
     require(k >= 1, "ihs_basis: k must be >= 1");
     require(tau > 0.0, "ihs_basis: tau must be positive");
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     InBuf bb(b, static_cast<size_t>(op.n_loc * K), where, ctx->stream);
     DBuf<double> c(static_cast<size_t>(op.d * K), ctx->stream);
     op_apply_t(ctx, op, bb.ptr, K, c.get(), true);
@@ -1633,7 +1812,7 @@ rp_status rp_ihs_basis_core(rp_ctx* ctx, const rp_precond* p, const double* c, i
     require(K >= 1, "ihs_basis_matrix: empty right-hand side");
     require(k >= 1, "ihs_basis: k must be >= 1");
     require(tau > 0.0, "ihs_basis: tau must be positive");
-    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    const OpView op = transpose_op ? op_dual(ctx) : op_primal(ctx);
     require(op.d == p->d, "ihs_basis: operator/right-hand-side mismatch");
     InBuf cc(c, static_cast<size_t>(op.d * K), where, ctx->stream);
     basis_core(ctx, p, op, cc.ptr, K, tau, k, terms_out, where);
@@ -1759,7 +1938,7 @@ double host_seconds_since(std::chrono::steady_clock::time_point t0) {
 void run_warm_cg(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out, BaselineRun& run) {
   cudaStream_t s = ctx->stream;
   const auto t_total = std::chrono::steady_clock::now();
-  const OpView op = ctx->op.primal();
+  const OpView op = op_primal(ctx);
   const int64_t d = op.d;
   GramOp gram;
   gram.ctx = ctx;
@@ -1815,7 +1994,7 @@ void run_warm_ihs(rp_ctx* ctx, const double* b, const PathCfg& cfg, const Sketch
                   double* x_out, BaselineRun& run) {
   cudaStream_t s = ctx->stream;
   const auto t_total = std::chrono::steady_clock::now();
-  const OpView op = ctx->op.primal();
+  const OpView op = op_primal(ctx);
   const int64_t d = op.d;
   DBuf<double> sa(static_cast<size_t>(spec.m * d), s);
   sketch_apply(spec, op, sa.get(), s);
@@ -1905,7 +2084,7 @@ void run_warm_ihs(rp_ctx* ctx, const double* b, const PathCfg& cfg, const Sketch
 void run_direct(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out, BaselineRun& run) {
   cudaStream_t s = ctx->stream;
   const auto t_total = std::chrono::steady_clock::now();
-  const OpView op = ctx->op.primal();
+  const OpView op = op_primal(ctx);
   const int64_t d = op.d;
   require(static_cast<double>(d) * d * 8.0 <= 32.0 * (1ull << 30), "direct_path: A^T A exceeds 32 GiB");
   DBuf<double> G;
@@ -1978,7 +2157,7 @@ void run_adaptive(rp_ctx* ctx, const double* b, double lambda_min, const rp_adap
                   const SketchSpecC& tmpl, const double* x0, double* x_out, rp_adaptive_result& res,
                   std::vector<rp_adaptive_step>& trace) {
   cudaStream_t s = ctx->stream;
-  const OpView op = ctx->op.primal();
+  const OpView op = op_primal(ctx);
   const int64_t d = op.d, nl = op.n_loc;
   // AdaptiveConfig::validate / initial_m / cap_m (adaptive.cpp:19-37)
   const int64_t m0 = cfg.m_initial > 0 ? cfg.m_initial : std::max<int64_t>(16, d / 64);
@@ -2114,7 +2293,7 @@ rp_status rp_warm_cg_path(rp_ctx* ctx, const double* b, const rp_path_config* cf
   return guarded(ctx, [&] {
     const PathCfg cfg = to_cfg(cfgp);
     cfg.validate();
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
     OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
     BaselineRun run;
@@ -2134,7 +2313,7 @@ rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_config* c
     const Rho rho = to_rho(rhop);
     rho_validate(rho);
     const SketchSpecC spec = to_spec(specp);
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(spec.n == op.n_global, "warm_ihs_path: spec.n must equal A.rows");
     validate_spec(spec);
     InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
@@ -2152,7 +2331,7 @@ rp_status rp_adaptive_sketch_dim(rp_ctx* ctx, const double* b, double lambda_min
   if (!ctx || !cfg || !result) return RP_EINVAL;
   return guarded(ctx, [&] {
     const SketchSpecC tmpl = to_spec(spec_template);
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     require(trace_cap >= 0, "adaptive: negative trace capacity");
     InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
     InBuf xb(x0, x0 ? static_cast<size_t>(op.d) : 0, where, ctx->stream);
@@ -2171,7 +2350,7 @@ rp_status rp_direct_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg
   return guarded(ctx, [&] {
     const PathCfg cfg = to_cfg(cfgp);
     cfg.validate();
-    const OpView op = ctx->op.primal();
+    const OpView op = op_primal(ctx);
     InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
     OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
     BaselineRun run;
@@ -2203,7 +2382,7 @@ rp_status rp_derive_rho(rp_ctx* ctx, const rp_sketch_spec* specp, int transpose_
       if (info) *info = inf;
       return;
     }
-    const OpView op = transpose_op ? ctx->op.dual() : ctx->op.primal();
+    const OpView op = transpose_op ? op_dual(ctx) : op_primal(ctx);
     validate_spec(spec);
     require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
     cudaStream_t s = ctx->stream;

@@ -546,126 +546,151 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       return;
     }
     case kCountSketch:
-    case kSjlt: {
-      const int blocks = spec.kind == kSjlt ? spec.s : 1;
-      const double entry = spec.kind == kSjlt ? 1.0 / std::sqrt(static_cast<double>(spec.s)) : 1.0;
-      const int64_t rpb = m / blocks;
-      DBuf<int32_t> h(static_cast<size_t>(spec.n * blocks), stream);
-      DBuf<double> sg(static_cast<size_t>(spec.n * blocks), stream);
-      draw_count(spec.seed, spec.n, rpb, blocks, entry, h.get(), sg.get(), stream);
-      zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
-      RP_LAUNCH_CHECK();
-      const int64_t threads = d * blocks;
-      if (!op.sparse) {
-        count_dense<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
-            op.a, op.ld, op.trans, op.n_loc, op.row0, spec.n, d, blocks, rpb, h.get(), sg.get(), d_sa, m);
-      } else {
-        count_csc<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
-            op.csc_off, op.csc_row, op.csc_val, op.row0, spec.n, d, blocks, rpb, h.get(), sg.get(), d_sa, m);
-      }
-      RP_LAUNCH_CHECK();
-      return;
-    }
+    case kSjlt:
     case kSrht: {
-      int64_t npad = 1;
-      int P = 0;
-      while (npad < spec.n) {
-        npad <<= 1;
-        ++P;
-      }
-      DBuf<double> signs(static_cast<size_t>(spec.n), stream);
-      DBuf<int64_t> rows(static_cast<size_t>(m), stream);
-      draw_srht(spec.seed, spec.n, m, signs.get(), rows.get(), stream);
-      // Pass plan: descending bit ranges of at most 8 bits, balanced (a
-      // single 0-bit pass when n_pad = 1).
-      std::vector<int> widths;
-      {
-        const int passes = std::max(1, (P + 7) / 8);
-        int rem = P;
-        for (int i = 0; i < passes; ++i) {
-          const int w = (rem + (passes - i) - 1) / (passes - i);
-          widths.push_back(w);
-          rem -= w;
-        }
-      }
-      FwhtArgs probe{};
-      probe.npad = npad;
-      const bool two_pass = !op.sparse && fwht2_ok(probe);
-      // (two-pass path: targets bucketed per CH-row chunk)
-      const int last_bits = two_pass ? [&] {
-        int lb = 0;
-        while ((int64_t{1} << lb) < fwht2_chunk(npad)) ++lb;
-        return lb;
-      }() : widths.back();
-      // Targets sorted by position, bucketed per block of the last pass.
-      std::vector<int64_t> hrows(static_cast<size_t>(m));
-      RP_CUDA(cudaMemcpyAsync(hrows.data(), rows.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToHost, stream));
-      RP_CUDA(cudaStreamSynchronize(stream));
-      std::vector<std::pair<int64_t, int32_t>> tg(static_cast<size_t>(m));
-      for (int64_t r = 0; r < m; ++r) tg[r] = {hrows[r], static_cast<int32_t>(r)};
-      std::sort(tg.begin(), tg.end());
-      const int64_t nblk = npad >> last_bits;
-      std::vector<int64_t> tpos(static_cast<size_t>(m));
-      std::vector<int32_t> meta(static_cast<size_t>(m + nblk + 1));
-      for (int64_t r = 0; r < m; ++r) {
-        tpos[r] = tg[r].first;
-        meta[r] = tg[r].second;
-      }
-      {
-        int64_t k = 0;
-        for (int64_t b = 0; b <= nblk; ++b) {
-          while (k < m && (tpos[k] >> last_bits) < b) ++k;
-          meta[m + b] = static_cast<int32_t>(k);
-        }
-      }
-      DBuf<int64_t> d_tpos(static_cast<size_t>(m), stream);
-      DBuf<int32_t> d_meta(meta.size(), stream);
-      RP_CUDA(cudaMemcpyAsync(d_tpos.get(), tpos.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, stream));
-      RP_CUDA(cudaMemcpyAsync(d_meta.get(), meta.data(), sizeof(int32_t) * meta.size(), cudaMemcpyHostToDevice,
-                              stream));
-      DBuf<double> x;  // pass scratch (not needed when one chunk holds the whole transform)
-      if (!two_pass || npad > fwht2_chunk(npad)) x.alloc(static_cast<size_t>(npad * d), stream);
-      FwhtArgs f{};
-      f.x = x.get();
-      f.npad = npad;
-      f.d = d;
-      f.signs = signs.get();
-      f.a = op.a;
-      f.lda = op.ld;
-      f.n_loc = op.n_loc;
-      f.row0 = op.row0;
-      f.trans = op.trans;
-      f.tpos = d_tpos.get();
-      f.tslot = d_meta.get();
-      f.boff = d_meta.get() + m;
-      f.scale = 1.0 / std::sqrt(static_cast<double>(m));
-      f.sa = d_sa;
-      f.m = m;
-      const bool first_from_op = !op.sparse;
-      if (two_pass) {
-        launch_fwht2(f, stream);
-        RP_CUDA(cudaStreamSynchronize(stream));  // host target tables must outlive the copies
-        return;
-      }
-      if (op.sparse) {
-        zero_fill<<<grid_for(npad * d), 256, 0, stream>>>(x.get(), npad, d, npad);
-        RP_LAUNCH_CHECK();
-        srht_scatter_csc<<<static_cast<unsigned>(d), 128, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, op.row0,
-                                                                       d, signs.get(), x.get(), npad);
-        RP_LAUNCH_CHECK();
-      }
-      int hi = P;
-      for (size_t i = 0; i < widths.size(); ++i) {
-        const int bits = widths[i];
-        f.lo = hi - bits;
-        f.from_op = (i == 0) && first_from_op;
-        f.to_sa = (i + 1 == widths.size());
-        launch_fwht(f, bits, stream);
-        hi -= bits;
-      }
-      RP_CUDA(cudaStreamSynchronize(stream));  // host target tables must outlive the copies
+      SketchPlan plan;
+      sketch_plan(spec, op, plan, stream);
+      sketch_apply_planned(plan, op, d_sa, stream);
       return;
     }
+  }
+}
+
+void sketch_plan(const SketchSpecC& spec, const OpView& op, SketchPlan& plan, cudaStream_t stream) {
+  validate_spec(spec);
+  plan.spec = spec;
+  plan.sparse = op.sparse;
+  const int64_t m = spec.m;
+  if (spec.kind == kCountSketch || spec.kind == kSjlt) {
+    plan.blocks = spec.kind == kSjlt ? spec.s : 1;
+    const double entry = spec.kind == kSjlt ? 1.0 / std::sqrt(static_cast<double>(spec.s)) : 1.0;
+    plan.rpb = m / plan.blocks;
+    plan.h.alloc(static_cast<size_t>(spec.n * plan.blocks), stream);
+    plan.sg.alloc(static_cast<size_t>(spec.n * plan.blocks), stream);
+    draw_count(spec.seed, spec.n, plan.rpb, plan.blocks, entry, plan.h.get(), plan.sg.get(), stream);
+    return;
+  }
+  require(spec.kind == kSrht, "sketch plan: only CountSketch / SJLT / SRHT are planned");
+  int64_t npad = 1;
+  int P = 0;
+  while (npad < spec.n) {
+    npad <<= 1;
+    ++P;
+  }
+  plan.npad = npad;
+  plan.P = P;
+  plan.signs.alloc(static_cast<size_t>(spec.n), stream);
+  DBuf<int64_t> rows(static_cast<size_t>(m), stream);
+  draw_srht(spec.seed, spec.n, m, plan.signs.get(), rows.get(), stream);
+  // Pass plan: descending bit ranges of at most 8 bits, balanced (a
+  // single 0-bit pass when n_pad = 1).
+  {
+    const int passes = std::max(1, (P + 7) / 8);
+    int rem = P;
+    for (int i = 0; i < passes; ++i) {
+      const int w = (rem + (passes - i) - 1) / (passes - i);
+      plan.widths.push_back(w);
+      rem -= w;
+    }
+  }
+  FwhtArgs probe{};
+  probe.npad = npad;
+  plan.two_pass = !op.sparse && fwht2_ok(probe);
+  // (two-pass path: targets bucketed per CH-row chunk)
+  const int last_bits = plan.two_pass ? [&] {
+    int lb = 0;
+    while ((int64_t{1} << lb) < fwht2_chunk(npad)) ++lb;
+    return lb;
+  }() : plan.widths.back();
+  // Targets sorted by position, bucketed per block of the last pass.
+  std::vector<int64_t> hrows(static_cast<size_t>(m));
+  RP_CUDA(cudaMemcpyAsync(hrows.data(), rows.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToHost, stream));
+  RP_CUDA(cudaStreamSynchronize(stream));
+  std::vector<std::pair<int64_t, int32_t>> tg(static_cast<size_t>(m));
+  for (int64_t r = 0; r < m; ++r) tg[r] = {hrows[r], static_cast<int32_t>(r)};
+  std::sort(tg.begin(), tg.end());
+  const int64_t nblk = npad >> last_bits;
+  plan.tpos.assign(static_cast<size_t>(m), 0);
+  plan.meta.assign(static_cast<size_t>(m + nblk + 1), 0);
+  for (int64_t r = 0; r < m; ++r) {
+    plan.tpos[r] = tg[r].first;
+    plan.meta[r] = tg[r].second;
+  }
+  {
+    int64_t k = 0;
+    for (int64_t b = 0; b <= nblk; ++b) {
+      while (k < m && (plan.tpos[k] >> last_bits) < b) ++k;
+      plan.meta[m + b] = static_cast<int32_t>(k);
+    }
+  }
+  plan.d_tpos.alloc(static_cast<size_t>(m), stream);
+  plan.d_meta.alloc(plan.meta.size(), stream);
+  // (the plan keeps the host tables alive until it is destroyed)
+  RP_CUDA(cudaMemcpyAsync(plan.d_tpos.get(), plan.tpos.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, stream));
+  RP_CUDA(cudaMemcpyAsync(plan.d_meta.get(), plan.meta.data(), sizeof(int32_t) * plan.meta.size(),
+                          cudaMemcpyHostToDevice, stream));
+}
+
+void sketch_apply_planned(const SketchPlan& plan, const OpView& op, double* d_sa, cudaStream_t stream) {
+  const SketchSpecC& spec = plan.spec;
+  require(op.n_global == spec.n, "sketch_apply: spec.n must match A.rows");
+  require(op.sparse == plan.sparse, "sketch plan: operator kind changed");
+  const int64_t m = spec.m, d = op.d;
+  if (spec.kind == kCountSketch || spec.kind == kSjlt) {
+    zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
+    RP_LAUNCH_CHECK();
+    const int64_t threads = d * plan.blocks;
+    if (!op.sparse) {
+      count_dense<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
+          op.a, op.ld, op.trans, op.n_loc, op.row0, spec.n, d, plan.blocks, plan.rpb, plan.h.get(), plan.sg.get(),
+          d_sa, m);
+    } else {
+      count_csc<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, stream>>>(
+          op.csc_off, op.csc_row, op.csc_val, op.row0, spec.n, d, plan.blocks, plan.rpb, plan.h.get(),
+          plan.sg.get(), d_sa, m);
+    }
+    RP_LAUNCH_CHECK();
+    return;
+  }
+  const int64_t npad = plan.npad;
+  DBuf<double> x;  // pass scratch (not needed when one chunk holds the whole transform)
+  if (!plan.two_pass || npad > fwht2_chunk(npad)) x.alloc(static_cast<size_t>(npad * d), stream);
+  FwhtArgs f{};
+  f.x = x.get();
+  f.npad = npad;
+  f.d = d;
+  f.signs = plan.signs.get();
+  f.a = op.a;
+  f.lda = op.ld;
+  f.n_loc = op.n_loc;
+  f.row0 = op.row0;
+  f.trans = op.trans;
+  f.tpos = plan.d_tpos.get();
+  f.tslot = plan.d_meta.get();
+  f.boff = plan.d_meta.get() + m;
+  f.scale = 1.0 / std::sqrt(static_cast<double>(m));
+  f.sa = d_sa;
+  f.m = m;
+  const bool first_from_op = !op.sparse;
+  if (plan.two_pass) {
+    launch_fwht2(f, stream);
+    return;
+  }
+  if (op.sparse) {
+    zero_fill<<<grid_for(npad * d), 256, 0, stream>>>(x.get(), npad, d, npad);
+    RP_LAUNCH_CHECK();
+    srht_scatter_csc<<<static_cast<unsigned>(d), 128, 0, stream>>>(op.csc_off, op.csc_row, op.csc_val, op.row0, d,
+                                                                   plan.signs.get(), x.get(), npad);
+    RP_LAUNCH_CHECK();
+  }
+  int hi = plan.P;
+  for (size_t i = 0; i < plan.widths.size(); ++i) {
+    const int bits = plan.widths[i];
+    f.lo = hi - bits;
+    f.from_op = (i == 0) && first_from_op;
+    f.to_sa = (i + 1 == plan.widths.size());
+    launch_fwht(f, bits, stream);
+    hi -= bits;
   }
 }
 

@@ -104,7 +104,40 @@ __global__ void residual_kernel(double* __restrict__ r, const double* __restrict
   RP_GRID_STRIDE(i, n) r[i] = __dsub_rn(r[i], b[i]);
 }
 
+__global__ void mirror_lower_kernel(double* __restrict__ g, int64_t n, int64_t ld) {
+  __shared__ double tile[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // source tile (rows bi, cols bj), bi >= bj
+  if (bi < bj) return;
+  const int64_t r0 = bi * 32, c0 = bj * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    if (r < n && c < n) tile[k][threadIdx.x] = g[r + c * ld];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = c0 + threadIdx.x, c = r0 + k;  // destination (r, c) = source (c, r)
+    if (r < n && c < n && r < c) g[r + c * ld] = tile[threadIdx.x][k];
+  }
+}
+
+__global__ void copy_mapped_kernel(const double* __restrict__ src, int64_t n, double* __restrict__ dst) {
+  RP_GRID_STRIDE(i, n) dst[i] = src[i];
+}
+
 }  // namespace
+
+void copy_mapped(const double* src, int64_t n, double* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  copy_mapped_kernel<<<blocks_for(n), 256, 0, s>>>(src, n, dst);
+  RP_LAUNCH_CHECK();
+}
+
+void mirror_lower(double* g, int64_t n, int64_t ld, cudaStream_t s) {
+  if (n <= 1) return;
+  const unsigned t = static_cast<unsigned>(ceil_div(n, 32));
+  mirror_lower_kernel<<<dim3(t, t), dim3(32, 8), 0, s>>>(g, n, ld);
+  RP_LAUNCH_CHECK();
+}
 
 void residual_in_place(double* r, const double* b, int64_t n, cudaStream_t s) {
   if (n <= 0) return;

@@ -32,8 +32,12 @@ void cg_update(double* x, double* r, const double* p, const double* q, const dou
 // p = r + (*rr_next / *rr) p           (baselines.cpp:152)
 void cg_direction(double* p, const double* r, const double* rr_next, const double* rr, int64_t n, cudaStream_t s);
 
+// dst = src, src a device-mapped (pinned) host buffer read over PCIe by the kernel
+void copy_mapped(const double* src, int64_t n, double* dst, cudaStream_t s);
 // r = r - b  (the residual apply(a, x) - b, adaptive.cpp:64-66)
 void residual_in_place(double* r, const double* b, int64_t n, cudaStream_t s);
+// g[i + j ld] = g[j + i ld] for i < j (copy the lower triangle onto the upper)
+void mirror_lower(double* g, int64_t n, int64_t ld, cudaStream_t s);
 // out (d x cols, ld d) = columns c0 .. c0+cols-1 of the d x d identity.
 void identity_block(double* out, int64_t d, int64_t cols, int64_t c0, cudaStream_t s);
 

@@ -22,7 +22,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libridgepath_b200.so")
 
-RP_HOST, RP_DEVICE = 0, 1
+RP_HOST, RP_DEVICE, RP_HOST_STREAM = 0, 1, 2
 SKETCH_KINDS = ("gaussian", "countsketch", "sjlt", "srht", "identity")
 RHO_PROVENANCE = ("gaussian", "sjlt", "srht", "identity", "manual")
 
@@ -993,9 +993,14 @@ def set_dense_rows_device(ctx: Context, n_global: int, row0: int, n_local: int, 
     ctx._op_key = ("device", ptr, n_global, row0, n_local, d)
 
 
-def set_dense_rows_host(ctx: Context, n_global: int, row0: int, n_local: int, d: int, ptr: int, lda: int):
-    """rp_set_dense_rows from host memory (pinned for full-speed DMA)."""
-    ctx.check(lib().rp_set_dense_rows(ctx.handle, n_global, row0, n_local, d, _P(ptr), lda, RP_HOST))
+def set_dense_rows_host(ctx: Context, n_global: int, row0: int, n_local: int, d: int, ptr: int, lda: int,
+                        stream: bool = False):
+    """rp_set_dense_rows from host memory (pinned for full-speed DMA).  With
+    stream=True (RP_HOST_STREAM) the upload runs asynchronously in column
+    chunks and the next path call consumes them as they land; the host buffer
+    must stay valid until that call returns."""
+    ctx.check(lib().rp_set_dense_rows(ctx.handle, n_global, row0, n_local, d, _P(ptr), lda,
+                                      RP_HOST_STREAM if stream else RP_HOST))
     ctx._op_key = ("host", ptr, n_global, row0, n_local, d)
 
 
