@@ -156,6 +156,10 @@ RP_API int64_t rp_launch_count(void);
 RP_API rp_status rp_last_gemm_profile(rp_ctx* ctx, double* seconds, double* flops, double* bytes, int64_t cap,
                                       int64_t* count);
 
+/* Multi-GPU (one process per GPU): rank 0 makes the id, every rank joins.
+ * world = 1 with id128 = NULL leaves the context without a communicator
+ * (collectives are no-ops); with an id it builds a one-rank NCCL communicator,
+ * so the collective code path runs on a single GPU too. */
 RP_API rp_status rp_comm_unique_id(void* id128);
 RP_API rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128);
 

@@ -395,7 +395,7 @@ OpView op_dual(rp_ctx* ctx) {
 }
 
 void allreduce(rp_ctx* ctx, double* buf, int64_t count) {
-  if (ctx->world <= 1 || count <= 0) return;
+  if (!ctx->comm || count <= 0) return;
   nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm, ctx->stream),
              "ncclAllReduce");
 }
@@ -1513,7 +1513,9 @@ rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128) {
     require(world >= 1 && rank >= 0 && rank < world, "comm: bad rank/world");
     ctx->rank = rank;
     ctx->world = world;
-    if (world == 1) return;
+    // world 1 without an id: no communicator (collectives are no-ops); with an
+    // id, a one-rank NCCL communicator (the collectives then run through NCCL)
+    if (world == 1 && id128 == nullptr) return;
     require(id128 != nullptr, "comm: null unique id");
     ncclUniqueId id;
     std::memcpy(&id, id128, 128);

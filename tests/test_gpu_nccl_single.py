@@ -1,0 +1,42 @@
+"""The NCCL code path on one GPU: a one-rank communicator (rp_comm_init with
+world = 1 and an id) routes every all-reduce of the path, the sketch, the
+Gram matrix, the losses and the baselines through ncclAllReduce.  A one-rank
+sum is the identity, so results must equal the communicator-free run bit for
+bit; this exercises NCCL loading (dlopen), communicator set-up and the stream
+semantics of the collectives on hardware."""
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _runs(rp, ctx, w, K=1):
+    a = w.a
+    if isinstance(a, dict):
+        a = rp.Csr(a["rows"], a["cols"], a["offsets"], a["indices"], a["values"])
+    grid = rp.log_grid(w.lambda_min, w.lambda_max, 30)
+    cfg = rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon)
+    sk = w.sketch
+    spec = rp.SketchSpec(sk["kind"], sk["m"], sk["n"], sk["s"], sk["seed"])
+    rho = rp.RhoBounds.manual(*w.rho)
+    path = rp.ihs_bin_path(a, w.b, cfg, spec, rho, ctx=ctx)
+    cg = rp.warm_cg_path(a, w.b[:, 0], rp.PathConfig(w.lambda_min, w.lambda_max, grid[-5:], 1e-8), ctx=ctx)
+    der = rp.derive_rho(spec, a, w.lambda_min, w.lambda_max, ctx=ctx)
+    return path, cg, der
+
+
+@pytest.mark.parametrize("name", ["c1", "c4"])
+def test_one_rank_nccl_matches_local(rp, oracle, name):
+    w = workloads.get(name, scale=1.0 if name == "c1" else 1 / 1024)
+    plain = rp.Context(0)
+    want = _runs(rp, plain, w)
+    comm = rp.Context(0)
+    rp.comm_init(comm, 0, 1, rp.comm_unique_id())
+    got = _runs(rp, comm, w)
+    for p, q in zip(got[0].points, want[0].points):
+        assert np.array_equal(p.solution, q.solution) and p.train_loss == q.train_loss
+    for p, q in zip(got[1].points, want[1].points):
+        assert np.array_equal(p.solution, q.solution) and p.iterations == q.iterations
+    assert got[2][0] == want[2][0]
