@@ -382,3 +382,16 @@ def test_dual_csr_path_matches_oracle(rp, ctx, oracle):
         ctx.set_option("csr_one_panel_bytes", 48 << 20)
     worst, npts = _worst(got.points, ref.points, oracle)
     assert npts == len(grid) and worst < TOL
+
+
+def test_c2_full_size_every_interval_parity(rp, ctx, oracle):
+    """Full C2 on every interval: all 1000 grid points of the bench workload
+    against the oracle (the CPU side is the bench's reference arm run to the
+    end, ~1-2 minutes on the box's host cores)."""
+    w = workloads.c2()
+    (oa, ocfg, ospec, orho), (ga, gcfg, gspec, grho) = _mirror(rp, oracle, w)
+    ref = oracle.ihs_bin_path(oa, w.b, ocfg, ospec, orho)
+    got = rp.ihs_bin_path(ga, w.b, gcfg, gspec, grho, ctx=ctx)
+    worst, n = _worst(got.points, ref.points, oracle)
+    print(f"C2 full, every interval: {n} lambdas, max rel err {worst:.3e}")
+    assert n == w.T and worst < TOL
