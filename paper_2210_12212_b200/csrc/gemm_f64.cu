@@ -731,8 +731,8 @@ struct TileShape {
   int bm, bn;
 };
 constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128},
-                                {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}};
-constexpr int kNumTiles = 11;
+                                {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}, {64, 48}, {128, 48}};
+constexpr int kNumTiles = 13;
 
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
@@ -749,7 +749,11 @@ void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
     case 8: launch_cfg<128, 64, 16, 2, 2, 3, AK, BKM, VEC>(kp, stream); break;
     // BK = 32, 2 stages: half the barriers per flop
     case 9: launch_cfg<64, 128, 32, 2, 4, 2, AK, BKM, VEC>(kp, stream); break;
-    default: launch_cfg<128, 64, 32, 4, 2, 2, AK, BKM, VEC>(kp, stream); break;
+    case 10: launch_cfg<128, 64, 32, 4, 2, 2, AK, BKM, VEC>(kp, stream); break;
+    // 48-wide tiles: N in (32, 48] (the recursion's P-apply at g + 1 <= 48)
+    // without padding the last third of a 64-wide tile
+    case 11: launch_cfg<64, 48, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
+    default: launch_cfg<128, 48, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
   }
 }
 
@@ -945,11 +949,14 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     // best shape; 9, 10 = BK 32 variants, kept for tuning only)
     // (TMA kernel, the default path; the 4-warp shapes 7, 8 only pay off in
     // the cp.async kernel)
-    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2};
-    static constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99};
+    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2};
+    // (the 48-wide tile only where N fits one of them and a 64-wide tile
+    // would pad a quarter or more: 24 % faster there, profiles/r01_gemm_tune_bn48.txt)
+    static constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0};
     double best = 1e300;
     for (int t = 0; t < kNumTiles; ++t) {
       if (kTiles[t].bn == 16 && g.n > 16) continue;
+      if (kTiles[t].bn == 48 && (g.n <= 32 || g.n > 48)) continue;
       if (kEff[t] <= 0.0) continue;
       const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
       const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));

@@ -28,6 +28,10 @@ int main(int argc, char** argv) {
       {"P  g=1   32x(1024x2x1024)", Op::N, Op::N, 1024, 2, 1024, 32, false, true},
       {"P  g=15  32x(1024x16x1024)", Op::N, Op::N, 1024, 16, 1024, 32, false, true},
       {"P  g=31  32x(1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 32, false, true},
+      {"P  g=35  32x(1024x36x1024)", Op::N, Op::N, 1024, 36, 1024, 32, false, true},
+      {"P  g=41  32x(1024x42x1024)", Op::N, Op::N, 1024, 42, 1024, 32, false, true},
+      {"P  g=47  32x(1024x48x1024)", Op::N, Op::N, 1024, 48, 1024, 32, false, true},
+      {"P  g=55  32x(1024x56x1024)", Op::N, Op::N, 1024, 56, 1024, 32, false, true},
       {"P  g=63  32x(1024x64x1024)", Op::N, Op::N, 1024, 64, 1024, 32, false, true},
       {"SYRK A^T A (1024,65536)", Op::T, Op::N, 1024, 1024, 65536, 1, true, false},
       {"square 4096^3", Op::N, Op::N, 4096, 4096, 4096, 1, false, false},
@@ -51,7 +55,7 @@ int main(int argc, char** argv) {
     auto& sh = shapes[si];
     if (only_shape >= 0 && static_cast<int>(si) != only_shape) continue;
     printf("%-32s", sh.name);
-    for (int tile = -1; tile < 11; ++tile) {
+    for (int tile = -1; tile < kNumTiles; ++tile) {
       if (only_tile != -9 && tile != only_tile) continue;
       GemmArgs g;
       g.opa = sh.opa;
@@ -83,7 +87,7 @@ int main(int argc, char** argv) {
       double fl = 2.0 * sh.m * sh.n * sh.k * sh.batch * (sh.lower ? 0.5 : 1.0);
       printf(" %s%6.1f", tile < 0 ? "auto:" : "", fl / (ms / iters * 1e-3) / 1e12);
     }
-    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64, 64x128w4, 128x64w4, 64x128k32, 128x64k32]\n");
+    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64, 64x128w4, 128x64w4, 64x128k32, 128x64k32, 64x48, 128x48]\n");
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
