@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -611,34 +612,36 @@ __global__ void splitk_reduce(KParams p) {
   }
 }
 
-struct Workspace {
-  std::mutex mu;
+// Split-K partials: one buffer per (device, stream), so GEMMs issued on
+// different streams (the preconditioner build overlapping the Gram matrix)
+// never share partials, and deferred partials stay valid until the next split
+// GEMM on the same stream.  Grown on demand (the grow path synchronizes the
+// stream before freeing the old buffer).
+struct WsBuf {
   double* ptr = nullptr;
   size_t bytes = 0;
-  int device = -1;
+};
+struct Workspace {
+  std::mutex mu;
+  std::map<std::pair<int, cudaStream_t>, WsBuf> bufs;
 };
 Workspace g_ws;
 
-// Split-K partials; grown on demand (the grow path synchronizes the stream).
 double* workspace(size_t bytes, cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(g_ws.mu);
   int dev = 0;
   RP_CUDA(cudaGetDevice(&dev));
-  if (g_ws.device != dev) {  // (a buffer of another device is abandoned)
-    g_ws.ptr = nullptr;
-    g_ws.bytes = 0;
-    g_ws.device = dev;
-  }
-  if (g_ws.bytes < bytes) {
-    if (g_ws.ptr) {
+  WsBuf& w = g_ws.bufs[{dev, stream}];
+  if (w.bytes < bytes) {
+    if (w.ptr) {
       RP_CUDA(cudaStreamSynchronize(stream));
-      RP_CUDA(cudaFree(g_ws.ptr));
+      RP_CUDA(cudaFree(w.ptr));
     }
-    g_ws.ptr = nullptr;
-    RP_CUDA(cudaMalloc(&g_ws.ptr, bytes));
-    g_ws.bytes = bytes;
+    w.ptr = nullptr;
+    RP_CUDA(cudaMalloc(&w.ptr, bytes));
+    w.bytes = bytes;
   }
-  return g_ws.ptr;
+  return w.ptr;
 }
 
 // ---- TMA launch path -------------------------------------------------------------

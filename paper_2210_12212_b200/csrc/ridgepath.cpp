@@ -340,6 +340,7 @@ struct rp_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
+  cudaStream_t side = nullptr;  // low-priority stream: the Gram matrix overlapping the preconditioner build
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -348,6 +349,8 @@ struct rp_ctx {
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
+  int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
+  bool gram_overlap = true;   // option "gram_overlap": Gram SYRK on the side stream, overlapping the precond build
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
   std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
@@ -394,9 +397,10 @@ OpView op_dual(rp_ctx* ctx) {
   return ctx->op.dual();
 }
 
-void allreduce(rp_ctx* ctx, double* buf, int64_t count) {
+void allreduce(rp_ctx* ctx, double* buf, int64_t count, cudaStream_t st = nullptr) {
   if (!ctx->comm || count <= 0) return;
-  nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm, ctx->stream),
+  nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm,
+                              st ? st : ctx->stream),
              "ncclAllReduce");
 }
 
@@ -564,8 +568,8 @@ struct GramOp {
     matrix = true;
   }
 
-  void build_matrix() {
-    cudaStream_t s = ctx->stream;
+  void build_matrix(cudaStream_t st = nullptr) {
+    cudaStream_t s = st ? st : ctx->stream;
     require(!op.sparse, "gram matrix mode needs a dense operator");
     G.alloc(static_cast<size_t>(op.d * op.d), s);
     GemmArgs g;  // G = M^T M (lower + mirror)
@@ -582,8 +586,12 @@ struct GramOp {
     g.ldc = op.d;
     g.lower_only = true;
     g.mirror = true;
+    // (tuning hook for the overlapped build; forcing 128 x 128 tiles, which
+    // leave shared memory for the Cholesky chain's kernels on every SM,
+    // measured slower than the auto choice: 19.16 vs 18.96 ms on C2)
+    if (st && ctx->gram_overlap_tile >= 0) g.force_tile = ctx->gram_overlap_tile;
     dgemm(g, s);
-    allreduce(ctx, G.get(), op.d * op.d);
+    allreduce(ctx, G.get(), op.d * op.d, s);
     matrix = true;
   }
 };
@@ -1049,7 +1057,23 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
       copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
     }
     RP_CUDA(cudaEventRecord(ev.ev[5], s));
-    if (use_matrix) gram.build_matrix();
+  }
+  // The Gram matrix (a throughput-bound SYRK over A) runs on the context's
+  // low-priority side stream, overlapping the preconditioner build below
+  // (a latency-bound Cholesky chain); the basis waits for both.
+  cudaEvent_t gram_done = nullptr;
+  if (use_matrix && !gram.matrix && !ctx->gram_overlap) gram.build_matrix();
+  if (use_matrix && !gram.matrix) {
+    if (!ctx->side) {
+      int lo = 0, hi = 0;
+      RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo));
+    }
+    RP_CUDA(cudaEventCreateWithFlags(&gram_done, cudaEventDisableTiming));
+    RP_CUDA(cudaEventRecord(gram_done, s));
+    RP_CUDA(cudaStreamWaitEvent(ctx->side, gram_done, 0));
+    gram.build_matrix(ctx->side);
+    RP_CUDA(cudaEventRecord(gram_done, ctx->side));
   }
   RP_CUDA(cudaEventRecord(ev.ev[6], s));
   // 4) Interval ownership.  With the Gram matrix every rank holds the whole
@@ -1075,6 +1099,10 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   P.col_stable = ctx->stable_columns;
   gram.col_stable = ctx->stable_columns;
   if (Lo > 0) P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
+  if (gram_done) {
+    RP_CUDA(cudaStreamWaitEvent(s, gram_done, 0));
+    RP_CUDA(cudaEventDestroy(gram_done));  // (released once complete)
+  }
   RP_CUDA(cudaEventRecord(ev.ev[2], s));
   // 5) Bases for all owned intervals at once; diverged intervals are retried
   //    at tau/2 (path_solver.cpp:132-140).
@@ -1432,6 +1460,10 @@ void rp_destroy(rp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->op = OperatorStore();
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->side) {
+      cudaStreamSynchronize(ctx->side);
+      cudaStreamDestroy(ctx->side);
+    }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     cudaSetDevice(prev);
@@ -1468,6 +1500,11 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "csr_panel_rows") {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
+    } else if (k == "gram_overlap_tile") {
+      require(value >= -1 && value < 13, "gram_overlap_tile must be in [-1, 12]");
+      ctx->gram_overlap_tile = static_cast<int>(value);
+    } else if (k == "gram_overlap") {
+      ctx->gram_overlap = value != 0;
     } else if (k == "upload_chunk_bytes") {
       require(value >= 1, "upload_chunk_bytes must be >= 1");
       ctx->upload_chunk_bytes = value;
