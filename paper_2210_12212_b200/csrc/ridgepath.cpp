@@ -1014,6 +1014,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   }
   DBuf<double> sa(static_cast<size_t>(spec.m * dim), s);
   DBuf<double> cbuf(static_cast<size_t>(dim * K), s);
+  cudaEvent_t gram_done = nullptr;  // side-stream Gram matrix (see below)
   if (stream_in) {
     // Chunked consumption of the upload: as column block [c0, c1) of A lands,
     // sketch its columns, form rows c0..c1 of c = A^T b and block row
@@ -1046,6 +1047,22 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     RP_CUDA(cudaEventRecord(ev.ev[5], s));
     if (use_matrix) gram.end_matrix();
   } else {
+    // The Gram matrix (a throughput-bound SYRK over A) runs on the context's
+    // low-priority side stream from the start, overlapping the HBM-bound
+    // sketch and the latency-bound preconditioner build; the basis waits for
+    // both.
+    if (use_matrix && ctx->gram_overlap) {
+      if (!ctx->side) {
+        int lo = 0, hi = 0;
+        RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo));
+      }
+      RP_CUDA(cudaEventCreateWithFlags(&gram_done, cudaEventDisableTiming));
+      RP_CUDA(cudaEventRecord(gram_done, s));
+      RP_CUDA(cudaStreamWaitEvent(ctx->side, gram_done, 0));
+      gram.build_matrix(ctx->side);
+      RP_CUDA(cudaEventRecord(gram_done, ctx->side));
+    }
     // 1) Sketch (once), summed over ranks.
     sketch_apply(spec, op, sa.get(), s);
     allreduce(ctx, sa.get(), spec.m * dim);
@@ -1058,23 +1075,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     }
     RP_CUDA(cudaEventRecord(ev.ev[5], s));
   }
-  // The Gram matrix (a throughput-bound SYRK over A) runs on the context's
-  // low-priority side stream, overlapping the preconditioner build below
-  // (a latency-bound Cholesky chain); the basis waits for both.
-  cudaEvent_t gram_done = nullptr;
-  if (use_matrix && !gram.matrix && !ctx->gram_overlap) gram.build_matrix();
-  if (use_matrix && !gram.matrix) {
-    if (!ctx->side) {
-      int lo = 0, hi = 0;
-      RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo));
-    }
-    RP_CUDA(cudaEventCreateWithFlags(&gram_done, cudaEventDisableTiming));
-    RP_CUDA(cudaEventRecord(gram_done, s));
-    RP_CUDA(cudaStreamWaitEvent(ctx->side, gram_done, 0));
-    gram.build_matrix(ctx->side);
-    RP_CUDA(cudaEventRecord(gram_done, ctx->side));
-  }
+  if (use_matrix && !gram.matrix) gram.build_matrix();  // (gram_overlap off)
   RP_CUDA(cudaEventRecord(ev.ev[6], s));
   // 4) Interval ownership.  With the Gram matrix every rank holds the whole
   //    operator state (SA, c, G are all-reduced), so the intervals -- which are
