@@ -1,6 +1,7 @@
 // Batched SPD inverse: potrf (right-looking, 64-wide panels) -> trtri
 // (recursive doubling) -> P = L^{-T} L^{-1}; the O(n^3) parts run as DMMA GEMMs.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -107,6 +108,158 @@ __global__ void __launch_bounds__(256) potrf_diag(double* h, int64_t ld, int64_t
   }
 }
 
+// Same contract as potrf_diag, blocked by 4 columns: per block of four a
+// single thread factors the 4 x 4 diagonal block (and inverts it), every
+// thread solves its row of the 64 x 4 panel against it, then applies the
+// rank-4 trailing update as four sequential rank-1 steps (the unblocked
+// kernel's order).  The triangular inverse runs as block forward
+// substitution with the stored 4 x 4 inverses.  3 + 2 barriers per four
+// columns instead of 2 + 2 per column.
+__global__ void __launch_bounds__(256) potrf_diag4(double* h, int64_t ld, int64_t stride, int64_t k0, int kb,
+                                                   int* info) {
+  __shared__ double Ls[NB][NB + 1];    // Ls[c][r] = L(r, c), r >= c
+  __shared__ double Pn[NB][5];         // the current 64 x 4 panel, Pn[r][s] = A(r, j0 + s)
+  __shared__ double invD[NB / 4][4][4];  // inverses of the 4 x 4 diagonal blocks of L
+  __shared__ double Yb[4][NB + 1];     // block forward substitution: right-hand rows / solved rows
+  __shared__ double Xb[4][NB + 1];
+  __shared__ int bad_s;
+  double* A = h + blockIdx.x * stride + k0 + k0 * ld;
+  const int r = threadIdx.x & (NB - 1);
+  const int part = threadIdx.x >> 6;  // 0..3
+  double t[NB / 4];
+  {
+    const int rc = min(r, kb - 1);
+    double v[NB / 4];
+#pragma unroll
+    for (int cc = 0; cc < NB / 4; ++cc) v[cc] = A[rc + static_cast<int64_t>(min(4 * cc + part, kb - 1)) * ld];
+#pragma unroll
+    for (int cc = 0; cc < NB / 4; ++cc) {
+      const int c = 4 * cc + part;
+      t[cc] = (r < kb && c < kb) ? (c <= r ? v[cc] : 0.0) : (r == c ? 1.0 : 0.0);
+    }
+  }
+  if (threadIdx.x == 0) bad_s = 0;
+#pragma unroll 1
+  for (int q = 0; q < NB / 4; ++q) {
+    const int j0 = 4 * q;
+    double tq = t[0];
+#pragma unroll
+    for (int cc = 1; cc < NB / 4; ++cc) tq = (cc == q) ? t[cc] : tq;
+    Pn[r][part] = tq;  // A(r, j0 + part) after the previous blocks' updates
+    __syncthreads();
+    if (threadIdx.x == 0) {  // 4 x 4 Cholesky of the diagonal block, then its inverse
+      double L4[4][4] = {};
+      for (int a = 0; a < 4; ++a) {
+        double d = Pn[j0 + a][a];
+        for (int b = 0; b < a; ++b) d -= L4[a][b] * L4[a][b];
+        if (!(d > 0.0) || !isfinite(d)) {
+          if (!bad_s) bad_s = j0 + a + 1;
+          d = 1.0;  // keep going; the caller reports the failure
+        }
+        L4[a][a] = sqrt(d);
+        const double rp = 1.0 / L4[a][a];
+        for (int i = a + 1; i < 4; ++i) {
+          double v = Pn[j0 + i][a];
+          for (int b = 0; b < a; ++b) v -= L4[i][b] * L4[a][b];
+          L4[i][a] = v * rp;
+        }
+      }
+      double I4[4][4] = {};
+      for (int a = 0; a < 4; ++a) {
+        I4[a][a] = 1.0 / L4[a][a];
+        for (int i = a + 1; i < 4; ++i) {
+          double v = 0.0;
+          for (int b = a; b < i; ++b) v += L4[i][b] * I4[b][a];
+          I4[i][a] = -v / L4[i][i];
+        }
+      }
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+          invD[q][a][b] = I4[a][b];
+          if (b <= a) Ls[j0 + b][j0 + a] = L4[a][b];
+        }
+    }
+    __syncthreads();
+    // panel rows below the block: L(r, j0 + part) = sum_{s <= part} A(r, j0 + s) (L44^{-1})(part, s)
+    if (r >= j0 + 4) {
+      double l = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2)
+        if (s2 <= part) l += Pn[r][s2] * invD[q][part][s2];
+      Ls[j0 + part][r] = l;
+    }
+    __syncthreads();
+    if (r >= j0) {
+      // this thread's column j0 + part of L (the diagonal block from Ls)
+      const double l = (r >= j0 + 4) ? Ls[j0 + part][r] : (part <= r - j0 ? Ls[j0 + part][r] : 0.0);
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) t[cc] = (cc == q) ? l : t[cc];
+    }
+    if (r >= j0 + 4) {  // rank-4 trailing update, four rank-1 steps in column order
+      double lr[4];
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) lr[s2] = Ls[j0 + s2][r];
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) {
+        const int c = 4 * cc + part;
+        if (cc > q && c <= r) {
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) t[cc] -= lr[s2] * Ls[j0 + s2][c];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int bad = bad_s;
+    if (bad && bad <= kb && info[blockIdx.x] == 0) info[blockIdx.x] = static_cast<int>(k0 + bad);
+  }
+  // X = L^{-1} by block forward substitution: y(r, :) = e_r - sum_{i < j0} L(r, i) X(i, :)
+  // for the rows of the current block, X_J = L_JJ^{-1} y_J.
+  double x[NB / 4];
+#pragma unroll
+  for (int cc = 0; cc < NB / 4; ++cc) x[cc] = (4 * cc + part == r) ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int q = 0; q < NB / 4; ++q) {
+    const int j0 = 4 * q;
+    if (r >= j0 && r < j0 + 4) {
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) Yb[r - j0][4 * cc + part] = x[cc];
+    }
+    __syncthreads();
+    if (r >= j0 && r < j0 + 4) {
+      const int a = r - j0;
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) {
+        const int c = 4 * cc + part;
+        double v = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2)
+          if (s2 <= a) v += invD[q][a][s2] * Yb[s2][c];
+        x[cc] = v;
+        Xb[a][c] = v;
+      }
+    }
+    __syncthreads();
+    if (r >= j0 + 4) {
+      double lr[4];
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) lr[s2] = Ls[j0 + s2][r];
+#pragma unroll
+      for (int cc = 0; cc < NB / 4; ++cc) {
+        const int c = 4 * cc + part;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) x[cc] -= lr[s2] * Xb[s2][c];
+      }
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < NB / 4; ++cc) {
+    const int c = 4 * cc + part;
+    if (r < kb && c < kb) A[r + c * ld] = (c <= r) ? x[cc] : 0.0;
+  }
+}
+
 __global__ void shifted_copy_kernel(const double* __restrict__ g, int64_t n, const double* __restrict__ shifts,
                                     double* __restrict__ h) {
   const int64_t b = blockIdx.y;
@@ -117,6 +270,15 @@ __global__ void shifted_copy_kernel(const double* __restrict__ g, int64_t n, con
     const int64_t i = idx % n, j = idx / n;
     H[idx] = (i == j) ? g[idx] + s : (i > j ? g[idx] : 0.0);
   }
+}
+
+// RP_POTRF_DIAG=1 selects the unblocked diagonal kernel (A/B).
+bool blocked_diag() {
+  static const bool on = [] {
+    const char* e = std::getenv("RP_POTRF_DIAG");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 unsigned grid1(int64_t work) {
@@ -191,7 +353,10 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   cudaEvent_t prev_rest = nullptr;  // trailing update of the previous panel (aux stream)
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
-    potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
+    if (blocked_diag())
+      potrf_diag4<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
+    else
+      potrf_diag<<<static_cast<unsigned>(batch), 256, 0, stream>>>(h, ld, stride, k0, kb, info.get());
     RP_LAUNCH_CHECK();
     const int64_t rows = n - k0 - kb;
     if (rows <= 0) break;
