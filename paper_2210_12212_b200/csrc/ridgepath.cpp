@@ -1051,7 +1051,9 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // low-priority side stream from the start, overlapping the HBM-bound
     // sketch and the latency-bound preconditioner build; the basis waits for
     // both.
-    if (use_matrix && ctx->gram_overlap) {
+    // (single process only: with a communicator the Gram all-reduce would be
+    // in flight on a second stream next to the sketch all-reduce)
+    if (use_matrix && ctx->gram_overlap && !ctx->comm) {
       if (!ctx->side) {
         int lo = 0, hi = 0;
         RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
