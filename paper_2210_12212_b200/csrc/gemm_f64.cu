@@ -518,6 +518,12 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32)
     tma::fence_barrier_init();
   }
   __syncthreads();
+  // Programmatic dependent launch: the next PDL-launched GEMM may start its
+  // CTAs (barrier set-up) as ours retire; nothing below touches global memory
+  // before the previous grid has completed (griddepcontrol.wait; a no-op when
+  // this grid was launched without the attribute).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   double acc[C::FM][C::FN][2];
 #pragma unroll
@@ -646,6 +652,12 @@ double* workspace(size_t bytes, cudaStream_t stream) {
 
 // ---- TMA launch path -------------------------------------------------------------
 
+// RP_GEMM_PDL=0 disables programmatic dependent launch of the TMA GEMM.
+bool g_pdl_enabled = [] {
+  const char* e = std::getenv("RP_GEMM_PDL");
+  return !(e && e[0] == '0');
+}();
+
 bool g_tma_enabled = [] {
   const char* e = std::getenv("RP_GEMM_TMA");
   return !(e && e[0] == '0');
@@ -700,7 +712,17 @@ bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
   }
   dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
             static_cast<unsigned>(kp.batch * kp.batch2 * kp.split));
-  kern<<<grid, C::THREADS + 32, smem, stream>>>(amap, bmap, kp, ab1, ab2, bb1, bb2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(C::THREADS + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl_enabled ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RP_CUDA(cudaLaunchKernelEx(&cfg, kern, amap, bmap, kp, ab1, ab2, bb1, bb2));
   RP_LAUNCH_CHECK();
   return true;
 }
