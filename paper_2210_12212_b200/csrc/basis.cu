@@ -22,6 +22,10 @@ __device__ __forceinline__ double sum_partials(const Partials& P, int64_t b, int
 // column bookkeeping (j, b, l, r) is done once per block, not per element.
 __global__ void build_args_kernel(BasisDims d, int64_t g, Partials y, const double* __restrict__ gen,
                                   const double* __restrict__ tau, double* __restrict__ args, int64_t col0) {
+  // (launched with programmatic dependent launch between the Gram GEMM and the
+  // preconditioner GEMM: let the latter start early, wait for the former)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t nb = d.L * d.K;
   const int64_t col = blockIdx.y + col0;  // = j*NB + b
   const int64_t j = col / nb, b = col - j * nb;
@@ -220,7 +224,16 @@ void for_col_chunks(int64_t rows, int64_t cols, F launch) {
 void build_args(const BasisDims& d, int64_t g, const Partials& y, const double* gen, const double* d_tau,
                 double* args_im, cudaStream_t stream) {
   for_col_chunks(d.dim, (g + 1) * d.nb(), [&](dim3 grid, int64_t c0) {
-    build_args_kernel<<<grid, 256, 0, stream>>>(d, g, y, gen, d_tau, args_im, c0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RP_CUDA(cudaLaunchKernelEx(&cfg, build_args_kernel, d, g, y, gen, d_tau, args_im, c0));
   });
 }
 
