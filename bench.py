@@ -364,6 +364,9 @@ def run_ours(args, w):
             byts = 8.0 * nl * d
             passes[name] = {"seconds": t, "algorithmic_bytes": byts, "achieved_gbs": byts / t / 1e9,
                             "frac_hbm": byts / t / 1e9 / hbm, "timing": "median of 10 calls, CUDA events"}
+            if name == "gram_fused_w4":
+                passes[name]["note"] = ("4 columns: 8 FP64 FMAs + 2 shared-memory reads per element of A on 17 "
+                                        "warps per SM; issue-bound, not HBM-bound (ncu: profiles/r01_ncu_colpass.json)")
 
     # e2e through the public API with host buffers: pinned A and b copied in,
     # x copied out, every step.
