@@ -9,7 +9,10 @@
  * (matrix.hpp:16-50).  `where` says whether a buffer lives in host memory
  * (RP_HOST, copied in/out inside the call) or in device memory on the
  * context's GPU (RP_DEVICE, used in place; results are ready when the call
- * returns unless stated otherwise).
+ * returns unless stated otherwise).  Device buffers are read and written on
+ * the context's stream (its own non-blocking stream unless rp_set_stream
+ * selects the caller's): a caller producing inputs on another stream must
+ * order them first (rp_set_stream to that stream, or a synchronization).
  *
  * Errors: every function returns rp_status; the message of the last failure on
  * a context is available from rp_last_error().  Status codes map the
