@@ -89,3 +89,39 @@ def test_streamed_upload_generic_readers_wait(rp, ctx, oracle):
     assert oracle.rel_error(out, b2.numpy() @ y) < 1e-13
     ctx.set_option("upload_chunk_bytes", 32 << 20)
     ctx._op_key = None
+
+
+def test_streamed_upload_pageable_and_column_shard(rp, ctx, oracle):
+    """RP_HOST_STREAM from pageable memory (the copies degrade to synchronous
+    ones) and for a column-sharded (dual-route) operator (no chunked consumer:
+    the first reader waits for the whole upload) give the resident results."""
+    w = workloads.c2(scale=1 / 16)
+    n, d = w.a.shape
+    grid = rp.log_grid(w.lambda_min, w.lambda_max, 20)
+    cfg = rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon)
+    spec = rp.SketchSpec("srht", 4 * d, n, 1, 3)
+    rho = rp.RhoBounds.manual(*workloads.mp_envelope(d, 4 * d))
+    ctx.set_option("upload_chunk_bytes", n * 8 * 24)
+    try:
+        xr, _ = _run(rp, ctx, w.a, w.b, cfg, spec, rho, False)
+        a_cm = np.ascontiguousarray(w.a.T)  # pageable, column-major A
+        b_cm = np.ascontiguousarray(w.b[:, 0])
+        x = np.empty(len(grid) * d)
+        ctx.check(rp.lib().rp_set_dense_rows(ctx.handle, n, 0, n, d, rp._ptr(a_cm), n, rp.RP_HOST_STREAM))
+        rp.path_raw(ctx, b_cm.ctypes.data, 1, cfg, spec, rho, x.ctypes.data, rp.RP_HOST)
+        ctx._op_key = None
+        for t in range(len(grid)):
+            assert oracle.rel_error(x[t * d:(t + 1) * d], xr[t, 0]) < 1e-11
+        # dual route on a column-sharded streamed operator (one rank holds every column)
+        a2 = np.ascontiguousarray(w.a[:, :40].T)  # A' = first 40 columns (n x 40), column-major
+        sk = rp.SketchSpec("countsketch", 16, 40, 1, 5)  # sketch of A'^T (40 rows)
+        outs = []
+        for where in (rp.RP_HOST, rp.RP_HOST_STREAM):
+            ctx.check(rp.lib().rp_set_dense_cols(ctx.handle, n, 40, 0, 40, rp._ptr(a2), n, where))
+            sa = np.empty(16 * n)
+            ctx.check(rp.lib().rp_sketch_apply(ctx.handle, rp.ctypes.byref(sk.c()), 1, rp._ptr(sa), rp.RP_HOST))
+            outs.append(sa)
+        ctx._op_key = None
+        assert np.array_equal(outs[0], outs[1])
+    finally:
+        ctx.set_option("upload_chunk_bytes", 32 << 20)
