@@ -341,6 +341,7 @@ struct rp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   cudaStream_t side = nullptr;  // low-priority stream: the Gram matrix overlapping the preconditioner build
+  cudaStream_t hi = nullptr;    // high-priority stream: the sketch while the Gram matrix is in flight
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -1065,8 +1066,26 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
       gram.build_matrix(ctx->side);
       RP_CUDA(cudaEventRecord(gram_done, ctx->side));
     }
-    // 1) Sketch (once), summed over ranks.
-    sketch_apply(spec, op, sa.get(), s);
+    // 1) Sketch (once), summed over ranks.  While the Gram SYRK occupies the
+    //    low-priority side stream, the sketch -- on the critical path to the
+    //    preconditioner -- runs on the context's high-priority stream.
+    if (gram_done) {
+      if (!ctx->hi) {
+        int lo = 0, hi = 0;
+        RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        RP_CUDA(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, hi));
+      }
+      cudaEvent_t fork;
+      RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      RP_CUDA(cudaEventRecord(fork, s));
+      RP_CUDA(cudaStreamWaitEvent(ctx->hi, fork, 0));
+      sketch_apply(spec, op, sa.get(), ctx->hi);
+      RP_CUDA(cudaEventRecord(fork, ctx->hi));
+      RP_CUDA(cudaStreamWaitEvent(s, fork, 0));
+      RP_CUDA(cudaEventDestroy(fork));
+    } else {
+      sketch_apply(spec, op, sa.get(), s);
+    }
     allreduce(ctx, sa.get(), spec.m * dim);
     RP_CUDA(cudaEventRecord(ev.ev[1], s));
     // 3) Linear term: c = M^T b (primal) or c = b (dual).
@@ -1466,6 +1485,10 @@ void rp_destroy(rp_ctx* ctx) {
     if (ctx->side) {
       cudaStreamSynchronize(ctx->side);
       cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->hi) {
+      cudaStreamSynchronize(ctx->hi);
+      cudaStreamDestroy(ctx->hi);
     }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->own) cudaStreamDestroy(ctx->own);
