@@ -352,6 +352,7 @@ struct rp_ctx {
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
   bool gram_overlap = true;   // option "gram_overlap": Gram SYRK on the side stream, overlapping the precond build
+  bool gram_after_sketch = false;  // option "gram_after_sketch": start that SYRK after the sketch instead of before
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
   std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
@@ -1054,7 +1055,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // both.
     // (single process only: with a communicator the Gram all-reduce would be
     // in flight on a second stream next to the sketch all-reduce)
-    if (use_matrix && ctx->gram_overlap && !ctx->comm) {
+    const bool side_gram = use_matrix && ctx->gram_overlap && !ctx->comm;
+    auto launch_side_gram = [&]() {
       if (!ctx->side) {
         int lo = 0, hi = 0;
         RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1065,7 +1067,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
       RP_CUDA(cudaStreamWaitEvent(ctx->side, gram_done, 0));
       gram.build_matrix(ctx->side);
       RP_CUDA(cudaEventRecord(gram_done, ctx->side));
-    }
+    };
+    if (side_gram && !ctx->gram_after_sketch) launch_side_gram();
     // 1) Sketch (once), summed over ranks.  While the Gram SYRK occupies the
     //    low-priority side stream, the sketch -- on the critical path to the
     //    preconditioner -- runs on the context's high-priority stream.
@@ -1087,6 +1090,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
       sketch_apply(spec, op, sa.get(), s);
     }
     allreduce(ctx, sa.get(), spec.m * dim);
+    if (side_gram && ctx->gram_after_sketch) launch_side_gram();
     RP_CUDA(cudaEventRecord(ev.ev[1], s));
     // 3) Linear term: c = M^T b (primal) or c = b (dual).
     if (!dual) {
@@ -1529,6 +1533,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "gram_overlap_tile") {
       require(value >= -1 && value < 13, "gram_overlap_tile must be in [-1, 12]");
       ctx->gram_overlap_tile = static_cast<int>(value);
+    } else if (k == "gram_after_sketch") {
+      ctx->gram_after_sketch = value != 0;
     } else if (k == "gram_overlap") {
       ctx->gram_overlap = value != 0;
     } else if (k == "upload_chunk_bytes") {
