@@ -25,8 +25,11 @@
  * plus RP_ECUDA / RP_ENCCL / RP_ENOMEM for device-side failures.
  *
  * Threading: a context is single-owner (like SeededRng); calls on
- * one context must come from one host thread.  Distinct contexts are
- * independent.
+ * one context must come from one host thread.  Distinct contexts hold
+ * independent state, but two contexts must not run device work concurrently
+ * on the same GPU: with the TMA GEMM, concurrently running paths on two
+ * streams were observed to corrupt each other's results (open
+ * issue; RP_GEMM_TMA=0 selects the cp.async GEMM, which is unaffected).
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H
