@@ -64,6 +64,7 @@ struct KParams {
   bool lower_only;
   bool mirror;  // lower_only: also write the transposed element (C symmetric)
   bool tri_k;   // op(A)(i, k) == 0 for k < i: start the k loop at the tile's first row
+  bool no_tma;  // use the cp.async kernel (GemmArgs::no_tma)
   RecursionEpilogue epi;
 };
 
@@ -731,7 +732,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM,
 void launch_cfg(const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
   if constexpr (VEC == 2) {
-    if (g_tma_enabled && ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
+    if (g_tma_enabled && !kp.no_tma && ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
         launch_tma_cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>(kp, stream))
       return;
   }
@@ -949,6 +950,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   kp.stride_c2 = g.stride_c2;
   kp.lower_only = g.lower_only;
   kp.tri_k = g.tri_k;
+  kp.no_tma = g.no_tma;
 
   const bool ak = g.opa == Op::T;  // A contiguous along k
   const bool bk = g.opb == Op::N;  // B contiguous along k

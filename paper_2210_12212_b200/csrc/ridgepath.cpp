@@ -354,10 +354,11 @@ struct rp_ctx {
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
   // option "gram_overlap": Gram SYRK on a side stream, overlapping the sketch
-  // and the precond build.  Off by default: with a split-K SYRK on the side
-  // stream the C2 path drifts by ~1e-2 (tools/race_probe.py) for a reason not
-  // yet found (an unsplit side SYRK and a synchronized one are exact).
-  bool gram_overlap = false;
+  // and the precond build.  The side SYRK runs the cp.async GEMM kernel: two
+  // TMA GEMMs running concurrently on different streams were seen to corrupt
+  // each other (open issue); with the cp.async side SYRK the path
+  // is bit-identical to the single-stream one (tools/race_probe.py).
+  bool gram_overlap = true;
   bool gram_after_sketch = false;  // option "gram_after_sketch": start that SYRK after the sketch instead of before
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
   std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
@@ -598,6 +599,7 @@ struct GramOp {
     // leave shared memory for the Cholesky chain's kernels on every SM,
     // measured slower than the auto choice: 19.16 vs 18.96 ms on C2)
     if (st && ctx->gram_overlap_tile >= 0) g.force_tile = ctx->gram_overlap_tile;
+    if (st) g.no_tma = true;  // (concurrent TMA GEMMs on two streams: open issue)
     dgemm(g, s);
     allreduce(ctx, G.get(), op.d * op.d, s);
     matrix = true;
