@@ -1063,7 +1063,9 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // both.
     // (single process only: with a communicator the Gram all-reduce would be
     // in flight on a second stream next to the sketch all-reduce)
-    const bool side_gram = use_matrix && ctx->gram_overlap && !ctx->comm;
+    // (only for small Gram matrices: a large SYRK -- C5's 16384^2 -- on the
+    // slower cp.async kernel outlasts what it overlaps)
+    const bool side_gram = use_matrix && ctx->gram_overlap && !ctx->comm && op.d <= 4096;
     auto launch_side_gram = [&]() {
       if (!ctx->side) {
         int lo = 0, hi = 0;
