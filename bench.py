@@ -283,8 +283,12 @@ def run_ours(args, w):
 
     # Roofline of the dominant kernel family (FP64 DMMA GEMM): the same steps
     # again with every GEMM bracketed by CUDA events on the step's stream.
+    # (profiled steps keep every GEMM on one stream, so each launch is timed
+    # alone: the side-stream Gram overlap of the timed steps is switched off)
     ctx.set_option("profile", 1)
+    ctx.set_option("gram_overlap", 0)
     prof = [step() for _ in range(max(1, min(args.steps, 3)))]
+    ctx.set_option("gram_overlap", 1)
     ctx.set_option("profile", 0)
     l_sec, l_flops, l_bytes = rp.last_gemm_profile(ctx)  # per launch, last profiled step
     g_s = sum(p.gemm_seconds for p in prof)
