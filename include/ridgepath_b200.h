@@ -26,10 +26,10 @@
  *
  * Threading: a context is single-owner (like SeededRng); calls on
  * one context must come from one host thread.  Distinct contexts hold
- * independent state, but two contexts must not run device work concurrently
- * on the same GPU: with the TMA GEMM, concurrently running paths on two
- * streams were observed to corrupt each other's results (open
- * issue; RP_GEMM_TMA=0 selects the cp.async GEMM, which is unaffected).
+ * independent state and may be driven from different threads: calls are
+ * synchronous and a per-device lock serializes the calls of contexts that
+ * share a GPU (concurrently running TMA GEMMs of two streams were observed to
+ * corrupt each other's results, open issue).
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <optional>
 #include <string>
@@ -1271,11 +1272,24 @@ namespace {
 
 thread_local std::string g_err_noctx;
 
+// One lock per device, held for the whole of every context call: calls are
+// synchronous, so contexts sharing a GPU never overlap their device work
+// (concurrently running TMA GEMMs of two streams were seen to corrupt each
+// other, DESIGN.md open issue).  Recursive: a call may use another entry point.
+std::recursive_mutex& device_mutex(int dev) {
+  static std::recursive_mutex m[64];
+  return m[static_cast<unsigned>(dev) % 64];
+}
+
 template <class F>
 rp_status guarded(rp_ctx* ctx, F&& f) {
   try {
     std::optional<DeviceGuard> guard;
-    if (ctx) guard.emplace(ctx->device);
+    std::unique_lock<std::recursive_mutex> lock;
+    if (ctx) {
+      lock = std::unique_lock<std::recursive_mutex>(device_mutex(ctx->device));
+      guard.emplace(ctx->device);
+    }
     f();
     return RP_OK;
   } catch (const InvalidArgument& e) {

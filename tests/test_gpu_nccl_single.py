@@ -40,3 +40,32 @@ def test_one_rank_nccl_matches_local(rp, oracle, name):
     for p, q in zip(got[1].points, want[1].points):
         assert np.array_equal(p.solution, q.solution) and p.iterations == q.iterations
     assert got[2][0] == want[2][0]
+
+
+def test_concurrent_contexts(rp, oracle):
+    """Two contexts on one GPU driven from two host threads give the results of
+    sequential runs (calls of contexts sharing a device are serialized)."""
+    import threading
+
+    w = workloads.get("c1")
+    grid = rp.log_grid(w.lambda_min, w.lambda_max, 30)
+    cfg = rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon)
+    sk = w.sketch
+    spec = rp.SketchSpec(sk["kind"], sk["m"], sk["n"], sk["s"], sk["seed"])
+    rho = rp.RhoBounds.manual(*w.rho)
+    want = rp.ihs_bin_path(w.a, w.b, cfg, spec, rho, ctx=rp.Context(0))
+    ctxs = [rp.Context(0), rp.Context(0)]
+    got = [None, None]
+
+    def run(i):
+        for _ in range(3):
+            got[i] = rp.ihs_bin_path(w.a, w.b, cfg, spec, rho, ctx=ctxs[i])
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for res in got:
+        for p, q in zip(res.points, want.points):
+            assert np.array_equal(p.solution, q.solution)
