@@ -354,6 +354,7 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
+  bool gram_overlap_tma = false;  // option "gram_overlap_tma": TMA kernel for the overlapped SYRK (probe)
   // option "gram_overlap": Gram SYRK on a side stream, overlapping the sketch
   // and the precond build.  The side SYRK runs the cp.async GEMM kernel: two
   // TMA GEMMs running concurrently on different streams were seen to corrupt
@@ -600,7 +601,7 @@ struct GramOp {
     // leave shared memory for the Cholesky chain's kernels on every SM,
     // measured slower than the auto choice: 19.16 vs 18.96 ms on C2)
     if (st && ctx->gram_overlap_tile >= 0) g.force_tile = ctx->gram_overlap_tile;
-    if (st) g.no_tma = true;  // (concurrent TMA GEMMs on two streams: open issue)
+    if (st && !ctx->gram_overlap_tma) g.no_tma = true;  // (concurrent TMA GEMMs on two streams: open issue)
     dgemm(g, s);
     allreduce(ctx, G.get(), op.d * op.d, s);
     matrix = true;
@@ -1554,6 +1555,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "csr_panel_rows") {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
+    } else if (k == "gram_overlap_tma") {
+      ctx->gram_overlap_tma = value != 0;
     } else if (k == "gram_overlap_tile") {
       require(value >= -1 && value < 13, "gram_overlap_tile must be in [-1, 12]");
       ctx->gram_overlap_tile = static_cast<int>(value);
