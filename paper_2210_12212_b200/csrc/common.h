@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -56,6 +58,29 @@ inline std::atomic<int64_t>& launch_counter() {
   } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+
+// Raises a kernel's dynamic shared-memory limit on the current device to at
+// least `bytes`, never lowering it: the attribute is per function and device,
+// shared by every thread and context, so a caller needing less must not
+// undercut another's launch (a lowered limit fails that launch with "invalid
+// argument").
+inline void ensure_dynamic_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> limits;
+  int dev = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = limits[{func, dev}];
+  if (bytes > cur) {
+    RP_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    cur = bytes;
+  }
+}
+template <class F>
+void ensure_dynamic_smem(F* func, size_t bytes) {
+  ensure_dynamic_smem(reinterpret_cast<const void*>(func), bytes);
+}
 
 }  // namespace rpb
 

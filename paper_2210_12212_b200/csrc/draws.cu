@@ -131,12 +131,8 @@ void run_jobs(const std::vector<JumpJob>& jobs, uint64_t* d_states, const uint64
   RP_CUDA(cudaMemcpyAsync(d_meta.get(), meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
   RP_CUDA(cudaMemcpyAsync(d_polys.get(), polys.data(), polys.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
                           stream));
-  static bool attr = false;
   const int smem = kSeqWords * 8;
-  if (!attr) {
-    RP_CUDA(cudaFuncSetAttribute(jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  ensure_dynamic_smem(jump_kernel, smem);
   const int n = static_cast<int>(jobs.size());
   const int parts = std::max(1, std::min(16, 296 / n));
   jump_kernel<<<n * parts, kJumpThreads, smem, stream>>>(src_base, d_meta.get(), d_states, d_meta.get() + n,
@@ -604,7 +600,7 @@ void draw_srht(uint64_t seed, int64_t n, int64_t m, double* d_signs, int64_t* d_
   RP_CUDA(cudaStreamSynchronize(stream));
   if (!hflag && npad <= 65536) {
     const int bytes = static_cast<int>(npad * sizeof(uint16_t));
-    RP_CUDA(cudaFuncSetAttribute(srht_swap_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    ensure_dynamic_smem(srht_swap_small_kernel, bytes);
     srht_swap_small_kernel<<<1, 256, bytes, stream>>>(jv.get(), m, npad, d_rows);
     RP_LAUNCH_CHECK();
     RP_CUDA(cudaStreamSynchronize(stream));
@@ -613,12 +609,12 @@ void draw_srht(uint64_t seed, int64_t n, int64_t m, double* d_signs, int64_t* d_
   auto go = [&](auto seq_kern, auto swap_kern, bool smem) {
     const int bytes = smem ? static_cast<int>(2 * cap * sizeof(int64_t)) : 0;
     if (!hflag) {
-      if (smem) RP_CUDA(cudaFuncSetAttribute(swap_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      if (smem) ensure_dynamic_smem(swap_kern, bytes);
       swap_kern<<<1, 256, bytes, stream>>>(jv.get(), m, d_rows, keys.get(), vals.get());
     } else {  // a rejection somewhere: exact sequential consumer from offset n
       DBuf<uint64_t> st(kN, stream);
       mt::states_at(seed, {static_cast<uint64_t>(n)}, st.get(), stream);
-      if (smem) RP_CUDA(cudaFuncSetAttribute(seq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      if (smem) ensure_dynamic_smem(seq_kern, bytes);
       seq_kern<<<1, kGenThreads, bytes, stream>>>(st.get(), m, npad, d_rows, keys.get(), vals.get());
       RP_CUDA(cudaStreamSynchronize(stream));
     }

@@ -23,6 +23,14 @@ namespace {
 
 thread_local int g_last_launches = 0;
 
+constexpr int kMaxDevices = 64;
+int current_device() {
+  int dev = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  require(dev >= 0 && dev < kMaxDevices, "dgemm: device ordinal out of range");
+  return dev;
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
@@ -706,10 +714,11 @@ bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
   if (!ok_b) return false;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
   constexpr int smem = C::SMEM_BYTES + 128;
-  static bool attr_set = false;  // per template instantiation
-  if (!attr_set) {
+  static std::atomic<bool> attr_set[kMaxDevices];  // per template instantiation and device
+  const int dev = current_device();
+  if (!attr_set[dev].load(std::memory_order_acquire)) {
     RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
+    attr_set[dev].store(true, std::memory_order_release);
   }
   dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
             static_cast<unsigned>(kp.batch * kp.batch2 * kp.split));
@@ -737,10 +746,11 @@ void launch_cfg(const KParams& kp, cudaStream_t stream) {
       return;
   }
   auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
-  static bool attr_set = false;  // per template instantiation
-  if (!attr_set) {
+  static std::atomic<bool> attr_set[kMaxDevices];  // per template instantiation and device
+  const int dev = current_device();
+  if (!attr_set[dev].load(std::memory_order_acquire)) {
     RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr_set = true;
+    attr_set[dev].store(true, std::memory_order_release);
   }
   require(ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
               ceil_div(kp.m, BM) < (int64_t{1} << 31),

@@ -492,18 +492,13 @@ bool colpass_launch(const double* a, int64_t lda, int64_t n, int64_t d, const do
   int dev = 0, sms = 0;
   RP_CUDA(cudaGetDevice(&dev));
   RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  static thread_local size_t smem_set = 0;  // (per instantiation: raise the limit once)
   const int64_t nfull = n / kPR;
   const bool tail = n % kPR != 0;
   const int grid = static_cast<int>(std::min<int64_t>(nfull, sms));
   const int64_t parts = grid + (tail ? 1 : 0);
   DBuf<double> ws(static_cast<size_t>(parts) * d * K, s);
   if (grid > 0) {
-    if (smem > smem_set) {
-      RP_CUDA(cudaFuncSetAttribute(colpass_kernel<K, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-      smem_set = smem;
-    }
+    ensure_dynamic_smem(colpass_kernel<K, GRAM>, smem);
     colpass_kernel<K, GRAM><<<grid, (kPWarps + 1) * 32, smem, s>>>(rowmap, colmap, n, nfull, d, v, ws.get(), stages);
     RP_LAUNCH_CHECK();
   }

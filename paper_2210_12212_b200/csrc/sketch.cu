@@ -393,14 +393,13 @@ void launch_fwht2(FwhtArgs f, cudaStream_t stream) {
   }
   if (ch == 8192) {
     const size_t smem = static_cast<size_t>(8192 + 8192 / 32) * sizeof(double);
-    RP_CUDA(cudaFuncSetAttribute(fwht_chunk8192_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+    ensure_dynamic_smem(fwht_chunk8192_kernel, smem);
     fwht_chunk8192_kernel<<<static_cast<unsigned>(f.d * (f.npad / ch)), kFwhtChunkThreads, smem, stream>>>(f, qb > 0);
     RP_LAUNCH_CHECK();
     return;
   }
   const size_t smem = static_cast<size_t>(ch) * sizeof(double);
-  RP_CUDA(cudaFuncSetAttribute(fwht_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  ensure_dynamic_smem(fwht_chunk_kernel, smem);
   fwht_chunk_kernel<<<static_cast<unsigned>(f.d * (f.npad / ch)), kFwhtChunkThreads, smem, stream>>>(f, ch, qb > 0);
   RP_LAUNCH_CHECK();
 }
@@ -417,7 +416,7 @@ void launch_fwht(FwhtArgs f, int bits, cudaStream_t stream) {
   const int64_t blocks = f.d * (f.npad >> (bits + logW + logG));
   const int smem = (S << (logW + logG)) * 8;
   auto go = [&](auto kern) {
-    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ensure_dynamic_smem(kern, smem);
     kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(f);
     RP_LAUNCH_CHECK();
   };

@@ -69,3 +69,27 @@ def test_concurrent_contexts(rp, oracle):
     for res in got:
         for p, q in zip(res.points, want.points):
             assert np.array_equal(p.solution, q.solution)
+
+
+def test_kernel_smem_limits_survive_other_threads(rp, ctx, oracle):
+    """A kernel's dynamic shared-memory limit is per function and device, shared
+    by every thread: a thread launching the fused column pass with a small
+    operator must not lower the limit a larger operator's launch in another
+    thread needs (regression: a per-thread cache of the limit let exactly that
+    happen and the large launch failed with "invalid argument")."""
+    import threading
+
+    rng = np.random.default_rng(5)
+    big = rng.standard_normal((4096, 1024))
+    small = rng.standard_normal((4096, 64))
+
+    def colpass(a, c):
+        y = np.random.default_rng(a.shape[1]).standard_normal(a.shape[0])
+        got = rp.apply_transpose(a, y, ctx=c)
+        assert np.allclose(got, a.T @ y, rtol=1e-12, atol=1e-9)
+
+    colpass(big, ctx)  # raises the limit (main thread)
+    t = threading.Thread(target=colpass, args=(small, rp.Context(0)))  # another thread, smaller need
+    t.start()
+    t.join()
+    colpass(big, ctx)  # still launches
