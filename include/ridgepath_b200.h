@@ -256,8 +256,10 @@ RP_API rp_status rp_interval_split(double lambda_min, double lambda_max, int32_t
  * nullable) are PathPoint::iterations / ::seconds; setup_total (host, 2
  * entries, nullable) receives RegPathResult setup_seconds and total_seconds.
  * Iteration caps and divergence raise RP_ESOLVER (SolverError) as in the
- * reference; direct_path's failed Cholesky is RP_ESOLVER too.  svd_path (a
- * thin SVD of A itself) is not provided. */
+ * reference; direct_path's failed Cholesky is RP_ESOLVER too.
+ * rp_svd_path replaces svd_path (baselines.hpp:15, baselines.cpp:51-78): the
+ * thin SVD of A as a Householder QR + SVD of the triangular factor (cuSOLVER,
+ * loaded at run time), one process only (RP_EINVAL with a communicator). */
 RP_API rp_status rp_warm_cg_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
                                  int32_t* iterations, double* seconds, double* setup_total);
 RP_API rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, const rp_sketch_spec* spec,
@@ -265,6 +267,8 @@ RP_API rp_status rp_warm_ihs_path(rp_ctx* ctx, const double* b, const rp_path_co
                                   double* seconds, double* setup_total);
 RP_API rp_status rp_direct_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
                                 double* seconds, double* setup_total);
+RP_API rp_status rp_svd_path(rp_ctx* ctx, const double* b, const rp_path_config* cfg, double* x_out, int where,
+                             double* seconds, double* setup_total);
 
 /* ---- adaptive sketch dimension (adaptive.hpp; adaptive.cpp:19-137) --------
  * AdaptiveConfig / AdaptiveStep / AdaptiveResult; m_initial, m_cap = 0 select

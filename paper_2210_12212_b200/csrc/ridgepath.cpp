@@ -13,6 +13,7 @@
 // sequential products.  The Gram operator is either a pass over the data
 // (M^T (M W), two DMMA GEMMs or two sparse products) or, when cheaper, the
 // precomputed Gram matrix G = M^T M (one DMMA SYRK) applied as G W.
+#include <cusolverDn.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -2247,6 +2248,179 @@ void run_direct(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out,
   run.total_seconds = host_seconds_since(t_total);
 }
 
+// ---- cuSOLVER, loaded at run time (svd_path's dense QR and SVD) -------------
+// A plain library factorization, like cuBLAS for a plain GEMM: svd_path is a
+// comparison baseline, not the hot path.  Loaded on first use so the library
+// keeps no link-time dependency on a specific cuSOLVER.
+struct CusolverApi {
+  void* lib = nullptr;
+  decltype(&cusolverDnCreate) Create = nullptr;
+  decltype(&cusolverDnDestroy) Destroy = nullptr;
+  decltype(&cusolverDnSetStream) SetStream = nullptr;
+  decltype(&cusolverDnDgeqrf_bufferSize) GeqrfSize = nullptr;
+  decltype(&cusolverDnDgeqrf) Geqrf = nullptr;
+  decltype(&cusolverDnDormqr_bufferSize) OrmqrSize = nullptr;
+  decltype(&cusolverDnDormqr) Ormqr = nullptr;
+  decltype(&cusolverDnDgesvd_bufferSize) GesvdSize = nullptr;
+  decltype(&cusolverDnDgesvd) Gesvd = nullptr;
+};
+
+CusolverApi& cusolver() {
+  static CusolverApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libcusolver.so.11", "libcusolver.so", "/usr/local/cuda/lib64/libcusolver.so.11"}) {
+      api.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (api.lib) break;
+    }
+    if (!api.lib) return;
+    auto sym = [](const char* n) { return dlsym(api.lib, n); };
+    api.Create = reinterpret_cast<decltype(api.Create)>(sym("cusolverDnCreate"));
+    api.Destroy = reinterpret_cast<decltype(api.Destroy)>(sym("cusolverDnDestroy"));
+    api.SetStream = reinterpret_cast<decltype(api.SetStream)>(sym("cusolverDnSetStream"));
+    api.GeqrfSize = reinterpret_cast<decltype(api.GeqrfSize)>(sym("cusolverDnDgeqrf_bufferSize"));
+    api.Geqrf = reinterpret_cast<decltype(api.Geqrf)>(sym("cusolverDnDgeqrf"));
+    api.OrmqrSize = reinterpret_cast<decltype(api.OrmqrSize)>(sym("cusolverDnDormqr_bufferSize"));
+    api.Ormqr = reinterpret_cast<decltype(api.Ormqr)>(sym("cusolverDnDormqr"));
+    api.GesvdSize = reinterpret_cast<decltype(api.GesvdSize)>(sym("cusolverDnDgesvd_bufferSize"));
+    api.Gesvd = reinterpret_cast<decltype(api.Gesvd)>(sym("cusolverDnDgesvd"));
+  });
+  if (!api.lib || !api.Create || !api.Geqrf || !api.Ormqr || !api.Gesvd)
+    throw CudaFailure("svd_path: cuSOLVER (libcusolver.so.11) could not be loaded");
+  return api;
+}
+
+void cusolver_check(cusolverStatus_t st, const char* what) {
+  if (st != CUSOLVER_STATUS_SUCCESS) throw CudaFailure(std::string(what) + ": cuSOLVER status " + std::to_string(st));
+}
+
+// svd_path (baselines.cpp:51-78): one thin SVD of A, then for every lambda
+// x = V diag(sigma / (sigma^2 + lambda)) U^T b.  The thin SVD is formed as a
+// Householder QR of A (or of A^T when n < d) followed by the SVD of the small
+// triangular factor -- A = Q R, R = U_R S V^T, so U^T b = U_R^T (Q^T b)[0:d] --
+// which is backward stable in A like the reference's JacobiSVD.  All T
+// solutions come out of one GEMM V Z, Z = the scaled r x T matrix.
+void run_svd(rp_ctx* ctx, const double* b, const PathCfg& cfg, double* x_out, BaselineRun& run) {
+  cudaStream_t s = ctx->stream;
+  const auto t_total = std::chrono::steady_clock::now();
+  require(ctx->world == 1, "svd_path: needs the whole operator on one device");
+  const OpView op = op_primal(ctx);
+  const int64_t n = op.n_loc, d = op.d, r = std::min(n, d);
+  const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
+  require(n < (int64_t{1} << 31) && d < (int64_t{1} << 31) && n * d * 8.0 <= 64.0 * (1ull << 30),
+          "svd_path: A exceeds the dense factorization limits");
+  CusolverApi& cs = cusolver();
+  cusolverDnHandle_t h = nullptr;
+  cusolver_check(cs.Create(&h), "cusolverDnCreate");
+  struct HandleGuard {
+    CusolverApi& cs;
+    cusolverDnHandle_t h;
+    ~HandleGuard() { cs.Destroy(h); }
+  } guard{cs, h};
+  cusolver_check(cs.SetStream(h, s), "cusolverDnSetStream");
+  const bool tall = n >= d;
+  // F: the matrix whose QR is taken -- A (n x d) when tall, else A^T (d x n).
+  const int64_t fm = tall ? n : d, fn = r;
+  DBuf<double> F(static_cast<size_t>(fm * fn), s);
+  if (tall) {
+    densify(op, F.get(), n, s);
+  } else {
+    DBuf<double> a(static_cast<size_t>(n * d), s);
+    densify(op, a.get(), n, s);
+    transpose(a.get(), n, d, n, F.get(), d, s);
+  }
+  DBuf<double> tau(static_cast<size_t>(r), s);
+  DBuf<int> info(1, s);
+  int lwork = 0;
+  cusolver_check(cs.GeqrfSize(h, static_cast<int>(fm), static_cast<int>(fn), F.get(), static_cast<int>(fm), &lwork),
+                 "geqrf_bufferSize");
+  int lw_svd = 0;
+  cusolver_check(cs.GesvdSize(h, static_cast<int>(r), static_cast<int>(r), &lw_svd), "gesvd_bufferSize");
+  DBuf<double> work(static_cast<size_t>(std::max(lwork, lw_svd) + 1), s);
+  cusolver_check(cs.Geqrf(h, static_cast<int>(fm), static_cast<int>(fn), F.get(), static_cast<int>(fm), tau.get(),
+                          work.get(), std::max(lwork, lw_svd), info.get()),
+                 "geqrf");
+  // the r x r triangle: R (tall) or R^T (wide: A = R^T Q^T)
+  DBuf<double> tri(static_cast<size_t>(r * r), s), R(static_cast<size_t>(r * r), s);
+  upper_triangle(F.get(), fm, r, tall ? R.get() : tri.get(), s);
+  if (!tall) transpose(tri.get(), r, r, r, R.get(), r, s);
+  DBuf<double> sigma(static_cast<size_t>(r), s), U(static_cast<size_t>(r * r), s), VT(static_cast<size_t>(r * r), s),
+      rwork(static_cast<size_t>(r), s);
+  cusolver_check(cs.Gesvd(h, 'A', 'A', static_cast<int>(r), static_cast<int>(r), R.get(), static_cast<int>(r),
+                          sigma.get(), U.get(), static_cast<int>(r), VT.get(), static_cast<int>(r), work.get(),
+                          std::max(lwork, lw_svd), rwork.get(), info.get()),
+                 "gesvd");
+  int hinfo = 0;
+  RP_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  // U^T b: tall -> U_R^T (Q^T b)[0:r]; wide -> U^T b (A = U S (Q W)^T)
+  DBuf<double> qb(static_cast<size_t>(n), s), utb(static_cast<size_t>(r), s);
+  RP_CUDA(cudaMemcpyAsync(qb.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (tall) {
+    int lw_q = 0;
+    cusolver_check(cs.OrmqrSize(h, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, static_cast<int>(n), 1, static_cast<int>(r), F.get(),
+                                static_cast<int>(n), tau.get(), qb.get(), static_cast<int>(n), &lw_q),
+                   "ormqr_bufferSize");
+    DBuf<double> wq(static_cast<size_t>(lw_q + 1), s);
+    cusolver_check(cs.Ormqr(h, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, static_cast<int>(n), 1, static_cast<int>(r), F.get(),
+                            static_cast<int>(n), tau.get(), qb.get(), static_cast<int>(n), wq.get(), lw_q, info.get()),
+                   "ormqr");
+  }
+  {
+    GemmArgs g;  // utb = U^T qb[0:r]
+    g.opa = Op::T;
+    g.m = r;
+    g.n = 1;
+    g.k = r;
+    g.a = U.get();
+    g.lda = r;
+    g.b = qb.get();
+    g.ldb = r;
+    g.c = utb.get();
+    g.ldc = r;
+    dgemm(g, s);
+  }
+  RP_CUDA(cudaStreamSynchronize(s));
+  if (hinfo != 0) throw SolverFailure("svd_path: the SVD did not converge");
+  run.setup_seconds = host_seconds_since(t_total);
+  const auto t_eval = std::chrono::steady_clock::now();
+  DBuf<double> lam(static_cast<size_t>(T), s), Z(static_cast<size_t>(r * T), s);
+  RP_CUDA(cudaMemcpyAsync(lam.get(), cfg.lambdas.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
+  svd_scale(sigma.get(), utb.get(), r, lam.get(), T, Z.get(), s);
+  GemmArgs g;  // x = V_R Z (tall) or W Z, then Q (wide)
+  g.opa = Op::T;
+  g.m = r;
+  g.n = T;
+  g.k = r;
+  g.a = VT.get();
+  g.lda = r;
+  g.b = Z.get();
+  g.ldb = r;
+  g.ldc = d;
+  if (tall) {
+    g.c = x_out;
+    dgemm(g, s);
+  } else {
+    fill(x_out, d * T, 0.0, s);
+    g.c = x_out;
+    dgemm(g, s);
+    int lw_q = 0;
+    cusolver_check(cs.OrmqrSize(h, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, static_cast<int>(d), static_cast<int>(T),
+                                static_cast<int>(r), F.get(), static_cast<int>(d), tau.get(), x_out,
+                                static_cast<int>(d), &lw_q),
+                   "ormqr_bufferSize");
+    DBuf<double> wq(static_cast<size_t>(lw_q + 1), s);
+    cusolver_check(cs.Ormqr(h, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, static_cast<int>(d), static_cast<int>(T),
+                            static_cast<int>(r), F.get(), static_cast<int>(d), tau.get(), x_out, static_cast<int>(d),
+                            wq.get(), lw_q, info.get()),
+                   "ormqr");
+  }
+  RP_CUDA(cudaStreamSynchronize(s));
+  const double secs = host_seconds_since(t_eval) / static_cast<double>(std::max<int64_t>(T, 1));
+  run.iterations.assign(static_cast<size_t>(T), 0);
+  run.seconds.assign(static_cast<size_t>(T), secs);
+  run.total_seconds = host_seconds_since(t_total);
+}
+
 // adaptive_sketch_dim (adaptive.cpp:53-135): sketched Newton steps at
 // lambda_min with Armijo backtracking, doubling m under a fresh seed when the
 // progress measure d.grad stalls.  Every vector lives on the device; the
@@ -2439,6 +2613,22 @@ rp_status rp_adaptive_sketch_dim(rp_ctx* ctx, const double* b, double lambda_min
     out.finish();
     if (trace)
       for (int64_t i = 0; i < std::min<int64_t>(trace_cap, static_cast<int64_t>(tr.size())); ++i) trace[i] = tr[i];
+  });
+}
+
+rp_status rp_svd_path(rp_ctx* ctx, const double* b, const rp_path_config* cfgp, double* x_out, int where,
+                      double* seconds, double* setup_total) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    const PathCfg cfg = to_cfg(cfgp);
+    cfg.validate();
+    const OpView op = op_primal(ctx);
+    InBuf bb(b, static_cast<size_t>(op.n_loc), where, ctx->stream);
+    OutBuf out(x_out, static_cast<size_t>(op.d * cfg.lambdas.size()), where, ctx->stream);
+    BaselineRun run;
+    run_svd(ctx, bb.ptr, cfg, out.dev, run);
+    out.finish();
+    finish_baseline(run, nullptr, seconds, setup_total);
   });
 }
 

@@ -190,4 +190,37 @@ void cg_direction(double* p, const double* r, const double* rr_next, const doubl
   RP_LAUNCH_CHECK();
 }
 
+__global__ void upper_triangle_kernel(const double* __restrict__ a, int64_t lda, int64_t r, double* __restrict__ out) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < r * r;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % r, j = idx / r;
+    out[idx] = i <= j ? a[i + j * lda] : 0.0;
+  }
+}
+
+void upper_triangle(const double* a, int64_t lda, int64_t r, double* out, cudaStream_t s) {
+  if (r <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(r * r, 256), 148 * 16));
+  upper_triangle_kernel<<<blocks, 256, 0, s>>>(a, lda, r, out);
+  RP_LAUNCH_CHECK();
+}
+
+__global__ void svd_scale_kernel(const double* __restrict__ sigma, const double* __restrict__ utb, int64_t r,
+                                 const double* __restrict__ lambda, int64_t T, double* __restrict__ z) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < r * T;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % r, t = idx / r;
+    const double sg = sigma[i];
+    z[idx] = __ddiv_rn(__dmul_rn(sg, utb[i]), __dadd_rn(__dmul_rn(sg, sg), lambda[t]));
+  }
+}
+
+void svd_scale(const double* sigma, const double* utb, int64_t r, const double* lambda, int64_t T, double* z,
+               cudaStream_t s) {
+  if (r <= 0 || T <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(r * T, 256), 148 * 16));
+  svd_scale_kernel<<<blocks, 256, 0, s>>>(sigma, utb, r, lambda, T, z);
+  RP_LAUNCH_CHECK();
+}
+
 }  // namespace rpb

@@ -40,5 +40,11 @@ void residual_in_place(double* r, const double* b, int64_t n, cudaStream_t s);
 void mirror_lower(double* g, int64_t n, int64_t ld, cudaStream_t s);
 // out (d x cols, ld d) = columns c0 .. c0+cols-1 of the d x d identity.
 void identity_block(double* out, int64_t d, int64_t cols, int64_t c0, cudaStream_t s);
+// out (r x r, ld r) = upper triangle of a (r x r block at a, ld lda), zeros below.
+void upper_triangle(const double* a, int64_t lda, int64_t r, double* out, cudaStream_t s);
+// svd_path's diagonal solve (baselines.cpp:66-68): z[i, t] = (sigma_i utb_i) / (sigma_i^2 + lambda_t),
+// z is r x T (ld r); no contraction, the reference's operation order.
+void svd_scale(const double* sigma, const double* utb, int64_t r, const double* lambda, int64_t T, double* z,
+               cudaStream_t s);
 
 }  // namespace rpb

@@ -163,6 +163,7 @@ SIGNATURES = {
     "rp_warm_ihs_path": ([_P, _P, ctypes.POINTER(_PathConfig), ctypes.POINTER(_SketchSpec), ctypes.POINTER(_Rho), _P,
                           _INT, _P, _P, _P], _INT),
     "rp_direct_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
+    "rp_svd_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
     "rp_adaptive_sketch_dim": ([_P, _P, _D, ctypes.POINTER(_AdaptiveConfig), ctypes.POINTER(_SketchSpec), _P, _P, _INT,
                                 ctypes.POINTER(_AdaptiveResult), _P, _I64], _INT),
     "rp_last_gemm_profile": ([_P, _P, _P, _P, _I64, _P], _INT),
@@ -844,6 +845,11 @@ def warm_ihs_path(a, b, config: PathConfig, spec: SketchSpec, rho: RhoBounds, ct
 def direct_path(a, b, config: PathConfig, ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
     """baselines.hpp: A^T A once, (A^T A + lambda I)^{-1} A^T b per lambda."""
     return _baseline("direct", lib().rp_direct_path, a, b, config, ctx, a_test, b_test, iterative=False)
+
+
+def svd_path(a, b, config: PathConfig, ctx: Optional[Context] = None, a_test=None, b_test=None) -> RegPathResult:
+    """baselines.hpp: one thin SVD of A, x = V diag(s / (s^2 + lambda)) U^T b per lambda."""
+    return _baseline("svd", lib().rp_svd_path, a, b, config, ctx, a_test, b_test, iterative=False)
 
 
 # ---------------------------------------------------------------------------

@@ -132,3 +132,59 @@ def test_baselines_errors(rp, ctx, oracle):
         rp.warm_ihs_path(a, b, gcfg, rp.SketchSpec("gaussian", 20, 29, 1, 0), rp.RhoBounds.identity(), ctx=ctx)
     with pytest.raises(ValueError):  # unsorted grid (PathConfig::validate)
         rp.direct_path(a, b, rp.PathConfig(0.5, 20.0, [2.0, 1.0], 1e-8), ctx=ctx)
+
+
+# ---- svd_path (baselines.cpp:51-78) -----------------------------------------
+
+
+def test_svd_path_scalar_kat(rp, ctx, oracle):  # the 1 x 1 case of test_oracle_pins: x = 2*4 / (4 + lambda)
+    got = rp.svd_path(np.array([[2.0]]), np.array([4.0]), rp.PathConfig(1.0, 1e7, [1.0, 1e7], 1e-8), ctx=ctx)
+    assert got.solver == "svd"
+    assert got.points[0].solution[0, 0] == pytest.approx(8.0 / 5.0, rel=1e-15)
+    assert got.points[1].solution[0, 0] == pytest.approx(8.0 / (4.0 + 1e7), rel=1e-15)
+
+
+@pytest.mark.parametrize("rows,cols", [(200, 24), (24, 200), (64, 64), (1, 5)])
+def test_svd_path_tall_wide_square(rp, ctx, oracle, rows, cols):
+    a, b = _ab(oracle, rows + cols, rows, cols)
+    gcfg, ocfg = _cfgs(rp, oracle, 1e-3, 1e3, oracle.log_grid(1e-3, 1e3, 25), 1e-8)
+    got = rp.svd_path(a, b, gcfg, ctx=ctx)
+    _same(got, oracle.svd_path(a, b, ocfg), oracle, 1e-10, iters=False)
+    for p in got.points:
+        assert oracle.rel_error(p.solution[:, 0], oracle.ridge_solve_oracle(a, b, p.lam)) < 1e-9
+        tr, _ = oracle.losses(a, b, p.solution[:, 0], p.lam)
+        assert p.train_loss == pytest.approx(tr, rel=1e-10)
+
+
+def test_svd_path_rank_deficient_and_csr(rp, ctx, oracle):
+    a, b = _ab(oracle, 9, 120, 10)
+    a = np.hstack([a, a[:, :4]])  # 14 columns, rank 10: zero singular values
+    gcfg, ocfg = _cfgs(rp, oracle, 0.01, 100.0, oracle.log_grid(0.01, 100.0, 9), 1e-8)
+    _same(rp.svd_path(a, b, gcfg, ctx=ctx), oracle.svd_path(a, b, ocfg), oracle, 1e-10, iters=False)
+    rng = np.random.default_rng(12)
+    dense = np.where(rng.random((300, 40)) < 0.2, rng.standard_normal((300, 40)), 0.0)
+    c = oracle.Csr.from_dense(dense)
+    gc = rp.Csr(c.rows, c.cols, c.offsets, c.indices, c.values)
+    bb = rng.standard_normal(300)
+    _same(rp.svd_path(gc, bb, gcfg, ctx=ctx), oracle.svd_path(c, bb, ocfg), oracle, 1e-10, iters=False)
+
+
+def test_svd_path_c1_full_size(rp, ctx, oracle):
+    """C1 (the reference's CPU-runnable config) at full size: the device thin SVD
+    path against the oracle's LAPACK SVD."""
+    import workloads
+
+    w = workloads.get("c1")
+    grid = list(w.lambdas(oracle.log_grid))
+    gcfg, ocfg = _cfgs(rp, oracle, w.lambda_min, w.lambda_max, grid, w.epsilon)
+    b = np.ravel(w.b)
+    got = rp.svd_path(w.a, b, gcfg, ctx=ctx)
+    _same(got, oracle.svd_path(w.a, b, ocfg), oracle, 1e-10, iters=False)
+
+
+def test_svd_path_errors(rp, ctx, oracle):
+    a, b = _ab(oracle, 3, 30, 8)
+    with pytest.raises(ValueError):
+        rp.svd_path(a, b[:-1], rp.PathConfig(0.5, 20.0, [1.0], 1e-8), ctx=ctx)
+    with pytest.raises(ValueError):  # unsorted grid (PathConfig::validate)
+        rp.svd_path(a, b, rp.PathConfig(0.5, 20.0, [2.0, 1.0], 1e-8), ctx=ctx)

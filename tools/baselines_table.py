@@ -34,12 +34,14 @@ def main():
     ctx.set_operator(w.a)
     rows = {}
     ref = None
-    for solver in ("ihs-bin", "direct", "warm-ihs", "warm-cg"):
+    for solver in ("ihs-bin", "direct", "svd", "warm-ihs", "warm-cg"):
         t0 = time.perf_counter()
         if solver == "ihs-bin":
             r = rp.ihs_bin_path(w.a, b, cfg, spec, rho, ctx=ctx)
         elif solver == "direct":
             r = rp.direct_path(w.a, b, cfg, ctx=ctx)
+        elif solver == "svd":
+            r = rp.svd_path(w.a, b, cfg, ctx=ctx)
         elif solver == "warm-ihs":
             r = rp.warm_ihs_path(w.a, b, cfg, spec, rho, ctx=ctx)
         else:
