@@ -57,7 +57,8 @@ typedef enum {
   RP_ESVD = 4,
   RP_ECUDA = 5,
   RP_ENCCL = 6,
-  RP_ENOMEM = 7
+  RP_ENOMEM = 7,
+  RP_EPARSE = 8 /* ParseError (data_io.hpp): rp_last_error(NULL) = "line L, column C: ..." */
 } rp_status;
 
 enum { RP_HOST = 0, RP_DEVICE = 1, RP_HOST_STREAM = 2 };
@@ -357,6 +358,26 @@ RP_API rp_status rp_srht_draws(rp_ctx* ctx, const rp_sketch_spec* spec, double* 
 
 /* Host-only self-check of the jump-ahead engine: 0 on success. */
 RP_API int rp_mt_selfcheck(uint64_t seed, uint64_t offset);
+
+/* ---- data formats either side of the path (data_io.hpp; data_io.cpp) ------
+ * rp_libsvm_parse replaces parse_libsvm (data_io.cpp:50-127) on an in-memory
+ * text of `len` bytes: call once with NULL arrays for rows / cols / nnz, then
+ * with offsets (rows + 1), col_indices (nnz, 0-based), values (nnz) and labels
+ * (rows).  feature_override < 0 = none (cols = max index), else the declared
+ * dimension (RP_EINVAL if below the max index).  Malformed input returns
+ * RP_EPARSE with the 1-based line / column in err_line / err_col (nullable).
+ * rp_write_csv replaces write_csv (data_io.cpp:344-364): results r = 0 ..
+ * nresults-1 with npoints[r] points each, the point arrays concatenated in
+ * result order; rows sorted stably by lambda then solver name, 17 significant
+ * digits, empty test_loss where has_test[i] == 0 (has_test nullable = none).
+ * *needed = bytes incl. the terminating NUL; out (cap bytes) may be NULL. */
+RP_API rp_status rp_libsvm_parse(const char* text, int64_t len, int64_t feature_override, int64_t* rows,
+                                 int64_t* cols, int64_t* nnz, int64_t* offsets, int64_t* col_indices, double* values,
+                                 double* labels, int64_t* err_line, int64_t* err_col);
+RP_API rp_status rp_write_csv(int64_t nresults, const char* const* solvers, const int64_t* npoints,
+                              const double* lambdas, const double* train_loss, const double* test_loss,
+                              const uint8_t* has_test, const double* seconds, char* out, int64_t cap,
+                              int64_t* needed);
 
 #ifdef __cplusplus
 }

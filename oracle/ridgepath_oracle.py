@@ -1116,3 +1116,97 @@ def rel_error(got, want) -> float:
     if denom == 0.0:
         return float(np.linalg.norm(got))
     return float(np.linalg.norm(np.asarray(got) - np.asarray(want)) / denom)
+
+
+# ---- data_io.cpp: LIBSVM and CSV (host formats either side of the path) ----
+
+
+class ParseError(RuntimeError):
+    """data_io.hpp ParseError (data_io.cpp:41-48): 'line L, column C: ...'."""
+
+    def __init__(self, msg, line, column):
+        super().__init__(f"line {line}, column {column}: {msg}")
+        self.line, self.column = line, column
+
+
+_C_SPACE = " \t\n\v\f\r"
+
+
+def _parse_real(tok, line, col):
+    """parse_real (data_io.cpp:23-39): std::stod on the whole token, finite only.
+    (Python's float() stands in for strtod on decimal input; hex floats and
+    ERANGE underflow are the C side's.)"""
+    import re
+
+    m = re.match(r"[+-]?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?|inf(?:inity)?|nan)", tok, re.IGNORECASE)
+    if not m:  # strtod converts nothing
+        raise ParseError(f"malformed number '{tok}'", line, col)
+    if m.end() != len(tok):  # strtod stops early: std::stod's `used` falls short
+        raise ParseError(f"trailing characters in number '{tok}'", line, col)
+    v = float(m.group(0))
+    if not math.isfinite(v):
+        raise ParseError(f"non-finite value '{tok}'", line, col)
+    return v
+
+
+def parse_libsvm(text, feature_override=None):
+    """parse_libsvm (data_io.cpp:50-127) -> (Csr, labels)."""
+    offsets, cols, vals, labels = [0], [], [], []
+    max_index = 0
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    for line_no, raw in enumerate(lines, start=1):
+        line = raw.split("#", 1)[0]
+        pos = 0
+
+        def token():
+            nonlocal pos
+            while pos < len(line) and line[pos] in _C_SPACE:
+                pos += 1
+            start = pos
+            while pos < len(line) and line[pos] not in _C_SPACE:
+                pos += 1
+            return line[start:pos], start + 1
+
+        lab, lcol = token()
+        if not lab:
+            continue
+        labels.append(_parse_real(lab, line_no, lcol))
+        prev = 0
+        while True:
+            tok, col = token()
+            if not tok:
+                break
+            colon = tok.find(":")
+            if colon <= 0 or colon + 1 == len(tok):
+                raise ParseError(f"expected index:value, got '{tok}'", line_no, col)
+            part = tok[:colon]
+            if not (part.isdigit() or (part[:1] == "-" and part[1:].isdigit())) or not part.isascii():
+                raise ParseError(f"malformed feature index '{part}'", line_no, col)
+            idx = int(part)
+            if idx < 1:
+                raise ParseError(f"feature index must be >= 1, got {idx}", line_no, col)
+            if idx <= prev:
+                raise ParseError(f"non-increasing feature index {idx}", line_no, col)
+            vals.append(_parse_real(tok[colon + 1:], line_no, col + colon + 1))
+            cols.append(idx - 1)
+            prev = idx
+            max_index = max(max_index, idx)
+        offsets.append(len(vals))
+    if feature_override is not None and feature_override < max_index:
+        raise ValueError(f"parse_libsvm: declared dimension {feature_override} below max index {max_index}")
+    ncols = max_index if feature_override is None else feature_override
+    return (Csr(len(labels), ncols, np.asarray(offsets, dtype=np.int64), np.asarray(cols, dtype=np.int64),
+                np.asarray(vals, dtype=np.float64)), np.asarray(labels, dtype=np.float64))
+
+
+def write_csv(results):
+    """write_csv (data_io.cpp:344-364) -> str."""
+    rows = [(p.lam, r.solver, p) for r in results for p in r.points]
+    rows.sort(key=lambda t: (t[0], t[1].encode()))  # (Python's sort is stable, like std::stable_sort)
+    out = ["lambda,train_loss,test_loss,time_s,solver\n"]
+    for lam, solver, p in rows:
+        test = "%.17g" % p.test_loss if getattr(p, "test_loss", None) is not None else ""
+        out.append(f"{'%.17g' % lam},{'%.17g' % p.train_loss},{test},{'%.17g' % p.seconds},{solver}\n")
+    return "".join(out)

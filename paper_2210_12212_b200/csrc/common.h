@@ -30,6 +30,11 @@ struct FactorFailure : std::runtime_error {
 struct CudaFailure : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// ParseError (data_io.hpp): message "line L, column C: ...", 1-based position.
+struct ParseFailure : std::runtime_error {
+  ParseFailure(const std::string& msg, int64_t l, int64_t c) : std::runtime_error(msg), line(l), column(c) {}
+  int64_t line, column;
+};
 struct NcclFailure : std::runtime_error {
   using std::runtime_error::runtime_error;
 };

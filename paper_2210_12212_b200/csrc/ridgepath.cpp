@@ -19,6 +19,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <string_view>
+#include <cerrno>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1294,6 +1297,9 @@ rp_status guarded(rp_ctx* ctx, F&& f) {
     }
     f();
     return RP_OK;
+  } catch (const ParseFailure& e) {
+    if (!ctx) g_err_noctx = e.what();
+    return status_of(ctx, e, RP_EPARSE);
   } catch (const InvalidArgument& e) {
     if (!ctx) g_err_noctx = e.what();
     return status_of(ctx, e, RP_EINVAL);
@@ -1311,6 +1317,7 @@ rp_status guarded(rp_ctx* ctx, F&& f) {
     const bool oom = std::string(e.what()).find("allocation") != std::string::npos;
     return status_of(ctx, e, oom ? RP_ENOMEM : RP_ECUDA);
   } catch (const std::invalid_argument& e) {
+    if (!ctx) g_err_noctx = e.what();
     return status_of(ctx, e, RP_EINVAL);
   } catch (const std::exception& e) {
     if (!ctx) g_err_noctx = e.what();
@@ -2880,6 +2887,162 @@ int rp_mt_selfcheck(uint64_t seed, uint64_t offset) {
   } catch (...) {
     return 2;
   }
+}
+
+// ---- data formats either side of the path (data_io.cpp) ----------------------
+
+namespace {
+
+// parse_real (data_io.cpp:23-39): std::stod semantics -- strtod on the whole
+// token, ERANGE (overflow or underflow) is "out of range", then finite only.
+double libsvm_real(const std::string& tok, int64_t line, int64_t col) {
+  auto fail = [&](const std::string& what) -> double {
+    throw ParseFailure("line " + std::to_string(line) + ", column " + std::to_string(col) + ": " + what, line, col);
+  };
+  const char* b = tok.c_str();
+  char* end = nullptr;
+  errno = 0;
+  const double v = std::strtod(b, &end);
+  if (end == b) return fail("malformed number '" + tok + "'");
+  if (errno == ERANGE) return fail("number out of range '" + tok + "'");
+  if (static_cast<size_t>(end - b) != tok.size()) return fail("trailing characters in number '" + tok + "'");
+  if (!std::isfinite(v)) return fail("non-finite value '" + tok + "'");
+  return v;
+}
+
+struct Libsvm {
+  std::vector<int64_t> offsets{0}, cols;
+  std::vector<double> values, labels;
+  int64_t max_index = 0;
+};
+
+// parse_libsvm (data_io.cpp:50-127): one record per line; '#' starts a
+// comment; blank lines are skipped; "label idx:value ..." with 1-based,
+// strictly increasing indices.  Errors carry 1-based line and column.
+Libsvm parse_libsvm_text(const char* text, int64_t len) {
+  Libsvm out;
+  int64_t line_no = 0;
+  int64_t pos0 = 0;
+  auto is_space = [](char c) { return std::isspace(static_cast<unsigned char>(c)) != 0; };
+  while (pos0 < len) {
+    int64_t eol = pos0;
+    while (eol < len && text[eol] != '\n') ++eol;
+    ++line_no;
+    std::string_view line(text + pos0, static_cast<size_t>(eol - pos0));
+    pos0 = eol + 1;
+    if (const auto hash = line.find('#'); hash != std::string_view::npos) line = line.substr(0, hash);
+    size_t pos = 0;
+    auto next_token = [&](int64_t* col) {
+      while (pos < line.size() && is_space(line[pos])) ++pos;
+      const size_t start = pos;
+      while (pos < line.size() && !is_space(line[pos])) ++pos;
+      *col = static_cast<int64_t>(start) + 1;
+      return std::string(line.substr(start, pos - start));
+    };
+    int64_t col = 0;
+    const std::string label = next_token(&col);
+    if (label.empty()) continue;
+    out.labels.push_back(libsvm_real(label, line_no, col));
+    int64_t prev = 0;
+    for (;;) {
+      const std::string tok = next_token(&col);
+      if (tok.empty()) break;
+      auto fail = [&](const std::string& what) {
+        throw ParseFailure("line " + std::to_string(line_no) + ", column " + std::to_string(col) + ": " + what,
+                           line_no, col);
+      };
+      const size_t colon = tok.find(':');
+      if (colon == std::string::npos || colon == 0 || colon + 1 == tok.size())
+        fail("expected index:value, got '" + tok + "'");
+      const std::string idx_part = tok.substr(0, colon);
+      int64_t idx = 0;
+      const auto [ptr, ec] = std::from_chars(idx_part.data(), idx_part.data() + idx_part.size(), idx);
+      if (ec != std::errc{} || ptr != idx_part.data() + idx_part.size())
+        fail("malformed feature index '" + idx_part + "'");
+      if (idx < 1) fail("feature index must be >= 1, got " + std::to_string(idx));
+      if (idx <= prev) fail("non-increasing feature index " + std::to_string(idx));
+      const double v = libsvm_real(tok.substr(colon + 1), line_no, col + static_cast<int64_t>(colon) + 1);
+      out.cols.push_back(idx - 1);
+      out.values.push_back(v);
+      prev = idx;
+      out.max_index = std::max(out.max_index, idx);
+    }
+    out.offsets.push_back(static_cast<int64_t>(out.values.size()));
+  }
+  return out;
+}
+
+// format_double (data_io.cpp:338-342)
+std::string format_g17(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+
+}  // namespace
+
+rp_status rp_libsvm_parse(const char* text, int64_t len, int64_t feature_override, int64_t* rows, int64_t* cols,
+                          int64_t* nnz, int64_t* offsets, int64_t* col_indices, double* values, double* labels,
+                          int64_t* err_line, int64_t* err_col) {
+  if (err_line) *err_line = 0;
+  if (err_col) *err_col = 0;
+  return guarded(nullptr, [&] {
+    require(len >= 0 && (text || len == 0) && rows && cols && nnz, "parse_libsvm: null argument");
+    Libsvm p;
+    try {
+      p = parse_libsvm_text(text, len);
+    } catch (const ParseFailure& e) {
+      if (err_line) *err_line = e.line;
+      if (err_col) *err_col = e.column;
+      throw;
+    }
+    if (feature_override >= 0 && feature_override < p.max_index)
+      throw InvalidArgument("parse_libsvm: declared dimension " + std::to_string(feature_override) +
+                            " below max index " + std::to_string(p.max_index));
+    *rows = static_cast<int64_t>(p.labels.size());
+    *cols = feature_override >= 0 ? feature_override : p.max_index;
+    *nnz = static_cast<int64_t>(p.values.size());
+    if (offsets) std::copy(p.offsets.begin(), p.offsets.end(), offsets);
+    if (col_indices) std::copy(p.cols.begin(), p.cols.end(), col_indices);
+    if (values) std::copy(p.values.begin(), p.values.end(), values);
+    if (labels) std::copy(p.labels.begin(), p.labels.end(), labels);
+  });
+}
+
+rp_status rp_write_csv(int64_t nresults, const char* const* solvers, const int64_t* npoints, const double* lambdas,
+                       const double* train_loss, const double* test_loss, const uint8_t* has_test,
+                       const double* seconds, char* out, int64_t cap, int64_t* needed) {
+  return guarded(nullptr, [&] {
+    require(nresults >= 0 && needed && (nresults == 0 || (solvers && npoints)), "write_csv: null argument");
+    struct Row {
+      double lambda;
+      const char* solver;
+      int64_t i;
+    };
+    std::vector<Row> rows;
+    int64_t at = 0;
+    for (int64_t r = 0; r < nresults; ++r) {
+      require(npoints[r] >= 0 && solvers[r], "write_csv: bad result");
+      for (int64_t j = 0; j < npoints[r]; ++j, ++at) rows.push_back({lambdas[at], solvers[r], at});
+    }
+    // (data_io.cpp:353-356: stable, by lambda then solver name)
+    std::stable_sort(rows.begin(), rows.end(), [](const Row& a, const Row& b) {
+      if (a.lambda != b.lambda) return a.lambda < b.lambda;
+      return std::strcmp(a.solver, b.solver) < 0;
+    });
+    std::string s = "lambda,train_loss,test_loss,time_s,solver\n";
+    for (const Row& row : rows) {
+      s += format_g17(row.lambda) + ',' + format_g17(train_loss[row.i]) + ',';
+      if (has_test && has_test[row.i]) s += format_g17(test_loss[row.i]);
+      s += ',' + format_g17(seconds[row.i]) + ',' + row.solver + '\n';
+    }
+    *needed = static_cast<int64_t>(s.size()) + 1;
+    if (out && cap > 0) {
+      const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(out, s.data(), n);
+      out[n] = '\0';
+    }
+  });
 }
 
 }  // extern "C"

@@ -44,6 +44,15 @@ class DeviceError(RuntimeError):
     pass
 
 
+class ParseError(RuntimeError):
+    """data_io.hpp ParseError: "line L, column C: ..." with 1-based .line / .column."""
+
+    def __init__(self, message: str, line: int = 0, column: int = 0):
+        super().__init__(message)
+        self.line = line
+        self.column = column
+
+
 # ---------------------------------------------------------------------------
 # ctypes binding
 # ---------------------------------------------------------------------------
@@ -164,6 +173,8 @@ SIGNATURES = {
                           _INT, _P, _P, _P], _INT),
     "rp_direct_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
     "rp_svd_path": ([_P, _P, ctypes.POINTER(_PathConfig), _P, _INT, _P, _P], _INT),
+    "rp_libsvm_parse": ([ctypes.c_char_p, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
+    "rp_write_csv": ([_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_char_p, _I64, _P], _INT),
     "rp_adaptive_sketch_dim": ([_P, _P, _D, ctypes.POINTER(_AdaptiveConfig), ctypes.POINTER(_SketchSpec), _P, _P, _INT,
                                 ctypes.POINTER(_AdaptiveResult), _P, _I64], _INT),
     "rp_last_gemm_profile": ([_P, _P, _P, _P, _I64, _P], _INT),
@@ -1066,3 +1077,82 @@ def last_device_seconds(ctx: Context) -> float:
 def apply_transpose_raw(ctx: Context, y_ptr: int, ncols: int, out_ptr: int, where: int = RP_DEVICE):
     """rp_apply_transpose on raw pointers: out = A^T y."""
     ctx.check(lib().rp_apply_transpose(ctx.handle, _P(y_ptr), ncols, _P(out_ptr), where))
+
+
+# ---------------------------------------------------------------------------
+# data_io.hpp: the formats either side of the path
+# ---------------------------------------------------------------------------
+
+
+def parse_libsvm(text, feature_override: Optional[int] = None):
+    """parse_libsvm (data_io.cpp:50-127) -> (Csr, labels).  `text` is str or bytes."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    fo = -1 if feature_override is None else int(feature_override)
+    if feature_override is not None and fo < 0:
+        raise ValueError("parse_libsvm: negative feature dimension")
+    rows, cols, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    el, ec = ctypes.c_int64(), ctypes.c_int64()
+    L = lib()
+
+    def call(*arrays):
+        st = L.rp_libsvm_parse(raw, len(raw), fo, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(nnz),
+                               *arrays, ctypes.byref(el), ctypes.byref(ec))
+        if st == 8:
+            raise ParseError(L.rp_last_error(None).decode(), el.value, ec.value)
+        _check(st)
+
+    call(None, None, None, None)
+    off = np.empty(rows.value + 1, dtype=np.int64)
+    idx = np.empty(nnz.value, dtype=np.int64)
+    val = np.empty(nnz.value)
+    lab = np.empty(rows.value)
+    call(_ptr(off), _ptr(idx), _ptr(val), _ptr(lab))
+    return Csr(rows.value, cols.value, off, idx, val), lab
+
+
+def _g17(v: float) -> str:
+    return "%.17g" % float(v)  # format_double (data_io.cpp:338-342)
+
+
+def write_libsvm(a, labels) -> str:
+    """write_libsvm (data_io.cpp:129-149): dense operators go through CSR
+    (explicit zeros dropped); indices 1-based, 17 significant digits."""
+    labels = np.asarray(labels, dtype=np.float64).reshape(-1)
+    if not isinstance(a, Csr):
+        d = np.asarray(a, dtype=np.float64)
+        off, idx, val = [0], [], []
+        for r in range(d.shape[0]):
+            nz = np.nonzero(d[r])[0]
+            idx.extend(nz.tolist())
+            val.extend(d[r, nz].tolist())
+            off.append(len(val))
+        a = Csr(d.shape[0], d.shape[1], np.asarray(off), np.asarray(idx, dtype=np.int64), np.asarray(val))
+    if labels.shape[0] != a.rows:
+        raise ValueError("write_libsvm: label count mismatch")
+    lines = []
+    for r in range(a.rows):
+        parts = [_g17(labels[r])]
+        for p in range(int(a.offsets[r]), int(a.offsets[r + 1])):
+            parts.append(f"{int(a.indices[p]) + 1}:{_g17(a.values[p])}")
+        lines.append(" ".join(parts) + "\n")
+    return "".join(lines)
+
+
+def write_csv(results: List[RegPathResult]) -> str:
+    """write_csv (data_io.cpp:344-364): every point of every result, sorted
+    stably by lambda then solver name, header lambda,train_loss,test_loss,time_s,solver."""
+    names = [r.solver.encode() for r in results]
+    c_names = (ctypes.c_char_p * max(len(names), 1))(*names)
+    npts = np.asarray([len(r.points) for r in results] or [0], dtype=np.int64)
+    pts = [p for r in results for p in r.points]
+    lam = np.asarray([p.lam for p in pts] or [0.0], dtype=np.float64)
+    tr = np.asarray([p.train_loss for p in pts] or [0.0], dtype=np.float64)
+    te = np.asarray([p.test_loss if p.test_loss is not None else 0.0 for p in pts] or [0.0], dtype=np.float64)
+    has = np.asarray([p.test_loss is not None for p in pts] or [0], dtype=np.uint8)
+    sec = np.asarray([p.seconds for p in pts] or [0.0], dtype=np.float64)
+    need = ctypes.c_int64()
+    args = [len(results), ctypes.cast(c_names, _P), _ptr(npts), _ptr(lam), _ptr(tr), _ptr(te), _ptr(has), _ptr(sec)]
+    _check(lib().rp_write_csv(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().rp_write_csv(*args, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
