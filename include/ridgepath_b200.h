@@ -28,8 +28,8 @@
  * one context must come from one host thread.  Distinct contexts hold
  * independent state and may be driven from different threads: calls are
  * synchronous and a per-device lock serializes the calls of contexts that
- * share a GPU (concurrently running TMA GEMMs of two streams were observed to
- * corrupt each other's results, open issue).
+ * share a GPU (a TMA GEMM running next to higher-priority work was observed
+ * to give wrong results, concurrency finding).
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H

@@ -42,8 +42,8 @@ struct GemmArgs {
   // op(A)(i, k) == 0 for k < i (A^T of a lower-triangular matrix): each output
   // tile skips the k range below its first row.  Requires split_k == 1.
   bool tri_k = false;
-  // Use the cp.async kernel instead of the TMA one (concurrent side-stream
-  // products, open issue on concurrent TMA GEMMs).
+  // Use the cp.async kernel instead of the TMA one (A/B switch; the cp.async
+  // pipeline survives preemption by higher-priority work).
   bool no_tma = false;
   // Deterministic split-K factor; 0 = heuristic.  With col_stable the
   // heuristic looks at (m, k) only, so column j of C does not depend on n.

@@ -348,7 +348,7 @@ struct rp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   cudaStream_t side = nullptr;  // low-priority stream: the Gram matrix overlapping the preconditioner build
-  cudaStream_t hi = nullptr;    // high-priority stream: the sketch while the Gram matrix is in flight
+  cudaStream_t hi = nullptr;    // second stream: the sketch while the Gram matrix is in flight
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -358,12 +358,16 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
-  bool gram_overlap_tma = false;  // option "gram_overlap_tma": TMA kernel for the overlapped SYRK (probe)
+  bool gram_overlap_tma = true;   // option "gram_overlap_tma": 0 = cp.async kernel for the overlapped SYRK
+  int gram_overlap_split = 0;     // option "gram_overlap_split": split-K of the overlapped SYRK (0 = auto; probe)
+  bool sketch_on_hi = true;       // option "sketch_on_hi": sketch on its own stream while the SYRK runs
+  // option "stream_priorities": 1 = side stream low, sketch stream high priority.  Off by default: a TMA GEMM
+  // running next to higher-priority work was measured to produce wrong results (concurrency).
+  bool stream_priorities = false;
   // option "gram_overlap": Gram SYRK on a side stream, overlapping the sketch
-  // and the precond build.  The side SYRK runs the cp.async GEMM kernel: two
-  // TMA GEMMs running concurrently on different streams were seen to corrupt
-  // each other (open issue); with the cp.async side SYRK the path
-  // is bit-identical to the single-stream one (tools/race_probe.py).
+  // and the precond build; bit-identical to the single-stream path as long as
+  // the streams share one priority (tools/race_probe.py; DESIGN.md,
+  // concurrency finding).
   bool gram_overlap = true;
   bool gram_after_sketch = false;  // option "gram_after_sketch": start that SYRK after the sketch instead of before
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
@@ -605,7 +609,8 @@ struct GramOp {
     // leave shared memory for the Cholesky chain's kernels on every SM,
     // measured slower than the auto choice: 19.16 vs 18.96 ms on C2)
     if (st && ctx->gram_overlap_tile >= 0) g.force_tile = ctx->gram_overlap_tile;
-    if (st && !ctx->gram_overlap_tma) g.no_tma = true;  // (concurrent TMA GEMMs on two streams: open issue)
+    if (st && !ctx->gram_overlap_tma) g.no_tma = true;
+    if (st && ctx->gram_overlap_split > 0) g.split_k = ctx->gram_overlap_split;
     dgemm(g, s);
     allreduce(ctx, G.get(), op.d * op.d, s);
     matrix = true;
@@ -1064,19 +1069,19 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     if (use_matrix) gram.end_matrix();
   } else {
     // The Gram matrix (a throughput-bound SYRK over A) runs on the context's
-    // low-priority side stream from the start, overlapping the HBM-bound
-    // sketch and the latency-bound preconditioner build; the basis waits for
-    // both.
+    // side stream from the start, overlapping the HBM-bound sketch and the
+    // latency-bound preconditioner build; the basis waits for both.  (All
+    // streams at one priority: with a low-priority side stream, the TMA SYRK
+    // running next to higher-priority work came out wrong -- DESIGN.md.)
     // (single process only: with a communicator the Gram all-reduce would be
     // in flight on a second stream next to the sketch all-reduce)
-    // (only for small Gram matrices: a large SYRK -- C5's 16384^2 -- on the
-    // slower cp.async kernel outlasts what it overlaps)
+    // (only for Gram matrices up to 4096^2, the measured range)
     const bool side_gram = use_matrix && ctx->gram_overlap && !ctx->comm && op.d <= 4096;
     auto launch_side_gram = [&]() {
       if (!ctx->side) {
         int lo = 0, hi = 0;
         RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo));
+        RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, ctx->stream_priorities ? lo : 0));
       }
       RP_CUDA(cudaEventCreateWithFlags(&gram_done, cudaEventDisableTiming));
       RP_CUDA(cudaEventRecord(gram_done, s));
@@ -1086,13 +1091,13 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     };
     if (side_gram && !ctx->gram_after_sketch) launch_side_gram();
     // 1) Sketch (once), summed over ranks.  While the Gram SYRK occupies the
-    //    low-priority side stream, the sketch -- on the critical path to the
-    //    preconditioner -- runs on the context's high-priority stream.
-    if (gram_done) {
+    //    side stream, the sketch -- on the critical path to the
+    //    preconditioner -- runs on a second stream of the context.
+    if (gram_done && ctx->sketch_on_hi) {
       if (!ctx->hi) {
         int lo = 0, hi = 0;
         RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        RP_CUDA(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, hi));
+        RP_CUDA(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, ctx->stream_priorities ? hi : 0));
       }
       cudaEvent_t fork;
       RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1279,8 +1284,8 @@ thread_local std::string g_err_noctx;
 
 // One lock per device, held for the whole of every context call: calls are
 // synchronous, so contexts sharing a GPU never overlap their device work
-// (concurrently running TMA GEMMs of two streams were seen to corrupt each
-// other, DESIGN.md open issue).  Recursive: a call may use another entry point.
+// (a second line of defence next to the single stream priority; DESIGN.md,
+// concurrency finding).  Recursive: a call may use another entry point.
 std::recursive_mutex& device_mutex(int dev) {
   static std::recursive_mutex m[64];
   return m[static_cast<unsigned>(dev) % 64];
@@ -1563,6 +1568,13 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "csr_panel_rows") {
       require(value >= 1 && value < (int64_t{1} << 31), "csr_panel_rows must be in [1, 2^31)");
       ctx->csr_panel_rows = value;
+    } else if (k == "gram_overlap_split") {
+      require(value >= 0 && value <= 64, "gram_overlap_split must be in [0, 64]");
+      ctx->gram_overlap_split = static_cast<int>(value);
+    } else if (k == "stream_priorities") {
+      ctx->stream_priorities = value != 0;
+    } else if (k == "sketch_on_hi") {
+      ctx->sketch_on_hi = value != 0;
     } else if (k == "gram_overlap_tma") {
       ctx->gram_overlap_tma = value != 0;
     } else if (k == "gram_overlap_tile") {

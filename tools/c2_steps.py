@@ -23,6 +23,9 @@ def main():
     a_dev = torch.from_numpy(np.ascontiguousarray(w.a.T)).cuda()
     b_dev = torch.from_numpy(np.ascontiguousarray(w.b.T)).cuda()
     ctx = rp.Context(0)
+    for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=gram_overlap_tma=1
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     rp.set_dense_rows_device(ctx, n, 0, n, d, a_dev.data_ptr(), n)
     grid = w.lambdas(rp.log_grid)

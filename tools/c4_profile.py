@@ -31,6 +31,9 @@ def main():
     b = w.b[:n]
     print(f"data {time.time()-t0:.1f}s  n={n} d={w.meta['d']} nnz={nnz}", flush=True)
     ctx = rp.Context(0)
+    for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=gram_overlap_tma=1
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     grid = rp.log_grid(w.lambda_min, w.lambda_max, w.T)
     cfg = rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon)
     spec = rp.SketchSpec("countsketch", w.sketch["m"], n, 1, 0)
