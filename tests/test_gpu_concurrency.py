@@ -1,0 +1,42 @@
+"""Regression for the concurrency finding: on the full C2 workload
+the overlapped Gram SYRK (TMA kernel on a side stream, next to the sketch and
+the preconditioner build) must give the same bits as the single-stream path.
+With a low-priority side stream next to a high-priority sketch stream it did
+not (x(lambda) off by 1e-2 in most runs), so the default keeps every stream at
+one priority; this test runs the default schedule several times."""
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def test_overlapped_gram_bitwise_c2_full(rp):
+    torch = pytest.importorskip("torch")
+    w = workloads.get("c2")
+    n, d = w.a.shape
+    a_dev = torch.from_numpy(np.ascontiguousarray(w.a.T)).cuda()
+    b_dev = torch.from_numpy(np.ascontiguousarray(w.b.T)).cuda()
+    torch.cuda.synchronize()
+    grid = w.lambdas(rp.log_grid)
+    cfg = rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon)
+    spec = rp.SketchSpec(w.sketch["kind"], w.sketch["m"], w.sketch["n"], w.sketch["s"], w.sketch["seed"])
+    rho = rp.RhoBounds.manual(*w.rho)
+
+    def run(opts, reps):
+        ctx = rp.Context(0)
+        for k, v in opts.items():
+            ctx.set_option(k, v)
+        rp.set_dense_rows_device(ctx, n, 0, n, d, a_dev.data_ptr(), n)
+        out = []
+        for _ in range(reps):
+            x = torch.empty(len(grid) * d, dtype=torch.float64, device="cuda")
+            rp.path_raw(ctx, b_dev.data_ptr(), 1, cfg, spec, rho, x.data_ptr())
+            torch.cuda.synchronize()
+            out.append(x.cpu().numpy())
+        return out
+
+    ref = run({"gram_overlap": 0}, 1)[0]
+    for x in run({}, 4):  # default: overlapped TMA SYRK, single priority
+        assert np.array_equal(x, ref)
