@@ -1296,8 +1296,12 @@ rp_status guarded(rp_ctx* ctx, F&& f) {
   try {
     std::optional<DeviceGuard> guard;
     std::unique_lock<std::recursive_mutex> lock;
+    static const bool no_lock = [] {  // RP_NO_DEVICE_LOCK=1: probe only (tools/concurrency_probe.py)
+      const char* e = std::getenv("RP_NO_DEVICE_LOCK");
+      return e && e[0] == '1';
+    }();
     if (ctx) {
-      lock = std::unique_lock<std::recursive_mutex>(device_mutex(ctx->device));
+      if (!no_lock) lock = std::unique_lock<std::recursive_mutex>(device_mutex(ctx->device));
       guard.emplace(ctx->device);
     }
     f();
