@@ -170,6 +170,20 @@ RP_API rp_status rp_last_gemm_profile(rp_ctx* ctx, double* seconds, double* flop
 RP_API rp_status rp_comm_unique_id(void* id128);
 RP_API rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128);
 
+/* Host-side communicator: the context's collectives run through caller
+ * callbacks on host memory instead of NCCL (an MPI / gloo / shared-memory
+ * transport of the caller's choosing, or several ranks sharing one GPU).  Each
+ * collective synchronizes the context's stream, copies the operand to a pinned
+ * staging buffer, calls the callback from the calling thread and copies the
+ * result back.  A callback returns 0 on success; anything else fails the call
+ * with RP_ENCCL.
+ *   allreduce: buf[0..count) <- sum over ranks, in place;
+ *   allgather: recv[r*count .. (r+1)*count) <- rank r's send[0..count). */
+typedef int (*rp_host_allreduce_fn)(void* user, double* buf, int64_t count);
+typedef int (*rp_host_allgather_fn)(void* user, const double* send, int64_t count, double* recv);
+RP_API rp_status rp_comm_init_host(rp_ctx* ctx, int rank, int world, rp_host_allreduce_fn allreduce,
+                                   rp_host_allgather_fn allgather, void* user);
+
 /* ---- data operator ----------------------------------------------------------
  * Matrix, matrix.hpp:54-73.  The context keeps one operator A (n x d).  With
  * several ranks each passes its shard: rows [row0, row0 + n_local) of the

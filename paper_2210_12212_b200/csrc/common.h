@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -128,7 +129,9 @@ class DBuf {
     }
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, s_);
+    if (p_) {
+      cudaFreeAsync(p_, s_);
+    }
     p_ = nullptr;
     n_ = 0;
   }

@@ -272,19 +272,6 @@ __global__ void shifted_copy_kernel(const double* __restrict__ g, int64_t n, con
   }
 }
 
-// RP_FACTOR_PRIORITIES=1 gives the critical chain a high-priority stream and
-// the trailing updates a low one (0.3 ms faster on C2).  Off by default: TMA
-// GEMMs running next to higher-priority work were measured to produce wrong
-// results (concurrency), so both lookahead streams keep the
-// default priority.
-bool factor_priorities() {
-  static const bool on = [] {
-    const char* e = std::getenv("RP_FACTOR_PRIORITIES");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 // RP_POTRF_DIAG=1 selects the unblocked diagonal kernel (A/B).
 bool blocked_diag() {
   static const bool on = [] {
@@ -318,16 +305,13 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // (one CTA per matrix) overlap the big trailing GEMMs.  All GEMMs here run
   // unsplit, so they share no workspace.
   // The critical chain (diagonal kernels, panel solves, next-column updates)
-  // runs on its own stream (high priority only with RP_FACTOR_PRIORITIES=1,
-  // see factor_priorities) so its CTAs can be scheduled ahead of the
-  // trailing-update CTAs as SMs free up.
+  // runs on its own stream.  Both streams keep the default priority: a
+  // high-priority chain would preempt trailing-update CTAs mid-TMA-pipeline,
+  // which corrupts results (concurrency finding).
   const cudaStream_t user = stream;
-  int prio_lo = 0, prio_hi = 0;
-  RP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   cudaStream_t aux = nullptr, hi = nullptr;
-  if (!factor_priorities()) prio_lo = prio_hi = 0;
-  RP_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, prio_lo));
-  RP_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, prio_hi));
+  RP_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  RP_CUDA(cudaStreamCreateWithFlags(&hi, cudaStreamNonBlocking));
   std::vector<cudaEvent_t> events;
   auto new_event = [&]() {
     cudaEvent_t e;
@@ -424,6 +408,8 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   }
   stream = user;
   for (cudaEvent_t e : events) RP_CUDA(cudaEventDestroy(e));  // (released once complete)
+  release_workspace(aux);  // (the GEMMs above run unsplit; this only guards a recycled handle)
+  release_workspace(hi);
   RP_CUDA(cudaStreamDestroy(aux));
   RP_CUDA(cudaStreamDestroy(hi));
   // 2) Triangular inverse in place.

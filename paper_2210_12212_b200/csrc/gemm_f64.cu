@@ -659,6 +659,21 @@ double* workspace(size_t bytes, cudaStream_t stream) {
   return w.ptr;
 }
 
+}  // namespace
+
+void release_workspace(cudaStream_t stream) {
+  std::lock_guard<std::mutex> lock(g_ws.mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  auto it = g_ws.bufs.find({dev, stream});
+  if (it == g_ws.bufs.end()) return;
+  cudaStreamSynchronize(stream);
+  if (it->second.ptr) cudaFree(it->second.ptr);
+  g_ws.bufs.erase(it);
+}
+
+namespace {
+
 // ---- TMA launch path -------------------------------------------------------------
 
 // RP_GEMM_PDL=0 disables programmatic dependent launch of the TMA GEMM.
@@ -769,6 +784,7 @@ struct TileShape {
 constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128},
                                 {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}, {64, 48}, {128, 48}};
 constexpr int kNumTiles = 13;
+constexpr int kTileBK[kNumTiles] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16};  // (launch_layout)
 
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
@@ -995,6 +1011,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
       if (kTiles[t].bn == 16 && g.n > 16) continue;
       if (kTiles[t].bn == 48 && (g.n <= 32 || g.n > 48)) continue;
       if (kEff[t] <= 0.0) continue;
+      if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;  // (a split's last k tile must not cross into the next)
       const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
       const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));
       const double cost = waves * kTiles[t].bm * kTiles[t].bn * kOcc[t] / kEff[t];
@@ -1004,7 +1021,12 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
       }
     }
   }
-  if (g.force_tile >= 0 && g.force_tile < kNumTiles) tile = g.force_tile;
+  if (g.force_tile >= 0 && g.force_tile < kNumTiles) {
+    // The kernels do not mask k past their split's end: a tile's BK must
+    // divide the K chunk (always true for BK = 16, k_chunk % 16 == 0).
+    require(k_chunk % kTileBK[g.force_tile] == 0, "dgemm: a BK = 32 tile needs a split K chunk that is a multiple of 32");
+    tile = g.force_tile;
+  }
   if (split > 1) kp.ws = workspace(sizeof(double) * static_cast<size_t>(nb * split) * g.m * g.n, stream);
   if (g.epilogue) {
     require(!g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0 && split == 1,

@@ -99,6 +99,11 @@ struct Partials {
 // when null and a split is wanted, an internal cached buffer is used.
 void dgemm(const GemmArgs& g, cudaStream_t stream);
 
+// Frees the split-K workspace cached for `stream` (after synchronizing it).
+// Owners of streams call it before destroying them, so no workspace outlives
+// its stream and a recycled stream handle never inherits a stale entry.
+void release_workspace(cudaStream_t stream);
+
 // The split-K factor dgemm() would use for `g` (1 = no split: a fused
 // epilogue is only allowed then).
 int dgemm_split(const GemmArgs& g);

@@ -181,6 +181,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -198,11 +199,12 @@ NcclApi& nccl() {
       api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
       api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
       api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.handle, "ncclAllGather"));
       api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
     }
   }
-  if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce)
+  if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather)
     throw NcclFailure("NCCL (libnccl.so.2) could not be loaded");
   return api;
 }
@@ -347,11 +349,17 @@ struct rp_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
-  cudaStream_t side = nullptr;  // low-priority stream: the Gram matrix overlapping the preconditioner build
+  cudaStream_t side = nullptr;  // side stream: the Gram matrix overlapping the sketch and the preconditioner build
   cudaStream_t hi = nullptr;    // second stream: the sketch while the Gram matrix is in flight
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  // host-side communicator (rp_comm_init_host): collectives through caller callbacks
+  rp_host_allreduce_fn host_allreduce = nullptr;
+  rp_host_allgather_fn host_allgather = nullptr;
+  void* host_user = nullptr;
+  double* host_stage = nullptr;  // pinned staging buffer of the host collectives
+  size_t host_stage_count = 0;
   int gram_mode = -1;
   bool profile = false;
   double last_device_seconds = 0.0;  // profile: device time of the last product call
@@ -361,9 +369,10 @@ struct rp_ctx {
   bool gram_overlap_tma = true;   // option "gram_overlap_tma": 0 = cp.async kernel for the overlapped SYRK
   int gram_overlap_split = 0;     // option "gram_overlap_split": split-K of the overlapped SYRK (0 = auto; probe)
   bool sketch_on_hi = true;       // option "sketch_on_hi": sketch on its own stream while the SYRK runs
-  // option "stream_priorities": 1 = side stream low, sketch stream high priority.  Off by default: a TMA GEMM
-  // running next to higher-priority work was measured to produce wrong results (concurrency).
-  bool stream_priorities = false;
+  // option "stream_priorities" is rejected: compute preemption (which stream
+  // priorities trigger) of a CTA with TMA copies in flight corrupts results
+  // (concurrency finding; repro tools/tma_race.cu).  Every stream
+  // of the library runs at the default priority.
   // option "gram_overlap": Gram SYRK on a side stream, overlapping the sketch
   // and the precond build; bit-identical to the single-stream path as long as
   // the streams share one priority (tools/race_probe.py; DESIGN.md,
@@ -416,11 +425,61 @@ OpView op_dual(rp_ctx* ctx) {
   return ctx->op.dual();
 }
 
+// True when the context's collectives do something (NCCL or host callbacks).
+bool has_comm(const rp_ctx* ctx) { return ctx->comm != nullptr || ctx->host_allreduce != nullptr; }
+
+double* host_stage(rp_ctx* ctx, size_t count) {
+  if (ctx->host_stage_count < count) {
+    if (ctx->host_stage) RP_CUDA(cudaFreeHost(ctx->host_stage));
+    ctx->host_stage = nullptr;
+    ctx->host_stage_count = 0;
+    RP_CUDA(cudaMallocHost(&ctx->host_stage, count * sizeof(double)));
+    ctx->host_stage_count = count;
+  }
+  return ctx->host_stage;
+}
+
+// Sum over ranks of buf[0..count), in place, stream-ordered on `st` (default:
+// the context's stream).
 void allreduce(rp_ctx* ctx, double* buf, int64_t count, cudaStream_t st = nullptr) {
-  if (!ctx->comm || count <= 0) return;
-  nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm,
-                              st ? st : ctx->stream),
+  if (count <= 0) return;
+  cudaStream_t s = st ? st : ctx->stream;
+  if (ctx->host_allreduce) {
+    double* h = host_stage(ctx, static_cast<size_t>(count));
+    RP_CUDA(cudaMemcpyAsync(h, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (ctx->host_allreduce(ctx->host_user, h, count) != 0) throw NcclFailure("host allreduce callback failed");
+    RP_CUDA(cudaMemcpyAsync(buf, h, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  if (!ctx->comm) return;
+  nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm, s),
              "ncclAllReduce");
+}
+
+// recv[r * count ...] = rank r's send[0..count) (recv holds world * count).
+void allgather(rp_ctx* ctx, const double* send, int64_t count, double* recv, cudaStream_t st = nullptr) {
+  cudaStream_t s = st ? st : ctx->stream;
+  if (count <= 0) return;
+  if (ctx->world == 1 || (!ctx->comm && !ctx->host_allgather)) {
+    require(ctx->world == 1, "allgather: no communicator");
+    if (recv != send)
+      RP_CUDA(cudaMemcpyAsync(recv, send, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (ctx->host_allgather) {
+    const size_t total = static_cast<size_t>(count) * static_cast<size_t>(ctx->world + 1);
+    double* h = host_stage(ctx, total);
+    double* hr = h + count;
+    RP_CUDA(cudaMemcpyAsync(h, send, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (ctx->host_allgather(ctx->host_user, h, count, hr) != 0) throw NcclFailure("host allgather callback failed");
+    RP_CUDA(cudaMemcpyAsync(recv, hr, sizeof(double) * count * ctx->world, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  nccl_check(nccl().AllGather(send, recv, static_cast<size_t>(count), ncclFloat64, ctx->comm, s), "ncclAllGather");
 }
 
 // ---- operator products -------------------------------------------------------
@@ -1071,17 +1130,15 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // The Gram matrix (a throughput-bound SYRK over A) runs on the context's
     // side stream from the start, overlapping the HBM-bound sketch and the
     // latency-bound preconditioner build; the basis waits for both.  (All
-    // streams at one priority: with a low-priority side stream, the TMA SYRK
-    // running next to higher-priority work came out wrong -- DESIGN.md.)
+    // streams at one priority: preempting a CTA of the TMA SYRK corrupts it
+    // -- DESIGN.md, concurrency finding.)
     // (single process only: with a communicator the Gram all-reduce would be
     // in flight on a second stream next to the sketch all-reduce)
     // (only for Gram matrices up to 4096^2, the measured range)
-    const bool side_gram = use_matrix && ctx->gram_overlap && !ctx->comm && op.d <= 4096;
+    const bool side_gram = use_matrix && ctx->gram_overlap && !has_comm(ctx) && op.d <= 4096;
     auto launch_side_gram = [&]() {
       if (!ctx->side) {
-        int lo = 0, hi = 0;
-        RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        RP_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, ctx->stream_priorities ? lo : 0));
+        RP_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
       }
       RP_CUDA(cudaEventCreateWithFlags(&gram_done, cudaEventDisableTiming));
       RP_CUDA(cudaEventRecord(gram_done, s));
@@ -1095,9 +1152,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     //    preconditioner -- runs on a second stream of the context.
     if (gram_done && ctx->sketch_on_hi) {
       if (!ctx->hi) {
-        int lo = 0, hi = 0;
-        RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        RP_CUDA(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, ctx->stream_priorities ? hi : 0));
+        RP_CUDA(cudaStreamCreateWithFlags(&ctx->hi, cudaStreamNonBlocking));
       }
       cudaEvent_t fork;
       RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1151,6 +1206,23 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     RP_CUDA(cudaEventDestroy(gram_done));  // (released once complete)
   }
   RP_CUDA(cudaEventRecord(ev.ev[2], s));
+  if (const char* dir = std::getenv("RP_DUMP_DIR")) {  // concurrency probe: the set-up products, raw bits
+    RP_CUDA(cudaDeviceSynchronize());
+    auto dump = [&](const char* name, const double* p, int64_t count) {
+      if (!p || count <= 0) return;
+      std::vector<double> h(static_cast<size_t>(count));
+      RP_CUDA(cudaMemcpy(h.data(), p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+      const std::string path = std::string(dir) + "/" + name + ".bin";
+      if (FILE* f = std::fopen(path.c_str(), "wb")) {
+        std::fwrite(h.data(), sizeof(double), h.size(), f);
+        std::fclose(f);
+      }
+    };
+    dump("sa", sa.get(), spec.m * dim);
+    dump("c", cbuf.get(), dim * K);
+    if (gram.matrix) dump("gram", gram.G.get(), dim * dim);
+    if (Lo > 0) dump("inv0", P.inv, P.n() * P.n());
+  }
   // 5) Bases for all owned intervals at once; diverged intervals are retried
   //    at tau/2 (path_solver.cpp:132-140).
   BasisRun run, run2;
@@ -1283,9 +1355,10 @@ namespace {
 thread_local std::string g_err_noctx;
 
 // One lock per device, held for the whole of every context call: calls are
-// synchronous, so contexts sharing a GPU never overlap their device work
-// (a second line of defence next to the single stream priority; DESIGN.md,
-// concurrency finding).  Recursive: a call may use another entry point.
+// synchronous, so contexts sharing a GPU in one process never overlap their
+// device work (a second line of defence next to the single stream priority:
+// the TMA pipelines must not be preempted, concurrency finding).
+// Recursive: a call may use another entry point.
 std::recursive_mutex& device_mutex(int dev) {
   static std::recursive_mutex m[64];
   return m[static_cast<unsigned>(dev) % 64];
@@ -1529,15 +1602,21 @@ void rp_destroy(rp_ctx* ctx) {
     ctx->op = OperatorStore();
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->side) {
+      release_workspace(ctx->side);
       cudaStreamSynchronize(ctx->side);
       cudaStreamDestroy(ctx->side);
     }
     if (ctx->hi) {
+      release_workspace(ctx->hi);
       cudaStreamSynchronize(ctx->hi);
       cudaStreamDestroy(ctx->hi);
     }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
-    if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    if (ctx->own) {
+      release_workspace(ctx->own);
+      cudaStreamDestroy(ctx->own);
+    }
     cudaSetDevice(prev);
   }
   delete ctx;
@@ -1576,7 +1655,9 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       require(value >= 0 && value <= 64, "gram_overlap_split must be in [0, 64]");
       ctx->gram_overlap_split = static_cast<int>(value);
     } else if (k == "stream_priorities") {
-      ctx->stream_priorities = value != 0;
+      require(value == 0,
+              "stream_priorities: rejected -- preempting a CTA with TMA copies in flight corrupts results "
+              "(DESIGN.md, concurrency finding)");
     } else if (k == "sketch_on_hi") {
       ctx->sketch_on_hi = value != 0;
     } else if (k == "gram_overlap_tma") {
@@ -1640,6 +1721,21 @@ rp_status rp_comm_init(rp_ctx* ctx, int rank, int world, const void* id128) {
     ncclUniqueId id;
     std::memcpy(&id, id128, 128);
     nccl_check(nccl().CommInitRank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+  });
+}
+
+rp_status rp_comm_init_host(rp_ctx* ctx, int rank, int world, rp_host_allreduce_fn allreduce_fn,
+                            rp_host_allgather_fn allgather_fn, void* user) {
+  if (!ctx) return RP_EINVAL;
+  return guarded(ctx, [&] {
+    require(world >= 1 && rank >= 0 && rank < world, "comm: bad rank/world");
+    require(allreduce_fn != nullptr && allgather_fn != nullptr, "comm: null host callback");
+    require(ctx->comm == nullptr, "comm: the context already has an NCCL communicator");
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->host_allreduce = allreduce_fn;
+    ctx->host_allgather = allgather_fn;
+    ctx->host_user = user;
   });
 }
 

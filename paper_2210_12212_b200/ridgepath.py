@@ -133,6 +133,7 @@ SIGNATURES = {
     "rp_launch_count": ([], _I64),
     "rp_comm_unique_id": ([_P], _INT),
     "rp_comm_init": ([_P, _INT, _INT, _P], _INT),
+    "rp_comm_init_host": ([_P, _INT, _INT, _P, _P, _P], _INT),
     "rp_set_dense": ([_P, _I64, _I64, _P, _I64, _INT], _INT),
     "rp_set_dense_rows": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _INT], _INT),
     "rp_set_dense_cols": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _INT], _INT),
@@ -493,10 +494,18 @@ class Context:
     def set_operator(self, a, force: bool = False):
         """Dense (numpy, n x d) or Csr; a torch CUDA tensor is used in place
         (column-major: pass A.T-contiguous storage, i.e. a tensor whose
-        transpose is contiguous)."""
-        key = (id(a), getattr(a, "shape", None))
-        if not force and key == self._op_key:
-            return
+        transpose is contiguous).
+
+        Host operators (numpy, Csr) are uploaded on every call, like the
+        reference reads A on every call: a caller may change them in place
+        between calls.  A device tensor is used in place (its current contents
+        are what the kernels read), so re-registering the same storage is
+        skipped."""
+        key = None
+        if _is_torch_cuda(a):
+            key = (a.data_ptr(), tuple(a.shape), tuple(a.stride()))
+            if not force and key == self._op_key:
+                return
         if isinstance(a, Csr):
             off = np.ascontiguousarray(a.offsets, dtype=np.int64)
             idx = np.ascontiguousarray(a.indices, dtype=np.int64)
@@ -1035,6 +1044,56 @@ def comm_unique_id() -> bytes:
 def comm_init(ctx: Context, rank: int, world: int, uid: bytes):
     buf = ctypes.create_string_buffer(uid, 128)
     ctx.check(lib().rp_comm_init(ctx.handle, rank, world, buf))
+
+
+_HOST_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, _P, ctypes.POINTER(ctypes.c_double), _I64)
+_HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, _P, ctypes.POINTER(ctypes.c_double), _I64,
+                                   ctypes.POINTER(ctypes.c_double))
+
+
+def comm_init_host(ctx: Context, rank: int, world: int, allreduce, allgather):
+    """rp_comm_init_host: the context's collectives run through Python
+    callables on host numpy arrays -- `allreduce(buf)` sums `buf` over ranks in
+    place, `allgather(send, recv)` fills recv (world x len(send)) with every
+    rank's send.  A raised exception fails the library call (RP_ENCCL)."""
+
+    def ar(_user, ptr, count):
+        try:
+            allreduce(np.ctypeslib.as_array(ptr, shape=(int(count),)))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    def ag(_user, send, count, recv):
+        try:
+            allgather(np.ctypeslib.as_array(send, shape=(int(count),)),
+                      np.ctypeslib.as_array(recv, shape=(int(world), int(count))))
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    cb = (_HOST_ALLREDUCE(ar), _HOST_ALLGATHER(ag))
+    ctx._host_comm = cb  # keep the thunks alive with the context
+    ctx.check(lib().rp_comm_init_host(ctx.handle, rank, world, ctypes.cast(cb[0], _P), ctypes.cast(cb[1], _P), None))
+
+
+def comm_init_torch_host(ctx: Context, group=None):
+    """Host communicator over an initialised torch.distributed process group
+    (e.g. gloo): several ranks may then share one GPU, or run without NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+
+    def allreduce(buf):
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t, group=group)
+
+    def allgather(send, recv):
+        outs = [torch.from_numpy(recv[r]) for r in range(world)]
+        dist.all_gather(outs, torch.from_numpy(send.copy()), group=group)
+
+    comm_init_host(ctx, dist.get_rank(group), world, allreduce, allgather)
 
 
 def path_raw(ctx: Context, b_ptr: int, K: int, config: PathConfig, spec: SketchSpec, rho: RhoBounds, x_ptr: int,

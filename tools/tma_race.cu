@@ -4,7 +4,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lcuda -I paper_2210_12212_b200/csrc \
 //        tools/tma_race.cu -o gpurun_out/tma_race && gpurun_out/tma_race
 // Modes (argv[1]): 0 = both TMA, 1 = side stream cp.async, 2 = split_k forced 1 on both,
-//                  3 = no lower_only on the side SYRK
+//   argv[3] = 0: both streams at one priority (default: side low, chain high)
+//                  3 = no lower_only on the side SYRK, 4 = the path's SYRK layout (A^T A, tile 3, split 4)
 #include "../paper_2210_12212_b200/csrc/gemm_f64.cu"
 
 #include <cstdio>
@@ -44,13 +45,18 @@ int main(int argc, char** argv) {
   cudaStream_t s1, s2;
   int lo, hi;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, lo);
-  cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi);
+  const bool prio = !(argc > 3 && atoi(argv[3]) == 0);  // argv[3] = 0: both streams at the default priority
+  cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, prio ? lo : 0);
+  cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio ? hi : 0);
 
   auto side = [&](double* out, cudaStream_t st) {  // the side-stream Gram SYRK
     GemmArgs g;
     g.opa = Op::N, g.opb = Op::T, g.m = d, g.n = d, g.k = n;
     g.a = A, g.lda = d, g.b = A, g.ldb = d, g.c = out, g.ldc = d;
+    if (mode == 4) {  // the path's layout: A n x d column-major, G = A^T A, 64 x 32 tile, split 4, mirrored
+      g.opa = Op::T, g.opb = Op::N, g.lda = n, g.ldb = n;
+      g.force_tile = 3, g.split_k = 4, g.mirror = true;
+    }
     g.lower_only = mode != 3;
     g.no_tma = mode == 1;
     if (mode == 2) g.split_k = 1;
@@ -90,7 +96,8 @@ int main(int argc, char** argv) {
     bad_g += dg != 0, bad_y += dy != 0;
     printf("rep %d: gram mismatches %lld, chain mismatches %lld\n", r, (long long)dg, (long long)dy);
   }
-  printf("mode %d: %d/%d gram runs differ, %d/%d chain runs differ; err %s\n", mode, bad_g, reps, bad_y, reps,
+  printf("mode %d%s: %d/%d gram runs differ, %d/%d chain runs differ; err %s\n", mode,
+         prio ? " (side low / chain high priority)" : " (one priority)", bad_g, reps, bad_y, reps,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
