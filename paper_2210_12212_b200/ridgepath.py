@@ -1035,6 +1035,24 @@ def set_dense_cols_device(ctx: Context, n: int, d_global: int, col0: int, d_loca
     ctx._op_key = ("device-cols", ptr, n, d_global, col0, d_local)
 
 
+def set_dense_cols_host(ctx: Context, n: int, d_global: int, col0: int, d_local: int, ptr: int, lda: int):
+    """rp_set_dense_cols from host memory: columns [col0, col0 + d_local) of
+    the n x d_global operator (dual route, column-sharded)."""
+    ctx.check(lib().rp_set_dense_cols(ctx.handle, n, d_global, col0, d_local, _P(ptr), lda, RP_HOST))
+    ctx._op_key = ("host-cols", ptr, n, d_global, col0, d_local)
+
+
+def set_csr_rows(ctx: Context, n_global: int, row0: int, shard: "Csr"):
+    """rp_set_csr_rows: `shard` holds rows [row0, row0 + shard.rows) of the
+    n_global x shard.cols CSR operator (offsets local, starting at 0)."""
+    off = np.ascontiguousarray(shard.offsets, dtype=np.int64)
+    idx = np.ascontiguousarray(shard.indices, dtype=np.int64)
+    val = np.ascontiguousarray(shard.values, dtype=np.float64)
+    ctx.check(lib().rp_set_csr_rows(ctx.handle, n_global, row0, shard.rows, shard.cols, _ptr(off), _ptr(idx),
+                                    _ptr(val), RP_HOST))
+    ctx._op_key = None
+
+
 def comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().rp_comm_unique_id(buf))
