@@ -108,6 +108,29 @@ __global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, const
   }
 }
 
+__global__ void woodbury_tail_rows_kernel(int64_t f0, int64_t rows, int64_t cols, int64_t L,
+                                          const double* __restrict__ args, int64_t ld_args, int64_t s_args,
+                                          const double* __restrict__ t3, const double* __restrict__ lambda0,
+                                          double* __restrict__ pack, int64_t blk) {
+  const int64_t N = cols * L;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rows * N;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx % rows, j = idx / rows, l = j / cols, c = j - l * cols;
+    pack[j * blk + r] =
+        __ddiv_rn(__dsub_rn(args[l * s_args + c * ld_args + f0 + r], t3[j * rows + r]), lambda0[l]);
+  }
+}
+
+__global__ void gather_row_blocks_kernel(const double* __restrict__ recv, int64_t blk, int64_t dim, int64_t cols,
+                                         int64_t L, double* __restrict__ out, int64_t s_out) {
+  const int64_t N = cols * L;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < dim * N;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx % dim, j = idx / dim, r = row / blk, l = j / cols, c = j - l * cols;
+    out[l * s_out + c * dim + row] = recv[r * blk * N + j * blk + (row - r * blk)];
+  }
+}
+
 __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
                                  double* __restrict__ out, int64_t ldo, int64_t cblk0) {
   __shared__ double tile[32][33];
@@ -270,6 +293,22 @@ void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t s_args, const d
   if (dim <= 0 || cols <= 0 || L <= 0) return;
   woodbury_tail_kernel<<<grid_for(dim * cols * L), 256, 0, stream>>>(dim, cols, L, args, s_args, t3, s_t3, d_lambda0,
                                                                      out, s_out);
+  RP_LAUNCH_CHECK();
+}
+
+void woodbury_tail_rows(int64_t f0, int64_t rows, int64_t cols, int64_t L, const double* args, int64_t ld_args,
+                        int64_t s_args, const double* t3, const double* d_lambda0, double* pack, int64_t blk,
+                        cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0 || L <= 0) return;
+  woodbury_tail_rows_kernel<<<grid_for(rows * cols * L), 256, 0, stream>>>(f0, rows, cols, L, args, ld_args, s_args,
+                                                                          t3, d_lambda0, pack, blk);
+  RP_LAUNCH_CHECK();
+}
+
+void gather_row_blocks(const double* recv, int64_t blk, int64_t dim, int64_t cols, int64_t L, double* out,
+                       int64_t s_out, cudaStream_t stream) {
+  if (dim <= 0 || cols <= 0 || L <= 0) return;
+  gather_row_blocks_kernel<<<grid_for(dim * cols * L), 256, 0, stream>>>(recv, blk, dim, cols, L, out, s_out);
   RP_LAUNCH_CHECK();
 }
 

@@ -57,6 +57,19 @@ void compose(const BasisDims& d, const double* tilde, const double* d_tau, const
 void woodbury_tail(int64_t dim, int64_t cols, int64_t L, int64_t s_args, const double* args, int64_t s_t3,
                    const double* t3, const double* d_lambda0, int64_t s_out, double* out, cudaStream_t stream);
 
+// Feature-sharded Woodbury tail: rows [f0, f0 + rows) of out_l = (args_l -
+// t3_l) / lambda0_l, written into this rank's pack block (ld blk, column
+// l*cols + c) for the all-gather.  args: interval stride s_args (0 =
+// broadcast), ld `ld_args`; t3: rows x (L*cols), ld rows.
+void woodbury_tail_rows(int64_t f0, int64_t rows, int64_t cols, int64_t L, const double* args, int64_t ld_args,
+                        int64_t s_args, const double* t3, const double* d_lambda0, double* pack, int64_t blk,
+                        cudaStream_t stream);
+// Unpack an all-gathered row-block matrix: recv holds world blocks of
+// blk x N (ld blk), block r = rows [r*blk, min(dim, (r+1)*blk)); column
+// j = l*cols + c goes to out[l*s_out + c*dim + row].
+void gather_row_blocks(const double* recv, int64_t blk, int64_t dim, int64_t cols, int64_t L, double* out,
+                       int64_t s_out, cudaStream_t stream);
+
 // Loss pieces (path_solver.cpp:425-454).  For output column j of R
 // (rows x cols, ld ldr): out[j] = sum_r (R[r, j] - B[r, j % K])^2 (B may be
 // null: plain sum of squares), summed over rows in a fixed order.

@@ -384,6 +384,11 @@ struct rp_ctx {
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
   int64_t csr_one_panel_bytes = 48 << 20;  // option "csr_one_panel_bytes": M W up to this size runs as one panel
   int64_t csr_chunk = 128;           // option "csr_chunk": right-hand columns per sparse Gram sweep (<= 128)
+  // option "feature_shard": with several ranks, the Woodbury preconditioner
+  // (m < d) is sharded over the d features (all-reduce of SA in,
+  // all-gather of the output rows) and its shifted m x m factors over the
+  // intervals (all-gather of the inverses); 0 = every rank applies it whole
+  bool feature_shard = true;
   std::string err;
 };
 
@@ -685,6 +690,11 @@ struct PrecondBatch {
   int64_t m = 0, d = 0, L = 0;
   bool woodbury = false;
   bool col_stable = true;  // (see GramOp::col_stable)
+  // feature sharding (Woodbury, several ranks): this rank applies SA[:, f0:f1],
+  // rows split in blocks of `blk` (the last rank's block may be short)
+  bool fshard = false;
+  int64_t f0 = 0, f1 = 0, blk = 0;
+  bool allow_fshard = true;  // false when the ranks build different interval sets (collectives would not match)
   const double* sa = nullptr;  // m x d
   std::vector<double> lambda0;
   DBuf<double> d_lambda0;
@@ -703,7 +713,38 @@ struct PrecondBatch {
     lambda0 = l0;
     for (double v : l0) require(v > 0.0, "preconditioner: shift must be positive");
     const int64_t nn = n();
+    fshard = woodbury && allow_fshard && ctx->feature_shard && ctx->world > 1 && has_comm(ctx);
+    if (fshard) {
+      blk = ceil_div(d, ctx->world);
+      f0 = std::min<int64_t>(d, blk * ctx->rank);
+      f1 = std::min<int64_t>(d, f0 + blk);
+    }
     DBuf<double> gbuf;
+    if (!gram && fshard) {
+      // SA SA^T = sum over ranks of SA[:, f0:f1] SA[:, f0:f1]^T
+      gbuf.alloc(static_cast<size_t>(nn * nn), s);
+      if (f1 > f0) {
+        GemmArgs g;
+        g.opa = Op::N;
+        g.opb = Op::T;
+        g.m = nn;
+        g.n = nn;
+        g.k = f1 - f0;
+        g.a = sa + f0 * m;
+        g.lda = m;
+        g.b = sa + f0 * m;
+        g.ldb = m;
+        g.c = gbuf.get();
+        g.ldc = nn;
+        g.lower_only = true;
+        g.mirror = true;
+        dgemm(g, s);
+      } else {
+        fill(gbuf.get(), nn * nn, 0.0, s);
+      }
+      allreduce(ctx, gbuf.get(), nn * nn);
+      gram = gbuf.get();
+    }
     if (!gram) {
       gbuf.alloc(static_cast<size_t>(nn * nn), s);
       GemmArgs g;
@@ -725,6 +766,22 @@ struct PrecondBatch {
     }
     d_lambda0.alloc(static_cast<size_t>(L), s);
     RP_CUDA(cudaMemcpyAsync(d_lambda0.get(), lambda0.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+    if (fshard && L > 1) {
+      // the shifted m x m factors split over the ranks by interval, then
+      // all-gathered: rank r inverts shifts [r*lb, min(L, (r+1)*lb))
+      const int64_t lb = ceil_div(L, ctx->world);
+      const int64_t s0 = std::min<int64_t>(L, lb * ctx->rank), s1 = std::min<int64_t>(L, s0 + lb);
+      DBuf<double> mine(static_cast<size_t>(lb * nn * nn), s);
+      if (s1 > s0) {
+        DBuf<double> h(static_cast<size_t>((s1 - s0) * nn * nn), s);
+        shifted_copies(gram, nn, d_lambda0.get() + s0, s1 - s0, h.get(), s);
+        spd_inverse_batched(h.get(), nn, nn, nn * nn, s1 - s0, mine.get(), nn, nn * nn, s);
+      }
+      inv_owned.alloc(static_cast<size_t>(ctx->world * lb * nn * nn), s);
+      allgather(ctx, mine.get(), lb * nn * nn, inv_owned.get());
+      inv = inv_owned.get();  // (rank blocks are consecutive shifts: the first L blocks are shifts 0..L-1)
+      return;
+    }
     DBuf<double> h(static_cast<size_t>(L * nn * nn), s);
     shifted_copies(gram, nn, d_lambda0.get(), L, h.get(), s);
     inv_owned.alloc(static_cast<size_t>(L * nn * nn), s);
@@ -741,6 +798,10 @@ struct PrecondBatch {
     v.woodbury = woodbury;
     v.col_stable = col_stable;
     v.sa = sa;
+    v.fshard = fshard;
+    v.f0 = f0;
+    v.f1 = f1;
+    v.blk = blk;
     v.lambda0 = {lambda0[static_cast<size_t>(l)]};
     v.d_lambda0.alloc(1, ctx->stream);
     RP_CUDA(cudaMemcpyAsync(v.d_lambda0.get(), v.lambda0.data(), sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -795,6 +856,10 @@ struct PrecondBatch {
     // the m x m middle factor is batched per interval.  A broadcast input is
     // multiplied by SA once.
     const bool bcast = sin == 0;
+    if (fshard) {
+      apply_feature_sharded(ctx, in, sin, cols, out, sout);
+      return;
+    }
     const double* src = in;
     DBuf<double> inb;
     if (!bcast && sin != d * cols) {
@@ -848,6 +913,83 @@ struct PrecondBatch {
     dgemm(g3, s);
     // out_l = (in_l - t3_l) / l0_l
     woodbury_tail(d, cols, L, sin, in, d * cols, t3.get(), d_lambda0.get(), sout, out, s);
+  }
+
+  // Woodbury apply with the features split over the ranks:
+  //   t1   = sum_p SA[:, f_p] in[f_p, :]          local GEMM + all-reduce (m x L*cols)
+  //   t2_l = W_l t1_l                             replicated m x m batch
+  //   t3_p = SA[:, f_p]^T t2                      local GEMM (|f_p| x L*cols)
+  //   out[f_p, :] = (in[f_p, :] - t3_p) / l0_l    local, then all-gather of the row blocks
+  // Per call: one all-reduce of 8*m*L*cols bytes and one all-gather of
+  // 8*d*L*cols bytes; the 4*m*d*L*cols SA flops are split over the ranks.
+  void apply_feature_sharded(rp_ctx* ctx, const double* in, int64_t sin, int64_t cols, double* out,
+                             int64_t sout) const {
+    cudaStream_t s = ctx->stream;
+    const bool bcast = sin == 0;
+    const int64_t dl = f1 - f0;
+    const double* src = in;
+    DBuf<double> inb;
+    if (!bcast && sin != d * cols) {
+      inb.alloc(static_cast<size_t>(L * d * cols), s);
+      for (int64_t l = 0; l < L; ++l) copy_cols(in + l * sin, d, cols, d, inb.get() + l * d * cols, d, s);
+      src = inb.get();
+    }
+    const int64_t n1 = bcast ? cols : L * cols;
+    DBuf<double> t1(static_cast<size_t>(m * n1), s), t2(static_cast<size_t>(L * m * cols), s);
+    if (dl > 0) {
+      GemmArgs g1;  // t1 = SA[:, f0:f1] in[f0:f1, :]
+      g1.m = m;
+      g1.n = n1;
+      g1.k = dl;
+      g1.a = sa + f0 * m;
+      g1.lda = m;
+      g1.b = src + f0;
+      g1.ldb = d;
+      g1.c = t1.get();
+      g1.ldc = m;
+      g1.col_stable = true;
+      dgemm(g1, s);
+    } else {
+      fill(t1.get(), m * n1, 0.0, s);
+    }
+    allreduce(ctx, t1.get(), m * n1);
+    GemmArgs g2;  // t2_l = W_l t1_l
+    g2.m = m;
+    g2.n = cols;
+    g2.k = m;
+    g2.a = inv;
+    g2.lda = m;
+    g2.stride_a = m * m;
+    g2.b = t1.get();
+    g2.ldb = m;
+    g2.stride_b = bcast ? 0 : m * cols;
+    g2.c = t2.get();
+    g2.ldc = m;
+    g2.stride_c = m * cols;
+    g2.batch = L;
+    g2.col_stable = true;
+    dgemm(g2, s);
+    DBuf<double> t3(static_cast<size_t>(std::max<int64_t>(dl, 1) * L * cols), s);
+    DBuf<double> pack(static_cast<size_t>(blk * L * cols), s);
+    if (dl > 0) {
+      GemmArgs g3;  // t3 = SA[:, f0:f1]^T [t2_0 .. t2_{L-1}]
+      g3.opa = Op::T;
+      g3.m = dl;
+      g3.n = L * cols;
+      g3.k = m;
+      g3.a = sa + f0 * m;
+      g3.lda = m;
+      g3.b = t2.get();
+      g3.ldb = m;
+      g3.c = t3.get();
+      g3.ldc = dl;
+      g3.col_stable = true;
+      dgemm(g3, s);
+      woodbury_tail_rows(f0, dl, cols, L, in, d, sin, t3.get(), d_lambda0.get(), pack.get(), blk, s);
+    }
+    DBuf<double> recv(static_cast<size_t>(ctx->world * blk * L * cols), s);
+    allgather(ctx, pack.get(), blk * L * cols, recv.get());
+    gather_row_blocks(recv.get(), blk, d, cols, L, out, sout, s);
   }
 };
 
@@ -1199,6 +1341,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     ks.push_back(plans[l].params.k);
   }
   P.col_stable = ctx->stable_columns;
+  P.allow_fshard = !split;
   gram.col_stable = ctx->stable_columns;
   if (Lo > 0) P.build(ctx, sa.get(), nullptr, spec.m, dim, l0s);
   if (gram_done) {
@@ -1244,6 +1387,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
         retry_slot[retry[j]] = static_cast<int>(j);
       }
       P2.col_stable = ctx->stable_columns;
+      P2.allow_fshard = !split;
       P2.build(ctx, sa.get(), nullptr, spec.m, dim, l0r);
       run_basis(ctx, gram, P2, cbuf.get(), K, taur, kr, run2);
       for (int v : run2.diverged) failed |= v;
@@ -1654,6 +1798,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "gram_overlap_split") {
       require(value >= 0 && value <= 64, "gram_overlap_split must be in [0, 64]");
       ctx->gram_overlap_split = static_cast<int>(value);
+    } else if (k == "feature_shard") {
+      ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {
       require(value == 0,
               "stream_priorities: rejected -- preempting a CTA with TMA copies in flight corrupts results "
