@@ -53,6 +53,8 @@ def parse():
                     help="also time the 1-thread CPU baseline (default: on for c1-c3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="c1 only: x(lambda) vs the oracle, every rank")
+    ap.add_argument("--path-only", action="store_true",
+                    help="only the timed steps (no roofline / pass / e2e / CPU legs): for ncu launch lists")
     a = ap.parse_args()
     if a.config is None:
         a.config = "c2" if a.gpus == 1 else "c3"
@@ -457,6 +459,15 @@ def run_ours(args):
               for k in ("sketch_seconds", "linear_seconds", "gram_seconds", "precond_seconds", "basis_seconds",
                         "eval_seconds", "total_seconds")}
     gram_mode = tms[-1].gram_mode
+    if args.path_only:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+                              "config": {"workload": dw.desc}, "phases_s": phases,
+                              "gpu_launches": int(launches)}), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     # Roofline of the dominant kernel family (the FP64 DMMA GEMMs: sketch,
     # SYRK, factor, preconditioner applies, Gram products): the same steps

@@ -183,6 +183,8 @@ __device__ __forceinline__ void tma_box(double* dst, const CUtensorMap* map, int
       : "memory");
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPWarps * 32) : "memory"); }
+template <int NW>
+__device__ __forceinline__ void consumer_sync_n() { asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory"); }
 
 // The tile sequence of one CTA, shared by producer and consumers.
 //   GRAM: row tiles of block 0; then for each block i, interleaved:
@@ -405,6 +407,144 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
   }
 }
 
+// ---- Gram pass on the FP64 tensor cores: z = A^T (A W), W up to 8 columns ------
+//
+// The column pass above is issue-bound beyond one right-hand column (each
+// element of A costs 2K FMAs plus their operand loads on the SIMT pipes).
+// Here both products run as DMMA m8n8k4 (W padded to 8 columns), so an
+// element of A costs 1/16 of a warp instruction whatever K <= 8 is, and every
+// block of A is read from HBM exactly once:
+//   * persistent CTAs (one per SM) own contiguous runs of 8-row blocks; a
+//     producer warp streams each block (8 rows x all d columns, 64-byte
+//     column segments) into a shared-memory ring with 2-D TMA boxes of
+//     8 x 256, 64B-swizzled (both fragment patterns below are then
+//     conflict-free);
+//   * eight consumer warps own d/8 columns each.  y pass:
+//     y_blk^T (K x 8 rows) = W^T A_blk^T with W^T as the register-resident A
+//     operand and the stage as the B operand, four accumulator chains;
+//   * the eight partial y tiles meet in shared memory (one named barrier per
+//     block, summed in warp order), then the z pass
+//     z[cols] (8 cols x K) += A_blk^T y_blk reads the same stage again as the
+//     A operand: z stays in registers for the whole kernel;
+//   * per-CTA z partials are summed in CTA order (sum_chunks_tree_kernel).
+// Fixed summation orders throughout: deterministic.  Bound: HBM (8 n d
+// bytes) as long as the DMMA pipe keeps up: 2 DMMA (512 flops each) per
+// 32 elements = 32 flops per 8 bytes, i.e. ~70 % of the DMMA peak at the
+// HBM roof on B200.
+
+constexpr int kGRows = 8;     // rows per block
+constexpr int kGWarps = 8;    // consumer warps
+constexpr int kGBox = 256;    // columns per TMA box
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Index (in doubles) of element (row r < 8, stage column c) in a 64B-swizzled
+// stage: the 16-byte chunk (byte-offset bits 4-5, = r >> 1) is XORed with
+// byte-offset bits 7-8 (= (c >> 1) & 3), i.e. r ^ (c & 6) -- written so that
+// the unrolled fragment offsets fold into immediates.
+__device__ __forceinline__ int sw64(int c, int r) { return c * kGRows + (r ^ (c & 6)); }
+
+template <int NT>  // columns per warp = 32 * NT
+__global__ void __launch_bounds__(kGWarps * 32, 1)
+    gram_dmma_kernel(const __grid_constant__ CUtensorMap map, int64_t n, int64_t d, int K,
+                     const double* __restrict__ w, double* __restrict__ ws, int stages) {
+  constexpr int CPW = 32 * NT;       // columns per warp
+  constexpr int KS = CPW / 4;        // k-steps of the y pass (also W fragments)
+  constexpr int MT = CPW / 8;        // 8-column tiles of the z pass
+  constexpr int DPAD = CPW * kGWarps;
+  constexpr int STAGE = DPAD * kGRows;  // doubles
+  extern __shared__ __align__(1024) double sm_raw[];
+  double* ring = sm_raw + (((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u) >> 3);
+  double* ypart = ring + stages * STAGE;  // [2][kGWarps][64]
+  __shared__ __align__(8) uint64_t full[kPMaxStages];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t nb = (n + kGRows - 1) / kGRows;
+  const int64_t b0 = (static_cast<int64_t>(blockIdx.x) * nb) / gridDim.x;
+  const int64_t cnt = (static_cast<int64_t>(blockIdx.x + 1) * nb) / gridDim.x - b0;
+  uint64_t pol = 0;
+  // Thread 0 issues the TMA boxes (no producer warp: 8 warps = 2 per SM
+  // sub-partition leave 255 registers per thread for the W fragments and the
+  // z accumulators).  Block j lives in stage j % stages; it is refilled with
+  // block j + stages once every warp is past the block barrier of block j + 1.
+  auto issue = [&](int64_t j) {
+    const int st = static_cast<int>(j % stages);
+    mbar_arrive_expect_tx(&full[st], STAGE * 8);
+    for (int c0 = 0; c0 < DPAD; c0 += kGBox)
+      tma_box(ring + st * STAGE + c0 * kGRows, &map, static_cast<int>((b0 + j) * kGRows), c0, &full[st], pol);
+  };
+  if (t == 0) {
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (int s2 = 0; s2 < stages; ++s2) mbar_init(&full[s2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t j = 0; j < stages && j < cnt; ++j) issue(j);
+  }
+  __syncthreads();
+
+  const int g4 = lane >> 2, q4 = lane & 3;
+  const int cw = wid * CPW;  // this warp's first column
+  // W^T fragments (A operand of the y pass): lane (m = K index g4, k = column q4)
+  double wf[KS];
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {
+    const int c = cw + 4 * i + q4;
+    wf[i] = (g4 < K && c < d) ? __ldg(w + c + static_cast<int64_t>(g4) * d) : 0.0;
+  }
+  double zacc[MT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) zacc[i][0] = zacc[i][1] = 0.0;
+  for (int64_t j = 0; j < cnt; ++j) {
+    const int st = static_cast<int>(j % stages);
+    mbar_wait(&full[st], static_cast<uint32_t>((j / stages) & 1));
+    const double* sg = ring + st * STAGE;
+    // y pass: yT (K x 8 rows) = W^T (K x CPW) A_blk^T (CPW x 8), four chains
+    double ya[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ya[u][0] = ya[u][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < KS; ++i) dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sg[sw64(cw + 4 * i + q4, g4)]);
+    const int buf = static_cast<int>(j & 1);
+    double* yp = ypart + (buf * kGWarps + wid) * 64;
+    yp[2 * lane] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
+    yp[2 * lane + 1] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
+    // every warp is done with block j - 1 (its z pass precedes this barrier):
+    // its stage takes block j - 1 + stages
+    __syncthreads();
+    if (t == 0 && j >= 1 && j - 1 + stages < cnt) issue(j - 1 + stages);
+    // B fragments of the z pass: y (k = row, n = K index) summed over the warps in order
+    double yb[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double* base = ypart + buf * kGWarps * 64 + g4 * 8 + 4 * h + q4;  // yT[K = g4][row = 4h + q4]
+      double sacc = base[0];
+#pragma unroll
+      for (int w2 = 1; w2 < kGWarps; ++w2) sacc += base[w2 * 64];
+      yb[h] = sacc;
+    }
+    // z pass: z (8 cols x K) += A_blk^T (8 cols x 8 rows) y (8 rows x K)
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int c = cw + 8 * i + g4;
+      dmma(zacc[i][0], zacc[i][1], sg[sw64(c, q4)], yb[0]);
+      dmma(zacc[i][0], zacc[i][1], sg[sw64(c, 4 + q4)], yb[1]);
+    }
+  }
+  // this CTA's z partial: lane holds z[col = cw + 8i + g4][K = 2 q4 + e]
+  double* out = ws + static_cast<int64_t>(blockIdx.x) * d * K;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int c = cw + 8 * i + g4;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = 2 * q4 + e;
+      if (c < d && k < K) out[c + static_cast<int64_t>(k) * d] = zacc[i][e];
+    }
+  }
+}
+
 // The last n % 32 rows (one CTA): the same sums, written as one more partial.
 template <int K, bool GRAM>
 __global__ void __launch_bounds__(256) colpass_tail_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
@@ -464,7 +604,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // Tensor map of the column-major operator: dims (rows n, columns d), box
 // rows x cols; the smem image is [column][row].
 bool operator_tensor_map(CUtensorMap* map, const double* a, int64_t lda, int64_t n, int64_t d, int box_rows,
-                         int box_cols, bool swizzle128) {
+                         int box_cols, bool swizzle128, bool swizzle64 = false) {
   auto enc = tensor_map_encoder();
   if (!enc || n >= (int64_t{1} << 31) || d >= (int64_t{1} << 31)) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(d)};
@@ -472,7 +612,8 @@ bool operator_tensor_map(CUtensorMap* map, const double* a, int64_t lda, int64_t
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : (swizzle64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -523,6 +664,57 @@ void atv_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double
   sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(d * K, 256), 1184)), 256, 0, s>>>(
       part.get(), chunks, d * K, x);
   RP_LAUNCH_CHECK();
+}
+
+
+// The DMMA Gram pass (k <= 8 columns, d <= 5 * 256): false if it does not apply.
+template <int NT>
+bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
+                         cudaStream_t s) {
+  constexpr int DPAD = 32 * NT * kGWarps;
+  CUtensorMap map;
+  if (!operator_tensor_map(&map, a, lda, n, d, kGRows, kGBox, false, true)) return false;
+  constexpr size_t stage_bytes = static_cast<size_t>(DPAD) * kGRows * sizeof(double);
+  const size_t fixed = 2 * kGWarps * 64 * sizeof(double) + 1024;
+  const size_t budget = 225 * 1024;
+  const int stages = static_cast<int>(std::min<size_t>(kPMaxStages, (budget - fixed) / stage_bytes));
+  if (stages < 3) return false;  // (block j uses one stage, block j - 1 is refilled, one in flight)
+  const size_t smem = fixed + static_cast<size_t>(stages) * stage_bytes;
+  int dev = 0, sms = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t nb = (n + kGRows - 1) / kGRows;
+  const int grid = static_cast<int>(std::min<int64_t>(nb, sms));
+  DBuf<double> ws(static_cast<size_t>(grid) * d * k, s);
+  ensure_dynamic_smem(gram_dmma_kernel<NT>, smem);
+  gram_dmma_kernel<NT><<<grid, kGWarps * 32, smem, s>>>(map, n, d, static_cast<int>(k), w, ws.get(), stages);
+  RP_LAUNCH_CHECK();
+  sum_chunks_tree_kernel<<<static_cast<unsigned>(ceil_div(d * k, 16)), 256, 0, s>>>(ws.get(), grid, d * k, z);
+  RP_LAUNCH_CHECK();
+  return true;
+}
+
+bool gram_dmma_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
+                      cudaStream_t s) {
+  if (k < 1 || k > 8 || n <= 0 || d <= 0 || lda % 2 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) return false;
+  switch (ceil_div(d, 32 * kGWarps)) {
+    case 1: return gram_dmma_launch_nt<1>(a, lda, n, d, w, k, z, s);
+    case 2: return gram_dmma_launch_nt<2>(a, lda, n, d, w, k, z, s);
+    case 3: return gram_dmma_launch_nt<3>(a, lda, n, d, w, k, z, s);
+    case 4: return gram_dmma_launch_nt<4>(a, lda, n, d, w, k, z, s);
+    case 5: return gram_dmma_launch_nt<5>(a, lda, n, d, w, k, z, s);
+    default: return false;
+  }
+}
+
+// Smallest column count sent to the DMMA pass (RP_GRAM_DMMA_MIN, default 2:
+// one column stays on the SIMT column pass).
+int64_t gram_dmma_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("RP_GRAM_DMMA_MIN");
+    return e ? std::atoll(e) : int64_t{2};
+  }();
+  return v;
 }
 
 }  // namespace
@@ -587,6 +779,7 @@ void atv_narrow(const double* a, int64_t lda, int64_t n, int64_t d, const double
 bool gram_fused(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
                 cudaStream_t stream) {
   if (k < 1 || k > 8 || d <= 0 || n <= 0) return false;
+  if (k >= gram_dmma_min() && gram_dmma_launch(a, lda, n, d, w, k, z, stream)) return true;
   return colpass_columns<true>(a, lda, n, d, w, d, k, z, stream) == k;
 }
 

@@ -16,6 +16,7 @@
 #include <cusolverDn.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -389,6 +390,7 @@ struct rp_ctx {
   // all-gather of the output rows) and its shifted m x m factors over the
   // intervals (all-gather of the inverses); 0 = every rank applies it whole
   bool feature_shard = true;
+  bool csr_l2_persist = false;  // option "csr_l2_persist": sparse Gram running sums as an L2-persisting window
   std::string err;
 };
 
@@ -606,7 +608,8 @@ struct GramOp {
           static_cast<double>(op.n_loc) * static_cast<double>(cols) * 8.0 <= static_cast<double>(ctx->csr_one_panel_bytes);
       const PanelView pv = one_panel ? single_panel(op.n_loc, op.d, op.csc_off, op.csc_row, op.csc_val)
                                      : view_of(panel_csc(ctx, op));
-      sparse_gram(op.csr_off, op.csr_col, op.csr_val, pv, W, op.d, cols, Y, op.d, ctx->csr_chunk, s);
+      sparse_gram(op.csr_off, op.csr_col, op.csr_val, pv, W, op.d, cols, Y, op.d, ctx->csr_chunk, s,
+                  ctx->csr_l2_persist);
       allreduce(ctx, Y, op.d * cols);
       return;
     }
@@ -1056,19 +1059,23 @@ void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c
       e.flags = flags.get();
       Partials py;
       for (int64_t g = 1; g < kmax; ++g) {
+        nvtxRangePushA("generation");
         e.g = g;
         e.kind = RecursionEpilogue::kArgs;
         gram.apply(out.gen.get(), g * NB, y.get(), &py, &e);
         e.kind = RecursionEpilogue::kUpdate;
         P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, nullptr, &e);
+        nvtxRangePop();
       }
     } else {
       Partials py, pa;
       for (int64_t g = 1; g < kmax; ++g) {
+        nvtxRangePushA("generation");
         gram.apply(out.gen.get(), g * NB, y.get(), &py);
         build_args(d, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
         P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
         update_gen(d, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+        nvtxRangePop();
       }
     }
   }
@@ -1157,6 +1164,23 @@ PathCfg to_cfg(const rp_path_config* c) {
   return o;
 }
 
+// NVTX ranges (header-only NVTX 3: free unless a profiler is attached).  The
+// reference's timing sites (path_solver.cpp:12-16, 153-189) become ranges a
+// profiler timeline shows: one per path, one per phase, one per generation.
+struct NvtxPhases {
+  bool open = false;
+  explicit NvtxPhases(const char* whole) { nvtxRangePushA(whole); }
+  void next(const char* name) {
+    if (open) nvtxRangePop();
+    nvtxRangePushA(name);
+    open = true;
+  }
+  ~NvtxPhases() {
+    if (open) nvtxRangePop();
+    nvtxRangePop();
+  }
+};
+
 // ---- run_path (path_solver.cpp:147-190) ------------------------------------------
 
 struct Events {
@@ -1212,6 +1236,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
 
   Events ev(8);
   RP_CUDA(cudaEventRecord(ev.ev[0], s));
+  NvtxPhases nv(dual ? "ridgepath: dual_path" : "ridgepath: ihs_bin_path");
+  nv.next("sketch + linear term (+ Gram matrix)");
   // 2) Plans (host, bit-identical to the reference).
   const auto plans = plan_intervals(cfg, rho, sigma_d);
   const int64_t L = static_cast<int64_t>(plans.size());
@@ -1320,6 +1346,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   }
   if (use_matrix && !gram.matrix) gram.build_matrix();  // (gram_overlap off)
   RP_CUDA(cudaEventRecord(ev.ev[6], s));
+  nv.next("preconditioners (batched factorization)");
   // 4) Interval ownership.  With the Gram matrix every rank holds the whole
   //    operator state (SA, c, G are all-reduced), so the intervals -- which are
   //    independent (path_solver.cpp:168-186) -- are split round-robin and the
@@ -1349,6 +1376,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     RP_CUDA(cudaEventDestroy(gram_done));  // (released once complete)
   }
   RP_CUDA(cudaEventRecord(ev.ev[2], s));
+  nv.next("interval bases (all intervals, lock-step generations)");
   if (const char* dir = std::getenv("RP_DUMP_DIR")) {  // concurrency probe: the set-up products, raw bits
     RP_CUDA(cudaDeviceSynchronize());
     auto dump = [&](const char* name, const double* p, int64_t count) {
@@ -1405,6 +1433,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   }
   if (failed) throw SolverFailure("interval basis diverged twice, even at tau/2");
   RP_CUDA(cudaEventRecord(ev.ev[3], s));
+  nv.next("compose x(lambda) + recovery");
   // 6) Compose x(lambda) for every owned grid point (Horner,
   //    path_solver.cpp:64-74).
   const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
@@ -1798,6 +1827,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "gram_overlap_split") {
       require(value >= 0 && value <= 64, "gram_overlap_split must be in [0, 64]");
       ctx->gram_overlap_split = static_cast<int>(value);
+    } else if (k == "csr_l2_persist") {
+      ctx->csr_l2_persist = value != 0;
     } else if (k == "feature_shard") {
       ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {

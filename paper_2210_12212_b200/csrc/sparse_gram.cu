@@ -219,12 +219,39 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
 }
 
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
-                 const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s) {
+                 const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s,
+                 bool l2_persist) {
   if (cols <= 0 || pc.d <= 0) return;
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, 128));
   const int64_t cmax = std::min(chunk, cols);
   DBuf<double> wr(static_cast<size_t>(pc.d * cmax), s), z(static_cast<size_t>(pc.d * cmax), s);
   DBuf<double> yp(static_cast<size_t>(std::max<int64_t>(1, std::min(pc.panel_rows, pc.n)) * cmax), s);
+  struct Persist {
+    cudaStream_t s = nullptr;
+    ~Persist() {
+      if (!s) return;
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+      cudaCtxResetPersistingL2Cache();
+    }
+  } persist;
+  if (l2_persist && pc.panels > 1) {
+    int dev = 0, max_window = 0, max_persist = 0;
+    RP_CUDA(cudaGetDevice(&dev));
+    RP_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    RP_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    const size_t zbytes = static_cast<size_t>(pc.d * cmax) * sizeof(double);
+    RP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(zbytes, max_persist)));
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = z.get();
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(zbytes, static_cast<size_t>(max_window));
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(zbytes));
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    RP_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+    persist.s = s;
+  }
   for (int64_t c0 = 0; c0 < cols; c0 += chunk) {
     const int cc = static_cast<int>(std::min(chunk, cols - c0));
     transpose(W + c0 * ldw, pc.d, cc, ldw, wr.get(), cc, s);  // row-major W chunk

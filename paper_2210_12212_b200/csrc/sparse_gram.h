@@ -56,7 +56,11 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
                      int64_t nnz, int64_t panel_rows, PanelCsc& out, cudaStream_t s);
 
 // Y (d x cols, column-major, ld ldy) = M^T (M W), W (d x cols, column-major, ld ldw).
+// l2_persist: mark the running sums Z (d x chunk) as persisting in L2 for the
+// duration of the product (stream access-policy window), so the panels'
+// Y_p gathers do not evict them.
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
-                 const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s);
+                 const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s,
+                 bool l2_persist = false);
 
 }  // namespace rpb

@@ -32,10 +32,13 @@ def main():
     x = torch.randn(d * cols, dtype=torch.float64, device="cuda")
     y = torch.empty(d * cols, dtype=torch.float64, device="cuda")
     ref = None
-    combos = [(p, c) for p in (32768, 65536, 131072, 262144) for c in (64, 96, 128)]
-    for panel, chunk in combos:
+    combos = [(p, c, l2) for p in (32768, 65536, 131072) for c in (64, 128) for l2 in (0, 1)]
+    if os.environ.get("CSR_COMBOS"):
+        combos = [tuple(int(v) for v in c.split(":")) for c in os.environ["CSR_COMBOS"].split(",")]
+    for panel, chunk, l2 in combos:
         ctx.set_option("csr_panel_rows", panel)
         ctx.set_option("csr_chunk", chunk)
+        ctx.set_option("csr_l2_persist", l2)
         rp.gram_apply_raw(ctx, x.data_ptr(), cols, y.data_ptr())
         if ref is None:
             ref = y.clone()
@@ -47,7 +50,7 @@ def main():
             ts.append(rp.last_device_seconds(ctx))
         ctx.set_option("profile", 0)
         t = statistics.median(ts)
-        print(f"panel {panel:7d} chunk {chunk:3d}: {t*1e3:8.2f} ms  {t/cols*1e6:7.2f} us/col  "
+        print(f"panel {panel:7d} chunk {chunk:3d} l2persist {l2}: {t*1e3:8.2f} ms  {t/cols*1e6:7.2f} us/col  "
               f"gather {2*nnz*8*cols/t/1e12:6.2f} TB/s", flush=True)
 
 
