@@ -496,41 +496,69 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
   double zacc[MT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i) zacc[i][0] = zacc[i][1] = 0.0;
-  for (int64_t j = 0; j < cnt; ++j) {
-    const int st = static_cast<int>(j % stages);
-    mbar_wait(&full[st], static_cast<uint32_t>((j / stages) & 1));
-    const double* sg = ring + st * STAGE;
-    // y pass: yT (K x 8 rows) = W^T (K x CPW) A_blk^T (CPW x 8), four chains
+  // Software-pipelined: iteration j runs the z pass of block j interleaved
+  // with the y pass of block j + 1 (independent DMMA streams), then one CTA
+  // barrier publishes y(j + 1) and frees block j's stage for block j + stages.
+  // Partial y tiles are stored [row][K] (8 doubles per row), so the reads of
+  // the reduction below are 32 consecutive doubles (conflict-free).
+  auto y_pass_store = [&](int64_t jb) {
+    const double* sg = ring + static_cast<int>(jb % stages) * STAGE;
     double ya[4][2];
 #pragma unroll
     for (int u = 0; u < 4; ++u) ya[u][0] = ya[u][1] = 0.0;
 #pragma unroll
     for (int i = 0; i < KS; ++i) dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sg[sw64(cw + 4 * i + q4, g4)]);
-    const int buf = static_cast<int>(j & 1);
-    double* yp = ypart + (buf * kGWarps + wid) * 64;
-    yp[2 * lane] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
-    yp[2 * lane + 1] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
-    // every warp is done with block j - 1 (its z pass precedes this barrier):
-    // its stage takes block j - 1 + stages
-    __syncthreads();
-    if (t == 0 && j >= 1 && j - 1 + stages < cnt) issue(j - 1 + stages);
-    // B fragments of the z pass: y (k = row, n = K index) summed over the warps in order
-    double yb[2];
+    double* yp = ypart + (static_cast<int>(jb & 1) * kGWarps + wid) * 64;
+    yp[(2 * q4) * 8 + g4] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
+    yp[(2 * q4 + 1) * 8 + g4] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
+  };
+  auto y_sum = [&](int64_t jb, double (&yb)[2]) {  // y (k = row, n = K) summed over the warps in order
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const double* base = ypart + buf * kGWarps * 64 + g4 * 8 + 4 * h + q4;  // yT[K = g4][row = 4h + q4]
+      const double* base = ypart + static_cast<int>(jb & 1) * kGWarps * 64 + (4 * h + q4) * 8 + g4;
       double sacc = base[0];
 #pragma unroll
       for (int w2 = 1; w2 < kGWarps; ++w2) sacc += base[w2 * 64];
       yb[h] = sacc;
     }
-    // z pass: z (8 cols x K) += A_blk^T (8 cols x 8 rows) y (8 rows x K)
+  };
+  double yb[2] = {0.0, 0.0};
+  if (cnt > 0) {
+    mbar_wait(&full[0], 0);
+    y_pass_store(0);
+    __syncthreads();
+    y_sum(0, yb);
+  }
+  for (int64_t j = 0; j < cnt; ++j) {
+    const double* sg = ring + static_cast<int>(j % stages) * STAGE;
+    const bool more = j + 1 < cnt;
+    if (more) {
+      mbar_wait(&full[(j + 1) % stages], static_cast<uint32_t>(((j + 1) / stages) & 1));
+      const double* sn = ring + static_cast<int>((j + 1) % stages) * STAGE;
+      double ya[4][2];
 #pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const int c = cw + 8 * i + g4;
-      dmma(zacc[i][0], zacc[i][1], sg[sw64(c, q4)], yb[0]);
-      dmma(zacc[i][0], zacc[i][1], sg[sw64(c, 4 + q4)], yb[1]);
+      for (int u = 0; u < 4; ++u) ya[u][0] = ya[u][1] = 0.0;
+      // z pass of block j (2 MT = KS DMMAs) interleaved with the y pass of block j + 1 (KS DMMAs)
+#pragma unroll
+      for (int i = 0; i < KS; ++i) {
+        dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sn[sw64(cw + 4 * i + q4, g4)]);
+        const int it = i >> 1, hh = i & 1;
+        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + g4, 4 * hh + q4)], yb[hh]);
+      }
+      double* yp = ypart + (static_cast<int>((j + 1) & 1) * kGWarps + wid) * 64;
+      yp[(2 * q4) * 8 + g4] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
+      yp[(2 * q4 + 1) * 8 + g4] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < KS; ++i) {
+        const int it = i >> 1, hh = i & 1;
+        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + g4, 4 * hh + q4)], yb[hh]);
+      }
     }
+    // every warp is done with block j: its stage takes block j + stages
+    __syncthreads();
+    if (t == 0 && j + stages < cnt) issue(j + stages);
+    if (more) y_sum(j + 1, yb);
   }
   // this CTA's z partial: lane holds z[col = cw + 8i + g4][K = 2 q4 + e]
   double* out = ws + static_cast<int64_t>(blockIdx.x) * d * K;
@@ -707,12 +735,13 @@ bool gram_dmma_launch(const double* a, int64_t lda, int64_t n, int64_t d, const 
   }
 }
 
-// Smallest column count sent to the DMMA pass (RP_GRAM_DMMA_MIN, default 2:
-// one column stays on the SIMT column pass).
+// Smallest column count sent to the DMMA pass (RP_GRAM_DMMA_MIN, default 1:
+// every width where it applies, so a column's bits do not depend on how many
+// columns are batched with it).
 int64_t gram_dmma_min() {
   static const int64_t v = [] {
     const char* e = std::getenv("RP_GRAM_DMMA_MIN");
-    return e ? std::atoll(e) : int64_t{2};
+    return e ? std::atoll(e) : int64_t{1};
   }();
   return v;
 }
