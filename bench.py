@@ -53,6 +53,7 @@ def parse():
                     help="also time the 1-thread CPU baseline (default: on for c1-c3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="c1 only: x(lambda) vs the oracle, every rank")
+    ap.add_argument("--dump-gemm", default=None, help="write the per-launch GEMM profile of a step (JSON)")
     ap.add_argument("--path-only", action="store_true",
                     help="only the timed steps (no roofline / pass / e2e / CPU legs): for ncu launch lists")
     a = ap.parse_args()
@@ -480,6 +481,10 @@ def run_ours(args):
     ctx.set_option("gram_overlap", 1)
     ctx.set_option("profile", 0)
     l_sec, l_flops, l_bytes = rp.last_gemm_profile(ctx)  # per launch, last profiled step
+    if args.dump_gemm and rank == 0:
+        with open(args.dump_gemm, "w") as f:
+            json.dump({"seconds": list(map(float, l_sec)), "flops": list(map(float, l_flops)),
+                       "bytes": list(map(float, l_bytes))}, f)
     g_s = sum(p.gemm_seconds for p in prof)
     g_f = sum(p.gemm_flops for p in prof)
     g_calls = sum(p.gemm_calls for p in prof)

@@ -13,6 +13,7 @@
 #include "tma_util.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -949,6 +950,15 @@ int choose_split(const GemmArgs& g) {
 }
 
 namespace {
+// RP_GEMM_LOG=path: every dgemm call's shape and launch choice, one line each.
+FILE* gemm_log() {
+  static FILE* f = [] {
+    const char* e = std::getenv("RP_GEMM_LOG");
+    return e ? std::fopen(e, "w") : nullptr;
+  }();
+  return f;
+}
+
 void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   g_last_launches = 0;
   require(g.m >= 0 && g.n >= 0 && g.k >= 0 && g.batch >= 1 && g.batch2 >= 1, "dgemm: negative dimensions");
@@ -1045,6 +1055,13 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
     aligned ? launch_layout<false, false, 2>(kp, tile, stream) : launch_layout<false, false, 1>(kp, tile, stream);
   }
   g_last_launches = 1;
+  if (FILE* log = gemm_log()) {  // (tuning aid: one line per GEMM -- shape, batch, split, tile, layout)
+    std::fprintf(log, "%lld %lld %lld batch %lld split %d tile %d ak %d bk %d tma %d epi %d lower %d\n",
+                 static_cast<long long>(g.m), static_cast<long long>(g.n), static_cast<long long>(g.k),
+                 static_cast<long long>(nb), split, tile, ak ? 1 : 0, bk ? 1 : 0, (g_tma_enabled && !kp.no_tma) ? 1 : 0,
+                 static_cast<int>(kp.epi.kind), g.lower_only ? 1 : 0);
+    std::fflush(log);
+  }
   const bool defer = g.partials && split > 1 && !g.lower_only && !g.mirror && g.alpha == 1.0 && g.beta == 0.0;
   if (g.partials)
     *g.partials = defer ? Partials{kp.ws, split, g.m, g.m * g.n, split * g.m * g.n}

@@ -447,6 +447,15 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // byte-offset bits 7-8 (= (c >> 1) & 3), i.e. r ^ (c & 6) -- written so that
 // the unrolled fragment offsets fold into immediates.
 __device__ __forceinline__ int sw64(int c, int r) { return c * kGRows + (r ^ (c & 6)); }
+// Partial y tile layout: element (K, row) at (row >> 2) * 32 + (row & 3) + 4 K,
+// so the reduction's reads (lane = 4 K + (row & 3)) are 32 consecutive doubles.
+__device__ __forceinline__ int ypos(int k, int row) { return (row >> 2) * 32 + (row & 3) + 4 * k; }
+// Column order inside each 8-column block: {0, 1, 4, 5, 2, 3, 6, 7}.  A 64-bit
+// shared load is served per half-warp; with this order the 16 (column, row)
+// pairs of each half-warp fall on 16 different 8-byte banks of the swizzled
+// stage, for both fragment patterns (y pass: 4 columns x 4 rows; z pass:
+// 4 columns x 4 rows).
+__device__ __forceinline__ int perm8(int g) { return (g & 1) | ((g & 2) << 1) | ((g & 4) >> 1); }
 
 template <int NT>  // columns per warp = 32 * NT
 __global__ void __launch_bounds__(kGWarps * 32, 1)
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
   double wf[KS];
 #pragma unroll
   for (int i = 0; i < KS; ++i) {
-    const int c = cw + 4 * i + q4;
+    const int c = cw + 8 * (i >> 1) + perm8(q4 + 4 * (i & 1));  // k-step i: columns {0,1,4,5} or {2,3,6,7}
     wf[i] = (g4 < K && c < d) ? __ldg(w + c + static_cast<int64_t>(g4) * d) : 0.0;
   }
   double zacc[MT][2];
@@ -507,15 +516,15 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u) ya[u][0] = ya[u][1] = 0.0;
 #pragma unroll
-    for (int i = 0; i < KS; ++i) dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sg[sw64(cw + 4 * i + q4, g4)]);
+    for (int i = 0; i < KS; ++i) dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sg[sw64(cw + 8 * (i >> 1) + perm8(q4 + 4 * (i & 1)), g4)]);
     double* yp = ypart + (static_cast<int>(jb & 1) * kGWarps + wid) * 64;
-    yp[(2 * q4) * 8 + g4] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
-    yp[(2 * q4 + 1) * 8 + g4] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
+    yp[ypos(g4, 2 * q4)] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
+    yp[ypos(g4, 2 * q4 + 1)] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
   };
   auto y_sum = [&](int64_t jb, double (&yb)[2]) {  // y (k = row, n = K) summed over the warps in order
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const double* base = ypart + static_cast<int>(jb & 1) * kGWarps * 64 + (4 * h + q4) * 8 + g4;
+      const double* base = ypart + static_cast<int>(jb & 1) * kGWarps * 64 + ypos(g4, 4 * h + q4);  // = h*32 + lane
       double sacc = base[0];
 #pragma unroll
       for (int w2 = 1; w2 < kGWarps; ++w2) sacc += base[w2 * 64];
@@ -541,18 +550,18 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
       // z pass of block j (2 MT = KS DMMAs) interleaved with the y pass of block j + 1 (KS DMMAs)
 #pragma unroll
       for (int i = 0; i < KS; ++i) {
-        dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sn[sw64(cw + 4 * i + q4, g4)]);
+        dmma(ya[i & 3][0], ya[i & 3][1], wf[i], sn[sw64(cw + 8 * (i >> 1) + perm8(q4 + 4 * (i & 1)), g4)]);
         const int it = i >> 1, hh = i & 1;
-        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + g4, 4 * hh + q4)], yb[hh]);
+        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + perm8(g4), 4 * hh + q4)], yb[hh]);
       }
       double* yp = ypart + (static_cast<int>((j + 1) & 1) * kGWarps + wid) * 64;
-      yp[(2 * q4) * 8 + g4] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
-      yp[(2 * q4 + 1) * 8 + g4] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
+      yp[ypos(g4, 2 * q4)] = (ya[0][0] + ya[1][0]) + (ya[2][0] + ya[3][0]);
+      yp[ypos(g4, 2 * q4 + 1)] = (ya[0][1] + ya[1][1]) + (ya[2][1] + ya[3][1]);
     } else {
 #pragma unroll
       for (int i = 0; i < KS; ++i) {
         const int it = i >> 1, hh = i & 1;
-        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + g4, 4 * hh + q4)], yb[hh]);
+        dmma(zacc[it][0], zacc[it][1], sg[sw64(cw + 8 * it + perm8(g4), 4 * hh + q4)], yb[hh]);
       }
     }
     // every warp is done with block j: its stage takes block j + stages
@@ -560,11 +569,11 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
     if (t == 0 && j + stages < cnt) issue(j + stages);
     if (more) y_sum(j + 1, yb);
   }
-  // this CTA's z partial: lane holds z[col = cw + 8i + g4][K = 2 q4 + e]
+  // this CTA's z partial: lane holds z[col = cw + 8i + perm8(g4)][K = 2 q4 + e]
   double* out = ws + static_cast<int64_t>(blockIdx.x) * d * K;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int c = cw + 8 * i + g4;
+    const int c = cw + 8 * i + perm8(g4);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int k = 2 * q4 + e;

@@ -352,6 +352,8 @@ struct rp_ctx {
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   cudaStream_t side = nullptr;  // side stream: the Gram matrix overlapping the sketch and the preconditioner build
   cudaStream_t hi = nullptr;    // second stream: the sketch while the Gram matrix is in flight
+  cudaStream_t basis2 = nullptr;  // second stream of the two-group basis recursion (option "basis_streams")
+  int basis_streams = 2;          // option "basis_streams": 1 = one recursion over all intervals
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -792,12 +794,12 @@ struct PrecondBatch {
     spd_inverse_batched(h.get(), nn, nn, nn * nn, L, inv_owned.get(), nn, nn * nn, s);
   }
 
-  // A one-shift view of shift l (no copy of the factor).
-  PrecondBatch single(rp_ctx* ctx, int64_t l) const {
+  // A view of shifts [l0, l1) (no copy of the factors).
+  PrecondBatch slice(rp_ctx* ctx, int64_t l0, int64_t l1) const {
     PrecondBatch v;
     v.m = m;
     v.d = d;
-    v.L = 1;
+    v.L = l1 - l0;
     v.woodbury = woodbury;
     v.col_stable = col_stable;
     v.sa = sa;
@@ -805,13 +807,15 @@ struct PrecondBatch {
     v.f0 = f0;
     v.f1 = f1;
     v.blk = blk;
-    v.lambda0 = {lambda0[static_cast<size_t>(l)]};
-    v.d_lambda0.alloc(1, ctx->stream);
-    RP_CUDA(cudaMemcpyAsync(v.d_lambda0.get(), v.lambda0.data(), sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    v.lambda0.assign(lambda0.begin() + l0, lambda0.begin() + l1);
+    v.d_lambda0.alloc(static_cast<size_t>(v.L), ctx->stream);
+    RP_CUDA(cudaMemcpyAsync(v.d_lambda0.get(), v.lambda0.data(), sizeof(double) * v.L, cudaMemcpyHostToDevice,
+                            ctx->stream));
     RP_CUDA(cudaStreamSynchronize(ctx->stream));
-    v.inv = inv + l * n() * n();
+    v.inv = inv + l0 * n() * n();
     return v;
   }
+  PrecondBatch single(rp_ctx* ctx, int64_t l) const { return slice(ctx, l, l + 1); }
 
   // out_l (d x cols) = P_l in_l for l < L; in/out strided by `sin`/`sout`
   // (sin = 0 broadcasts one input to every interval).
@@ -1008,80 +1012,125 @@ struct BasisRun {
   std::vector<int> diverged;  // per interval
 };
 
-void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c, int64_t K,
-               const std::vector<double>& tau, const std::vector<int>& ks, BasisRun& out) {
-  cudaStream_t s = ctx->stream;
-  const int64_t L = P.L;
-  const int64_t dim = P.d;
+// The recursion as a resumable object: begin() (gen_0 = P c), step(g) for
+// g = 1 .. kmax-1, finish() (divergence flags to the host, asynchronously).
+// Every launch goes to `stream`: run_path interleaves two steppers over
+// disjoint interval groups on two streams, so one group's HBM-bound
+// preconditioner GEMMs (early generations read every P_l) overlap the other
+// group's compute-bound Gram GEMMs and the GEMMs' wave tails fill in.
+struct BasisStepper {
+  rp_ctx* ctx;
+  GramOp& gram;
+  const PrecondBatch& P;
+  BasisRun& out;
+  cudaStream_t stream;
+  int64_t K = 0, L = 0, dim = 0, NB = 0, stride_im = 0;
   int kmax = 1;
-  for (int kv : ks) {
-    require(kv >= 1, "ihs_basis: k must be >= 1");
-    kmax = std::max(kmax, kv);
-  }
-  for (double t : tau) require(t > 0.0, "ihs_basis: tau must be positive");
-  BasisDims d{dim, L, K, kmax};
-  out.dims = d;
-  out.tau = tau;
-  out.k = ks;
-  const int64_t NB = d.nb();
-  out.gen.alloc(static_cast<size_t>(dim * kmax * NB), s);
-  out.tilde.alloc(static_cast<size_t>(dim * kmax * NB), s);
-  out.d_tau.alloc(static_cast<size_t>(L), s);
-  out.d_k.alloc(static_cast<size_t>(L), s);
-  RP_CUDA(cudaMemcpyAsync(out.d_tau.get(), tau.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(out.d_k.get(), ks.data(), sizeof(int) * L, cudaMemcpyHostToDevice, s));
-  DBuf<int> flags(static_cast<size_t>(L), s);
-  RP_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * L, s));
-  // gen_0 = P c (every interval, every RHS), tilde_0 = gen_0.
-  P.apply(ctx, c, 0, K, out.gen.get(), K * dim);
-  fill(out.tilde.get(), dim * kmax * NB, 0.0, s);
-  copy_cols(out.gen.get(), dim, NB, dim, out.tilde.get(), dim, s);
-  if (kmax > 1) {
-    const int64_t stride_im = dim * kmax * K;
-    DBuf<double> args(static_cast<size_t>(L * stride_im), s);
-    DBuf<double> y(static_cast<size_t>(dim * (kmax - 1) * NB), s);  // (used when the Gram product is split)
-    DBuf<double> applied(static_cast<size_t>(L * stride_im), s);
-    if (gram.matrix && !P.woodbury) {
-      // Two kernels per generation: the Gram GEMM builds the preconditioner
-      // arguments in its epilogue, the preconditioner GEMM updates gen/tilde
-      // (and seeds the next generation's last argument column) in its own.
-      seed_args(d, out.gen.get(), args.get(), s);
-      RecursionEpilogue e;
-      e.dim = dim;
-      e.L = L;
-      e.K = K;
-      e.kmax = kmax;
-      e.tau = out.d_tau.get();
-      e.kb = out.d_k.get();
-      e.gen = out.gen.get();
-      e.tilde = out.tilde.get();
-      e.args = args.get();
-      e.flags = flags.get();
-      Partials py;
-      for (int64_t g = 1; g < kmax; ++g) {
-        nvtxRangePushA("generation");
-        e.g = g;
-        e.kind = RecursionEpilogue::kArgs;
-        gram.apply(out.gen.get(), g * NB, y.get(), &py, &e);
-        e.kind = RecursionEpilogue::kUpdate;
-        P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, nullptr, &e);
-        nvtxRangePop();
-      }
-    } else {
-      Partials py, pa;
-      for (int64_t g = 1; g < kmax; ++g) {
-        nvtxRangePushA("generation");
-        gram.apply(out.gen.get(), g * NB, y.get(), &py);
-        build_args(d, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
-        P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
-        update_gen(d, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
-        nvtxRangePop();
+  BasisDims dims{};
+  DBuf<int> flags;
+  DBuf<double> args, y, applied;
+  RecursionEpilogue e{};
+  bool fused = false;
+
+  // (the library's building blocks launch on ctx->stream: point it at ours)
+  struct Use {
+    rp_ctx* c;
+    cudaStream_t prev;
+    Use(rp_ctx* c_, cudaStream_t s) : c(c_), prev(c_->stream) { c->stream = s; }
+    ~Use() { c->stream = prev; }
+  };
+
+  BasisStepper(rp_ctx* ctx_, GramOp& gram_, const PrecondBatch& P_, BasisRun& out_, cudaStream_t st)
+      : ctx(ctx_), gram(gram_), P(P_), out(out_), stream(st) {}
+
+  void begin(const double* c, int64_t K_, const std::vector<double>& tau, const std::vector<int>& ks) {
+    Use u(ctx, stream);
+    cudaStream_t s = stream;
+    K = K_;
+    L = P.L;
+    dim = P.d;
+    for (int kv : ks) {
+      require(kv >= 1, "ihs_basis: k must be >= 1");
+      kmax = std::max(kmax, kv);
+    }
+    for (double t : tau) require(t > 0.0, "ihs_basis: tau must be positive");
+    dims = BasisDims{dim, L, K, kmax};
+    out.dims = dims;
+    out.tau = tau;
+    out.k = ks;
+    NB = dims.nb();
+    out.gen.alloc(static_cast<size_t>(dim * kmax * NB), s);
+    out.tilde.alloc(static_cast<size_t>(dim * kmax * NB), s);
+    out.d_tau.alloc(static_cast<size_t>(L), s);
+    out.d_k.alloc(static_cast<size_t>(L), s);
+    RP_CUDA(cudaMemcpyAsync(out.d_tau.get(), tau.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(out.d_k.get(), ks.data(), sizeof(int) * L, cudaMemcpyHostToDevice, s));
+    flags.alloc(static_cast<size_t>(L), s);
+    RP_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * L, s));
+    // gen_0 = P c (every interval, every RHS), tilde_0 = gen_0.
+    P.apply(ctx, c, 0, K, out.gen.get(), K * dim);
+    fill(out.tilde.get(), dim * kmax * NB, 0.0, s);
+    copy_cols(out.gen.get(), dim, NB, dim, out.tilde.get(), dim, s);
+    if (kmax > 1) {
+      stride_im = dim * kmax * K;
+      args.alloc(static_cast<size_t>(L * stride_im), s);
+      y.alloc(static_cast<size_t>(dim * (kmax - 1) * NB), s);  // (used when the Gram product is split)
+      applied.alloc(static_cast<size_t>(L * stride_im), s);
+      fused = gram.matrix && !P.woodbury;
+      if (fused) {
+        // Two kernels per generation: the Gram GEMM builds the preconditioner
+        // arguments in its epilogue, the preconditioner GEMM updates gen/tilde
+        // (and seeds the next generation's last argument column) in its own.
+        seed_args(dims, out.gen.get(), args.get(), s);
+        e.dim = dim;
+        e.L = L;
+        e.K = K;
+        e.kmax = kmax;
+        e.tau = out.d_tau.get();
+        e.kb = out.d_k.get();
+        e.gen = out.gen.get();
+        e.tilde = out.tilde.get();
+        e.args = args.get();
+        e.flags = flags.get();
       }
     }
   }
-  out.diverged.assign(static_cast<size_t>(L), 0);
-  RP_CUDA(cudaMemcpyAsync(out.diverged.data(), flags.get(), sizeof(int) * L, cudaMemcpyDeviceToHost, s));
-  RP_CUDA(cudaStreamSynchronize(s));
+
+  void step(int64_t g) {
+    if (g >= kmax) return;
+    Use u(ctx, stream);
+    cudaStream_t s = stream;
+    nvtxRangePushA("generation");
+    if (fused) {
+      Partials py;
+      e.g = g;
+      e.kind = RecursionEpilogue::kArgs;
+      gram.apply(out.gen.get(), g * NB, y.get(), &py, &e);
+      e.kind = RecursionEpilogue::kUpdate;
+      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, nullptr, &e);
+    } else {
+      Partials py, pa;
+      gram.apply(out.gen.get(), g * NB, y.get(), &py);
+      build_args(dims, g, py, out.gen.get(), out.d_tau.get(), args.get(), s);
+      P.apply(ctx, args.get(), stride_im, (g + 1) * K, applied.get(), stride_im, &pa);
+      update_gen(dims, g, pa, out.d_k.get(), out.gen.get(), out.tilde.get(), flags.get(), s);
+    }
+    nvtxRangePop();
+  }
+
+  void finish() {
+    out.diverged.assign(static_cast<size_t>(L), 0);
+    RP_CUDA(cudaMemcpyAsync(out.diverged.data(), flags.get(), sizeof(int) * L, cudaMemcpyDeviceToHost, stream));
+  }
+};
+
+void run_basis(rp_ctx* ctx, GramOp& gram, const PrecondBatch& P, const double* c, int64_t K,
+               const std::vector<double>& tau, const std::vector<int>& ks, BasisRun& out) {
+  BasisStepper b(ctx, gram, P, out, ctx->stream);
+  b.begin(c, K, tau, ks);
+  for (int64_t g = 1; g < b.kmax; ++g) b.step(g);
+  b.finish();
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // ---- helpers for host/device buffers -------------------------------------------
@@ -1396,14 +1445,53 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   }
   // 5) Bases for all owned intervals at once; diverged intervals are retried
   //    at tau/2 (path_solver.cpp:132-140).
-  BasisRun run, run2;
+  BasisRun run2;
+  // the first attempt's bases: one run over all owned intervals, or (option
+  // "basis_streams" = 2, Gram-matrix mode, explicit P) two runs over the two
+  // halves of the intervals, interleaved generation by generation on two
+  // streams (BasisStepper); part p covers own positions [pbeg[p], pend[p])
+  std::vector<BasisRun> runs(1);
+  std::vector<int64_t> pbeg{0}, pend{Lo};
   std::vector<int64_t> retry;             // positions in `own`
   std::vector<int> retry_slot(static_cast<size_t>(Lo), -1);
   int failed = 0;
   if (Lo > 0) {
-    run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, run);
-    for (int64_t i = 0; i < Lo; ++i)
-      if (run.diverged[i]) retry.push_back(i);
+    const bool two = ctx->basis_streams >= 2 && gram.matrix && !P.woodbury && Lo >= 2;
+    if (!two) {
+      run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, runs[0]);
+    } else {
+      if (!ctx->basis2) RP_CUDA(cudaStreamCreateWithFlags(&ctx->basis2, cudaStreamNonBlocking));
+      const int64_t h = (Lo + 1) / 2;
+      runs.resize(2);
+      pbeg = {0, h};
+      pend = {h, Lo};
+      const PrecondBatch PA = P.slice(ctx, 0, h), PB = P.slice(ctx, h, Lo);
+      cudaEvent_t fork;
+      RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      RP_CUDA(cudaEventRecord(fork, s));
+      RP_CUDA(cudaStreamWaitEvent(ctx->basis2, fork, 0));
+      {
+        BasisStepper A(ctx, gram, PA, runs[0], s), B(ctx, gram, PB, runs[1], ctx->basis2);
+        A.begin(cbuf.get(), K, std::vector<double>(taus.begin(), taus.begin() + h),
+                std::vector<int>(ks.begin(), ks.begin() + h));
+        B.begin(cbuf.get(), K, std::vector<double>(taus.begin() + h, taus.end()),
+                std::vector<int>(ks.begin() + h, ks.end()));
+        for (int64_t g = 1; g < std::max(A.kmax, B.kmax); ++g) {
+          A.step(g);
+          B.step(g);
+        }
+        A.finish();
+        B.finish();
+        RP_CUDA(cudaEventRecord(fork, ctx->basis2));  // (the steppers' buffers are freed on their streams)
+      }
+      RP_CUDA(cudaStreamWaitEvent(s, fork, 0));
+      RP_CUDA(cudaStreamSynchronize(s));
+      RP_CUDA(cudaStreamSynchronize(ctx->basis2));
+      RP_CUDA(cudaEventDestroy(fork));
+    }
+    for (size_t q = 0; q < runs.size(); ++q)
+      for (int64_t i = pbeg[q]; i < pend[q]; ++i)
+        if (runs[q].diverged[static_cast<size_t>(i - pbeg[q])]) retry.push_back(i);
     if (!retry.empty()) {
       PrecondBatch P2;
       std::vector<double> l0r, taur;
@@ -1439,18 +1527,21 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   const int64_t T = static_cast<int64_t>(cfg.lambdas.size());
   DBuf<double> xs(static_cast<size_t>(dim * K * T), s);
   if (split) fill(xs.get(), dim * K * T, 0.0, s);
-  for (int pass = 0; pass < 2; ++pass) {
-    BasisRun& R = pass == 0 ? run : run2;
-    if (pass == 1 && retry.empty()) break;
+  const size_t nparts = runs.size();
+  for (size_t pass = 0; pass <= nparts; ++pass) {
+    const bool retry_pass = pass == nparts;
+    BasisRun& R = retry_pass ? run2 : runs[pass];
+    if (retry_pass && retry.empty()) break;
     std::vector<double> lam;
     std::vector<int> itv;
     std::vector<int64_t> tidx;
-    for (int64_t i = 0; i < Lo; ++i) {
-      const bool mine = (pass == 0) ? retry_slot[i] < 0 : retry_slot[i] >= 0;
+    const int64_t i0 = retry_pass ? 0 : pbeg[pass], i1 = retry_pass ? Lo : pend[pass];
+    for (int64_t i = i0; i < i1; ++i) {
+      const bool mine = retry_pass ? retry_slot[i] >= 0 : retry_slot[i] < 0;
       if (!mine) continue;
       for (int64_t t : plans[own[i]].grid) {
         lam.push_back(cfg.lambdas[t]);
-        itv.push_back(pass == 0 ? static_cast<int>(i) : retry_slot[i]);
+        itv.push_back(retry_pass ? retry_slot[i] : static_cast<int>(i - i0));
         tidx.push_back(t);
       }
     }
@@ -1784,6 +1875,11 @@ void rp_destroy(rp_ctx* ctx) {
       cudaStreamSynchronize(ctx->hi);
       cudaStreamDestroy(ctx->hi);
     }
+    if (ctx->basis2) {
+      release_workspace(ctx->basis2);
+      cudaStreamSynchronize(ctx->basis2);
+      cudaStreamDestroy(ctx->basis2);
+    }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
     if (ctx->own) {
@@ -1829,6 +1925,9 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->gram_overlap_split = static_cast<int>(value);
     } else if (k == "csr_l2_persist") {
       ctx->csr_l2_persist = value != 0;
+    } else if (k == "basis_streams") {
+      require(value == 1 || value == 2, "basis_streams must be 1 or 2");
+      ctx->basis_streams = static_cast<int>(value);
     } else if (k == "feature_shard") {
       ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {

@@ -395,3 +395,23 @@ def test_c2_full_size_every_interval_parity(rp, ctx, oracle):
     worst, n = _worst(got.points, ref.points, oracle)
     print(f"C2 full, every interval: {n} lambdas, max rel err {worst:.3e}")
     assert n == w.T and worst < TOL
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c2", 1 / 8)])
+def test_two_stream_basis_bitwise(rp, ctx, oracle, name, scale):
+    """The two-group basis recursion on two streams (option basis_streams = 2,
+    the default in Gram-matrix mode) gives x(lambda) bit-identical to one
+    recursion over all intervals: every GEMM is column-stable, so a column's
+    bits do not depend on how many intervals share the launch."""
+    w = workloads.get(name, scale=scale)
+    _, (ga, gcfg, gspec, grho) = _mirror(rp, oracle, w)
+    xs = {}
+    try:
+        for mode in (1, 2):
+            ctx.set_option("basis_streams", mode)
+            got = rp.ihs_bin_path(ga, w.b, gcfg, gspec, grho, ctx=ctx)
+            assert got.timings["gram_mode"] == 1
+            xs[mode] = np.stack([p.solution for p in got.points])
+    finally:
+        ctx.set_option("basis_streams", 2)
+    assert np.array_equal(xs[1], xs[2])
