@@ -33,7 +33,7 @@ def main(csv_path, log_path, steps=1):
     off = len(gk) - n  # align on the last calls (the profiled steps)
     for (name, t), g in zip(gk[off:], gemms[len(gemms) - n:]):
         m, nn, k = int(g[0]), int(g[1]), int(g[2])
-        batch, split, tile, epi = int(g[4]), int(g[6]), int(g[8]), int(g[18])
+        batch, split, tile, epi = int(g[4]), int(g[6]), int(g[8]), int(g[16])
         fl = 2.0 * m * nn * k * batch
         key = f"m{m} k{k} batch{batch} epi{epi} n{'<=64' if nn <= 64 else '>64'}"
         c = cls[key]
