@@ -69,6 +69,9 @@ struct KParams {
   int64_t stride_a2, stride_b2, stride_c2;
   int split;        // number of K splits
   int64_t k_chunk;  // K per split (multiple of the tile K)
+  int vchunk;       // > 0: "virtual split" -- one CTA per tile runs every K chunk of vchunk k-tiles, each
+                    // chunk accumulated from zero and added to the running total in chunk order: the bits
+                    // of a real split (partials summed 0..S-1), without partials or a consumer kernel
   double* ws;       // split partials: [batch][split][n][m]
   bool lower_only;
   bool mirror;  // lower_only: also write the transposed element (C symmetric)
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
 // (conflict-free fragment loads); the extra elements are never read.  The
 // arithmetic (k order, fragment mapping, epilogue) is the cp.async kernel's,
 // so both produce identical bits.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool VS>
 __global__ void __launch_bounds__((WM * WN + 1) * 32)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, KParams p,
                      int a_batched, int a_batched2, int b_batched, int b_batched2) {
@@ -572,6 +575,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32)
     const int k4 = lane & 3;
     int stage = 0;
     uint32_t phase = 0;
+    double tot[VS ? C::FM : 1][VS ? C::FN : 1][2];  // (virtual split: the running total over chunks)
     for (int kt = 0; kt < ktiles; ++kt) {
       tma::mbar_wait(&full[stage], phase);
       const double* as = As + stage * C::A_STAGE;
@@ -600,6 +604,28 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32)
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
+      }
+      if constexpr (VS) {
+        if ((kt + 1) % p.vchunk == 0 || kt + 1 == ktiles) {
+          const bool first = kt < p.vchunk;
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                tot[i][j][e] = first ? acc[i][j][e] : __dadd_rn(tot[i][j][e], acc[i][j][e]);
+                acc[i][j][e] = 0.0;
+              }
+        }
+      }
+    }
+    if constexpr (VS) {
+      if (ktiles > 0) {
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) acc[i][j][0] = tot[i][j][0], acc[i][j][1] = tot[i][j][1];
       }
     }
   }
@@ -712,7 +738,15 @@ bool operand_map(CUtensorMap* map, const double* base, int64_t inner, int64_t ou
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+// Tiles whose per-warp accumulators fit twice in registers (the virtual split
+// keeps a running total beside the chunk accumulator): 2 x 2 warps with warp
+// tiles of at most 32 x 32 (64 x 64, 64 x 48, 64 x 32 -- no spills).
+template <int BM, int BN, int WM, int WN>
+constexpr bool vsplit_tile() {
+  return WM * WN == 4 && (BM / WM) <= 32 && (BN / WN) <= 32;  // (2 x 2 warps: room for both register sets)
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool VS>
 bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
   CUtensorMap amap, bmap;
@@ -728,7 +762,7 @@ bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
                         : operand_map(&bmap, kp.b, kp.n, kp.k, kp.ldb, kp.stride_b, kp.batch, kp.stride_b2,
                                       kp.batch2, BN + 4, BK, &bb1, &bb2);
   if (!ok_b) return false;
-  auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
+  auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VS>;
   constexpr int smem = C::SMEM_BYTES + 128;
   static std::atomic<bool> attr_set[kMaxDevices];  // per template instantiation and device
   const int dev = current_device();
@@ -757,10 +791,14 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM,
 void launch_cfg(const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
   if constexpr (VEC == 2) {
-    if (g_tma_enabled && !kp.no_tma && ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535 &&
-        launch_tma_cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>(kp, stream))
-      return;
+    if (g_tma_enabled && !kp.no_tma && ceil_div(kp.n, BN) <= 65535 && kp.batch * kp.batch2 * kp.split <= 65535) {
+      if constexpr (vsplit_tile<BM, BN, WM, WN>() && BK == 16) {
+        if (kp.vchunk > 0 && launch_tma_cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, true>(kp, stream)) return;
+      }
+      if (kp.vchunk == 0 && launch_tma_cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, false>(kp, stream)) return;
+    }
   }
+  require(kp.vchunk == 0, "dgemm: virtual split needs the TMA kernel");
   auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
   static std::atomic<bool> attr_set[kMaxDevices];  // per template instantiation and device
   const int dev = current_device();
@@ -831,7 +869,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 int dgemm_last_launches() { return g_last_launches; }
 
-int dgemm_split(const GemmArgs& g) { return choose_split(g); }
+namespace {
+bool vsplit_planned(const GemmArgs& g);
+}
+// The effective split: a split that runs as a virtual split is no split for
+// the caller (no partials; a fused epilogue is allowed).
+int dgemm_split(const GemmArgs& g) {
+  const int s = choose_split(g);
+  return (s > 1 && vsplit_planned(g)) ? 1 : s;
+}
 
 namespace {
 thread_local GemmProfiler* g_prof = nullptr;
@@ -959,6 +1005,71 @@ FILE* gemm_log() {
   return f;
 }
 
+// Tile choice: estimated time = waves x per-wave tile work, where a wave is
+// 148 SMs x CTAs-per-SM for the shape (ties keep the larger tile).  With the
+// virtual split only the tiles whose accumulators fit twice are candidates.
+// CTAs per SM and relative large-problem throughput per shape (measured,
+// profiles/r01_gemm_tune.txt; 9, 10 = BK 32 variants, kept for tuning only;
+// the 4-warp shapes 7, 8 only pay off in the cp.async kernel; the 48-wide
+// tile only where N fits one of them and a 64-wide tile would pad a quarter
+// or more: 24 % faster there, profiles/r01_gemm_tune_bn48.txt).
+constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2};
+constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0};
+constexpr bool kVsTile[] = {false, true, false, true, false, false, false, false, false, false, false, true, false};
+
+int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
+  const int64_t nb = g.batch * g.batch2;
+  int tile = 0;
+  double best = 1e300;
+  for (int t = 0; t < kNumTiles; ++t) {
+    if (kTiles[t].bn == 16 && g.n > 16) continue;
+    if (kTiles[t].bn == 48 && (g.n <= 32 || g.n > 48)) continue;
+    if (kEff[t] <= 0.0) continue;
+    if (vs && !kVsTile[t]) continue;
+    if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;  // (a split's last k tile must not cross into the next)
+    const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
+    const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));
+    const double cost = waves * kTiles[t].bm * kTiles[t].bn * kOcc[t] / kEff[t];
+    if (cost < best * 0.999) {
+      best = cost;
+      tile = t;
+    }
+  }
+  return tile;
+}
+
+// RP_GEMM_VSPLIT=0 disables the virtual split (A/B).
+bool g_vsplit_enabled = [] {
+  const char* e = std::getenv("RP_GEMM_VSPLIT");
+  return !(e && e[0] == '0');
+}();
+
+// A column-stable split product runs as a virtual split (one CTA per tile,
+// the chunks summed in order inside it) when the tiles alone fill the GPU:
+// same bits, no partials round trip, and a fused epilogue becomes possible.
+bool use_vsplit(const GemmArgs& g, int split, int64_t k_chunk, bool aligned) {
+  if (!g_vsplit_enabled || split <= 1 || !g.col_stable || g.lower_only || g.tri_k || g.no_tma || !g_tma_enabled ||
+      !aligned || g.force_tile >= 0 || g.split_k > 0 || k_chunk % 16 != 0)
+    return false;
+  const int t = choose_tile(g, 1, k_chunk, true);
+  const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * g.batch * g.batch2;
+  return ctas >= 148 * kOcc[t];  // at least one full wave without the split
+}
+
+bool operands_aligned(const GemmArgs& g) {
+  return (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) && (reinterpret_cast<uintptr_t>(g.b) % 16 == 0) &&
+         g.lda % 2 == 0 && g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
+         g.stride_b2 % 2 == 0;
+}
+
+bool vsplit_planned(const GemmArgs& g) {
+  int split = choose_split(g);
+  int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
+  if (k_chunk == 0) k_chunk = 16;
+  split = static_cast<int>(std::max<int64_t>(1, ceil_div(g.k, k_chunk)));
+  return use_vsplit(g, split, k_chunk, operands_aligned(g));
+}
+
 void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   g_last_launches = 0;
   require(g.m >= 0 && g.n >= 0 && g.k >= 0 && g.batch >= 1 && g.batch2 >= 1, "dgemm: negative dimensions");
@@ -990,10 +1101,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
 
   const bool ak = g.opa == Op::T;  // A contiguous along k
   const bool bk = g.opb == Op::N;  // B contiguous along k
-  const bool aligned = (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(g.b) % 16 == 0) && g.lda % 2 == 0 &&
-                       g.ldb % 2 == 0 && g.stride_a % 2 == 0 && g.stride_b % 2 == 0 && g.stride_a2 % 2 == 0 &&
-                       g.stride_b2 % 2 == 0;
+  const bool aligned = operands_aligned(g);
 
   int split = choose_split(g);
   int64_t k_chunk = ceil_div(ceil_div(g.k, split), 16) * 16;
@@ -1002,34 +1110,12 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   kp.split = split;
   kp.k_chunk = k_chunk;
 
-  // Tile choice: estimated time = waves x per-wave tile work, where a wave is
-  // 148 SMs x CTAs-per-SM for the shape (ties keep the larger tile).
-  int tile = 0;
-  {
-    // CTAs per SM and relative large-problem throughput per shape (measured,
-    // profiles/gemm_tune_r01.txt)
-    // (profiles/r01_gemm_tune.txt: large-problem throughput relative to the
-    // best shape; 9, 10 = BK 32 variants, kept for tuning only)
-    // (TMA kernel, the default path; the 4-warp shapes 7, 8 only pay off in
-    // the cp.async kernel)
-    static constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2};
-    // (the 48-wide tile only where N fits one of them and a 64-wide tile
-    // would pad a quarter or more: 24 % faster there, profiles/r01_gemm_tune_bn48.txt)
-    static constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0};
-    double best = 1e300;
-    for (int t = 0; t < kNumTiles; ++t) {
-      if (kTiles[t].bn == 16 && g.n > 16) continue;
-      if (kTiles[t].bn == 48 && (g.n <= 32 || g.n > 48)) continue;
-      if (kEff[t] <= 0.0) continue;
-      if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;  // (a split's last k tile must not cross into the next)
-      const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
-      const double waves = static_cast<double>(ceil_div(ctas, 148 * kOcc[t]));
-      const double cost = waves * kTiles[t].bm * kTiles[t].bn * kOcc[t] / kEff[t];
-      if (cost < best * 0.999) {
-        best = cost;
-        tile = t;
-      }
-    }
+  const bool vs = use_vsplit(g, split, k_chunk, aligned);
+  int tile = choose_tile(g, vs ? 1 : split, k_chunk, vs);
+  if (vs) {
+    kp.split = 1;
+    kp.vchunk = static_cast<int>(k_chunk / 16);
+    split = 1;
   }
   if (g.force_tile >= 0 && g.force_tile < kNumTiles) {
     // The kernels do not mask k past their split's end: a tile's BK must
