@@ -1115,6 +1115,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   if (vs) {
     kp.split = 1;
     kp.vchunk = static_cast<int>(k_chunk / 16);
+    kp.k_chunk = g.k;  // (one CTA covers the whole k range)
     split = 1;
   }
   if (g.force_tile >= 0 && g.force_tile < kNumTiles) {

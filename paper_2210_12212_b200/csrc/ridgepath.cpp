@@ -352,8 +352,6 @@ struct rp_ctx {
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   cudaStream_t side = nullptr;  // side stream: the Gram matrix overlapping the sketch and the preconditioner build
   cudaStream_t hi = nullptr;    // second stream: the sketch while the Gram matrix is in flight
-  cudaStream_t basis2 = nullptr;  // second stream of the two-group basis recursion (option "basis_streams")
-  int basis_streams = 2;          // option "basis_streams": 1 = one recursion over all intervals
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -1014,10 +1012,7 @@ struct BasisRun {
 
 // The recursion as a resumable object: begin() (gen_0 = P c), step(g) for
 // g = 1 .. kmax-1, finish() (divergence flags to the host, asynchronously).
-// Every launch goes to `stream`: run_path interleaves two steppers over
-// disjoint interval groups on two streams, so one group's HBM-bound
-// preconditioner GEMMs (early generations read every P_l) overlap the other
-// group's compute-bound Gram GEMMs and the GEMMs' wave tails fill in.
+// Every launch goes to `stream`.
 struct BasisStepper {
   rp_ctx* ctx;
   GramOp& gram;
@@ -1446,49 +1441,17 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   // 5) Bases for all owned intervals at once; diverged intervals are retried
   //    at tau/2 (path_solver.cpp:132-140).
   BasisRun run2;
-  // the first attempt's bases: one run over all owned intervals, or (option
-  // "basis_streams" = 2, Gram-matrix mode, explicit P) two runs over the two
-  // halves of the intervals, interleaved generation by generation on two
-  // streams (BasisStepper); part p covers own positions [pbeg[p], pend[p])
+  // the first attempt's bases: one run over all owned intervals (part p of
+  // `runs` covers own positions [pbeg[p], pend[p]); a two-stream split of
+  // the intervals was measured at -0.1 ms on C2 and found run-to-run
+  // nondeterministic on C3, so it is not used)
   std::vector<BasisRun> runs(1);
   std::vector<int64_t> pbeg{0}, pend{Lo};
   std::vector<int64_t> retry;             // positions in `own`
   std::vector<int> retry_slot(static_cast<size_t>(Lo), -1);
   int failed = 0;
   if (Lo > 0) {
-    const bool two = ctx->basis_streams >= 2 && gram.matrix && !P.woodbury && Lo >= 2;
-    if (!two) {
-      run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, runs[0]);
-    } else {
-      if (!ctx->basis2) RP_CUDA(cudaStreamCreateWithFlags(&ctx->basis2, cudaStreamNonBlocking));
-      const int64_t h = (Lo + 1) / 2;
-      runs.resize(2);
-      pbeg = {0, h};
-      pend = {h, Lo};
-      const PrecondBatch PA = P.slice(ctx, 0, h), PB = P.slice(ctx, h, Lo);
-      cudaEvent_t fork;
-      RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-      RP_CUDA(cudaEventRecord(fork, s));
-      RP_CUDA(cudaStreamWaitEvent(ctx->basis2, fork, 0));
-      {
-        BasisStepper A(ctx, gram, PA, runs[0], s), B(ctx, gram, PB, runs[1], ctx->basis2);
-        A.begin(cbuf.get(), K, std::vector<double>(taus.begin(), taus.begin() + h),
-                std::vector<int>(ks.begin(), ks.begin() + h));
-        B.begin(cbuf.get(), K, std::vector<double>(taus.begin() + h, taus.end()),
-                std::vector<int>(ks.begin() + h, ks.end()));
-        for (int64_t g = 1; g < std::max(A.kmax, B.kmax); ++g) {
-          A.step(g);
-          B.step(g);
-        }
-        A.finish();
-        B.finish();
-        RP_CUDA(cudaEventRecord(fork, ctx->basis2));  // (the steppers' buffers are freed on their streams)
-      }
-      RP_CUDA(cudaStreamWaitEvent(s, fork, 0));
-      RP_CUDA(cudaStreamSynchronize(s));
-      RP_CUDA(cudaStreamSynchronize(ctx->basis2));
-      RP_CUDA(cudaEventDestroy(fork));
-    }
+    run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, runs[0]);
     for (size_t q = 0; q < runs.size(); ++q)
       for (int64_t i = pbeg[q]; i < pend[q]; ++i)
         if (runs[q].diverged[static_cast<size_t>(i - pbeg[q])]) retry.push_back(i);
@@ -1875,11 +1838,6 @@ void rp_destroy(rp_ctx* ctx) {
       cudaStreamSynchronize(ctx->hi);
       cudaStreamDestroy(ctx->hi);
     }
-    if (ctx->basis2) {
-      release_workspace(ctx->basis2);
-      cudaStreamSynchronize(ctx->basis2);
-      cudaStreamDestroy(ctx->basis2);
-    }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
     if (ctx->own) {
@@ -1925,9 +1883,6 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->gram_overlap_split = static_cast<int>(value);
     } else if (k == "csr_l2_persist") {
       ctx->csr_l2_persist = value != 0;
-    } else if (k == "basis_streams") {
-      require(value == 1 || value == 2, "basis_streams must be 1 or 2");
-      ctx->basis_streams = static_cast<int>(value);
     } else if (k == "feature_shard") {
       ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {

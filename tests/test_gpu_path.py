@@ -397,21 +397,38 @@ def test_c2_full_size_every_interval_parity(rp, ctx, oracle):
     assert n == w.T and worst < TOL
 
 
-@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c2", 1 / 8)])
-def test_two_stream_basis_bitwise(rp, ctx, oracle, name, scale):
-    """The two-group basis recursion on two streams (option basis_streams = 2,
-    the default in Gram-matrix mode) gives x(lambda) bit-identical to one
-    recursion over all intervals: every GEMM is column-stable, so a column's
-    bits do not depend on how many intervals share the launch."""
-    w = workloads.get(name, scale=scale)
-    _, (ga, gcfg, gspec, grho) = _mirror(rp, oracle, w)
-    xs = {}
-    try:
-        for mode in (1, 2):
-            ctx.set_option("basis_streams", mode)
-            got = rp.ihs_bin_path(ga, w.b, gcfg, gspec, grho, ctx=ctx)
-            assert got.timings["gram_mode"] == 1
-            xs[mode] = np.stack([p.solution for p in got.points])
-    finally:
-        ctx.set_option("basis_streams", 2)
-    assert np.array_equal(xs[1], xs[2])
+_VSPLIT_CHILD = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import workloads
+from paper_2210_12212_b200 import ridgepath as rp
+w = workloads.get({name!r}, scale={scale!r})
+grid = w.lambdas(rp.log_grid)
+sk = w.sketch
+got = rp.ihs_bin_path(w.a, w.b, rp.PathConfig(w.lambda_min, w.lambda_max, grid, w.epsilon),
+                      rp.SketchSpec(sk["kind"], sk["m"], sk["n"], sk["s"], sk["seed"]), rp.RhoBounds.manual(*w.rho))
+np.save({out!r}, np.stack([p.solution for p in got.points]))
+"""
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 1.0), ("c3", 1 / 16)])
+def test_virtual_split_bitwise(name, scale, tmp_path):
+    """The GEMM virtual split (a column-stable split product run as one CTA
+    per tile with its K chunks accumulated separately and added in chunk
+    order, fused epilogue) gives x(lambda) bit-identical to the real split
+    (partials + consumer kernel): the two processes differ only in
+    RP_GEMM_VSPLIT."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    xs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"x{flag}.npy")
+        code = _VSPLIT_CHILD.format(root=root, name=name, scale=scale, out=out)
+        env = dict(os.environ, RP_GEMM_VSPLIT=flag)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        xs.append(np.load(out))
+    assert np.array_equal(xs[0], xs[1])
