@@ -1038,10 +1038,15 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   return tile;
 }
 
-// RP_GEMM_VSPLIT=0 disables the virtual split (A/B).
+// RP_GEMM_VSPLIT=1 enables the virtual split.  Off by default: measured on
+// C2 it loses -- the second register set costs the 64 x 64 tile its second
+// CTA per SM (255 registers; capped at 168 it spills), and one CTA per tile
+// quantizes worse than the real split's four (path 19.9 vs 18.7 ms,
+// profiles/r02_vsplit_c2.txt).  Bit-identical either way
+// (test_virtual_split_bitwise).
 bool g_vsplit_enabled = [] {
   const char* e = std::getenv("RP_GEMM_VSPLIT");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }();
 
 // A column-stable split product runs as a virtual split (one CTA per tile,

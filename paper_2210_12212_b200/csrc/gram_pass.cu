@@ -419,11 +419,12 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
 //     column segments) into a shared-memory ring with 2-D TMA boxes of
 //     8 x 256, 64B-swizzled (both fragment patterns below are then
 //     conflict-free);
-//   * eight consumer warps own d/8 columns each.  y pass:
+//   * the CTA's NW warps (16; 8 with RP_GRAM_DMMA_WARPS=8) own d/NW columns
+//     each.  y pass:
 //     y_blk^T (K x 8 rows) = W^T A_blk^T with W^T as the register-resident A
 //     operand and the stage as the B operand, four accumulator chains;
-//   * the eight partial y tiles meet in shared memory (one named barrier per
-//     block, summed in warp order), then the z pass
+//   * the NW partial y tiles meet in shared memory (one barrier per block,
+//     summed in warp order), then the z pass
 //     z[cols] (8 cols x K) += A_blk^T y_blk reads the same stage again as the
 //     A operand: z stays in registers for the whole kernel;
 //   * per-CTA z partials are summed in CTA order (sum_chunks_tree_kernel).
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
 // HBM roof on B200.
 
 constexpr int kGRows = 8;     // rows per block
-constexpr int kGWarps = 8;    // consumer warps
+constexpr int kGWarpsMax = 16;  // warps per CTA (template NW: 8 or 16)
 constexpr int kGBox = 256;    // columns per TMA box
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -457,14 +458,16 @@ __device__ __forceinline__ int ypos(int k, int row) { return (row >> 2) * 32 + (
 // 4 columns x 4 rows).
 __device__ __forceinline__ int perm8(int g) { return (g & 1) | ((g & 2) << 1) | ((g & 4) >> 1); }
 
-template <int NT>  // columns per warp = 32 * NT
-__global__ void __launch_bounds__(kGWarps * 32, 1)
+template <int NT, int NW>  // NW warps, 256 * NT / NW * 8 ... columns per warp = 256 * NT / NW
+__global__ void __launch_bounds__(NW * 32, 1)
     gram_dmma_kernel(const __grid_constant__ CUtensorMap map, int64_t n, int64_t d, int K,
                      const double* __restrict__ w, double* __restrict__ ws, int stages) {
-  constexpr int CPW = 32 * NT;       // columns per warp
+  constexpr int kGWarps = NW;
+  constexpr int CPW = 256 * NT / NW;  // columns per warp (multiple of 8)
+  static_assert(CPW % 8 == 0, "columns per warp");
   constexpr int KS = CPW / 4;        // k-steps of the y pass (also W fragments)
   constexpr int MT = CPW / 8;        // 8-column tiles of the z pass
-  constexpr int DPAD = CPW * kGWarps;
+  constexpr int DPAD = CPW * kGWarps;  // = 256 * NT
   constexpr int STAGE = DPAD * kGRows;  // doubles
   extern __shared__ __align__(1024) double sm_raw[];
   double* ring = sm_raw + (((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u) >> 3);
@@ -705,10 +708,11 @@ void atv_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double
 
 
 // The DMMA Gram pass (k <= 8 columns, d <= 5 * 256): false if it does not apply.
-template <int NT>
+template <int NT, int NW>
 bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
                          cudaStream_t s) {
-  constexpr int DPAD = 32 * NT * kGWarps;
+  constexpr int kGWarps = NW;
+  constexpr int DPAD = 256 * NT;
   CUtensorMap map;
   if (!operator_tensor_map(&map, a, lda, n, d, kGRows, kGBox, false, true)) return false;
   constexpr size_t stage_bytes = static_cast<size_t>(DPAD) * kGRows * sizeof(double);
@@ -723,8 +727,8 @@ bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, con
   const int64_t nb = (n + kGRows - 1) / kGRows;
   const int grid = static_cast<int>(std::min<int64_t>(nb, sms));
   DBuf<double> ws(static_cast<size_t>(grid) * d * k, s);
-  ensure_dynamic_smem(gram_dmma_kernel<NT>, smem);
-  gram_dmma_kernel<NT><<<grid, kGWarps * 32, smem, s>>>(map, n, d, static_cast<int>(k), w, ws.get(), stages);
+  ensure_dynamic_smem(gram_dmma_kernel<NT, NW>, smem);
+  gram_dmma_kernel<NT, NW><<<grid, NW * 32, smem, s>>>(map, n, d, static_cast<int>(k), w, ws.get(), stages);
   RP_LAUNCH_CHECK();
   sum_chunks_tree_kernel<<<static_cast<unsigned>(ceil_div(d * k, 16)), 256, 0, s>>>(ws.get(), grid, d * k, z);
   RP_LAUNCH_CHECK();
@@ -734,12 +738,16 @@ bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, con
 bool gram_dmma_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
                       cudaStream_t s) {
   if (k < 1 || k > 8 || n <= 0 || d <= 0 || lda % 2 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) return false;
-  switch (ceil_div(d, 32 * kGWarps)) {
-    case 1: return gram_dmma_launch_nt<1>(a, lda, n, d, w, k, z, s);
-    case 2: return gram_dmma_launch_nt<2>(a, lda, n, d, w, k, z, s);
-    case 3: return gram_dmma_launch_nt<3>(a, lda, n, d, w, k, z, s);
-    case 4: return gram_dmma_launch_nt<4>(a, lda, n, d, w, k, z, s);
-    case 5: return gram_dmma_launch_nt<5>(a, lda, n, d, w, k, z, s);
+  // (RP_GRAM_DMMA_WARPS=8: eight warps per CTA instead of sixteen -- A/B)
+  static const bool w8 = [] {
+    const char* e = std::getenv("RP_GRAM_DMMA_WARPS");
+    return e && std::atoi(e) == 8;
+  }();
+  switch (ceil_div(d, 256)) {
+    case 1: return w8 ? gram_dmma_launch_nt<1, 8>(a, lda, n, d, w, k, z, s) : gram_dmma_launch_nt<1, 16>(a, lda, n, d, w, k, z, s);
+    case 2: return w8 ? gram_dmma_launch_nt<2, 8>(a, lda, n, d, w, k, z, s) : gram_dmma_launch_nt<2, 16>(a, lda, n, d, w, k, z, s);
+    case 3: return w8 ? gram_dmma_launch_nt<3, 8>(a, lda, n, d, w, k, z, s) : gram_dmma_launch_nt<3, 16>(a, lda, n, d, w, k, z, s);
+    case 4: return w8 ? gram_dmma_launch_nt<4, 8>(a, lda, n, d, w, k, z, s) : gram_dmma_launch_nt<4, 16>(a, lda, n, d, w, k, z, s);
     default: return false;
   }
 }

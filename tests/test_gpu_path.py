@@ -424,7 +424,7 @@ def test_virtual_split_bitwise(name, scale, tmp_path):
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     xs = []
-    for flag in ("1", "0"):
+    for flag in ("1", "0"):  # (the virtual split is opt-in: RP_GEMM_VSPLIT=1)
         out = str(tmp_path / f"x{flag}.npy")
         code = _VSPLIT_CHILD.format(root=root, name=name, scale=scale, out=out)
         env = dict(os.environ, RP_GEMM_VSPLIT=flag)
