@@ -821,9 +821,13 @@ struct TileShape {
   int bm, bn;
 };
 constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128, 16}, {64, 128},
-                                {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}, {64, 48}, {128, 48}};
-constexpr int kNumTiles = 13;
-constexpr int kTileBK[kNumTiles] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16};  // (launch_layout)
+                                 {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}, {64, 48}, {128, 48},
+                                 // narrow N (the recursion's batched preconditioner GEMM, N = g + 1 <= 64):
+                                 // 128-row tiles of 4 x 1 warps in steps of 8 columns
+                                 {128, 24},  {128, 40}, {128, 48}, {128, 56}, {128, 64}};
+constexpr int kNumTiles = 18;
+constexpr int kTileBK[kNumTiles] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16,
+                                    16, 16, 16, 16, 16};  // (launch_layout)
 
 template <bool AK, bool BKM, int VEC>
 void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
@@ -844,7 +848,14 @@ void launch_layout(const KParams& kp, int tile, cudaStream_t stream) {
     // 48-wide tiles: N in (32, 48] (the recursion's P-apply at g + 1 <= 48)
     // without padding the last third of a 64-wide tile
     case 11: launch_cfg<64, 48, 16, 2, 2, 4, AK, BKM, VEC>(kp, stream); break;
-    default: launch_cfg<128, 48, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    case 12: launch_cfg<128, 48, 16, 4, 2, 3, AK, BKM, VEC>(kp, stream); break;
+    // narrow N in steps of 8: the per-SM padded work, not the tile count,
+    // sets the time of the N <= 64 batched products
+    case 13: launch_cfg<128, 24, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+    case 14: launch_cfg<128, 40, 16, 4, 1, 4, AK, BKM, VEC>(kp, stream); break;
+    case 15: launch_cfg<128, 48, 16, 4, 1, 3, AK, BKM, VEC>(kp, stream); break;
+    case 16: launch_cfg<128, 56, 16, 4, 1, 3, AK, BKM, VEC>(kp, stream); break;
+    default: launch_cfg<128, 64, 16, 4, 1, 3, AK, BKM, VEC>(kp, stream); break;
   }
 }
 
@@ -1013,15 +1024,39 @@ FILE* gemm_log() {
 // the 4-warp shapes 7, 8 only pay off in the cp.async kernel; the 48-wide
 // tile only where N fits one of them and a 64-wide tile would pad a quarter
 // or more: 24 % faster there, profiles/r01_gemm_tune_bn48.txt).
-constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2};
-constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0};
-constexpr bool kVsTile[] = {false, true, false, true, false, false, false, false, false, false, false, true, false};
+constexpr int kOcc[] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2, 2, 2, 2, 2, 2};
+constexpr double kEff[] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0,
+                           1.0, 1.0, 1.0, 1.0, 1.0};
+constexpr bool kVsTile[] = {false, true, false, true, false, false, false, false, false, false, false, true, false,
+                            false, false, false, false, false};
+// RP_GEMM_NARROW=0: no narrow-N tiles (A/B)
+bool g_narrow_tiles = [] {
+  const char* e = std::getenv("RP_GEMM_NARROW");
+  return !(e && e[0] == '0');
+}();
 
 int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   const int64_t nb = g.batch * g.batch2;
   int tile = 0;
   double best = 1e300;
+  // Narrow products (N <= 64): one tile column, sized to N in steps of 8,
+  // costed by the padded work on the busiest SM -- ceil(CTAs / 148) tiles of
+  // BM x BN -- since such products never fill the GPU evenly.
+  const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0;
   for (int t = 0; t < kNumTiles; ++t) {
+    const bool narrow_tile = t >= 13;
+    if (narrow) {
+      if (kTiles[t].bn < g.n || (!narrow_tile && t != 4 && t != 2)) continue;  // 128 x 16 / 32 and the steps of 8
+      if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;
+      const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * nb * split;
+      const double cost = static_cast<double>(ceil_div(ctas, 148)) * kTiles[t].bm * kTiles[t].bn / kEff[t];
+      if (cost < best * 0.999) {
+        best = cost;
+        tile = t;
+      }
+      continue;
+    }
+    if (narrow_tile) continue;
     if (kTiles[t].bn == 16 && g.n > 16) continue;
     if (kTiles[t].bn == 48 && (g.n <= 32 || g.n > 48)) continue;
     if (kEff[t] <= 0.0) continue;

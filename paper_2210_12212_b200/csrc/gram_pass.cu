@@ -419,7 +419,7 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
 //     column segments) into a shared-memory ring with 2-D TMA boxes of
 //     8 x 256, 64B-swizzled (both fragment patterns below are then
 //     conflict-free);
-//   * the CTA's NW warps (16; 8 with RP_GRAM_DMMA_WARPS=8) own d/NW columns
+//   * the CTA's NW warps (8; 16 with RP_GRAM_DMMA_WARPS=16) own d/NW columns
 //     each.  y pass:
 //     y_blk^T (K x 8 rows) = W^T A_blk^T with W^T as the register-resident A
 //     operand and the stage as the B operand, four accumulator chains;
@@ -738,10 +738,11 @@ bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, con
 bool gram_dmma_launch(const double* a, int64_t lda, int64_t n, int64_t d, const double* w, int64_t k, double* z,
                       cudaStream_t s) {
   if (k < 1 || k > 8 || n <= 0 || d <= 0 || lda % 2 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) return false;
-  // (RP_GRAM_DMMA_WARPS=8: eight warps per CTA instead of sixteen -- A/B)
+  // (RP_GRAM_DMMA_WARPS=16: sixteen warps per CTA instead of eight -- A/B;
+  // measured 0.63 vs 0.73 of HBM on the C2 operator, profiles/r02_gram_pass_dmma.txt)
   static const bool w8 = [] {
     const char* e = std::getenv("RP_GRAM_DMMA_WARPS");
-    return e && std::atoi(e) == 8;
+    return !(e && std::atoi(e) == 16);
   }();
   switch (ceil_div(d, 256)) {
     case 1: return w8 ? gram_dmma_launch_nt<1, 8>(a, lda, n, d, w, k, z, s) : gram_dmma_launch_nt<1, 16>(a, lda, n, d, w, k, z, s);
