@@ -545,6 +545,44 @@ __global__ void __launch_bounds__(kGenThreads) gauss_rows_kernel(uint64_t* __res
 
 }  // namespace
 
+namespace {
+// Normals [first, first + count) of the normal() stream (first even), times
+// scale, contiguous: segment s starts at pair-aligned word first + s*seg.
+__global__ void __launch_bounds__(kGenThreads) gauss_stream_kernel(const uint64_t* __restrict__ states, int64_t seg,
+                                                                   int64_t count, double scale,
+                                                                   double* __restrict__ out) {
+  __shared__ uint64_t sm[2 * kN];
+  BlockGen g;
+  g.init(sm);
+  g.load(states + static_cast<int64_t>(blockIdx.x) * kN);
+  const int64_t start = static_cast<int64_t>(blockIdx.x) * seg;
+  const int64_t len = min(seg, count - start);
+  constexpr int kPairs = kN / 2;
+  for (int64_t done = 0; done < len; done += kN) {
+    g.step();
+    const int t = threadIdx.x;
+    if (t < kPairs) {
+      double cv, sv;
+      box_muller(d_temper(g.cur[2 * t]), d_temper(g.cur[2 * t + 1]), cv, sv);
+      const int64_t q = done + 2 * t;
+      if (q < len) out[start + q] = __dmul_rn(scale, cv);
+      if (q + 1 < len) out[start + q + 1] = __dmul_rn(scale, sv);
+    }
+  }
+}
+}  // namespace
+
+void draw_gauss_stream(uint64_t seed, int64_t first, int64_t count, double scale, double* d_out, cudaStream_t stream) {
+  require(first % 2 == 0, "gaussian stream: the first normal must start a pair");
+  if (count <= 0) return;
+  const int64_t seg = seg_words(count);  // (even: pairs never straddle segments)
+  const int64_t segs = ceil_div(count, seg);
+  DBuf<uint64_t> st(static_cast<size_t>(segs) * kN, stream);
+  mt::states_at(seed, progression(static_cast<uint64_t>(first), seg, segs), st.get(), stream);
+  gauss_stream_kernel<<<static_cast<unsigned>(segs), kGenThreads, 0, stream>>>(st.get(), seg, count, scale, d_out);
+  RP_LAUNCH_CHECK();
+}
+
 void gauss_rows_next(GaussRows& g, int64_t J, double scale, double* d_out, int64_t ld, cudaStream_t stream) {
   if (J <= 0) return;
   gauss_rows_kernel<<<static_cast<unsigned>(g.rows), kGenThreads, 0, stream>>>(g.d_states, g.d_cursor, J, scale,

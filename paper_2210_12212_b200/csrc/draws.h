@@ -34,6 +34,13 @@ void gauss_rows_init(uint64_t seed, int64_t rows, int64_t first, int64_t stride,
 void gauss_rows_next(GaussRows& g, int64_t J, double scale, double* d_out, int64_t ld,
                      cudaStream_t stream);
 
+// Normals [first, first + count) of the SeededRng(seed) normal() stream
+// (first even), times `scale`, contiguous in d_out: a Gaussian sketch whose
+// rows are consecutive stretches of the stream (S = m x n, row stride n) is
+// one such stream -- a handful of segment jumps instead of one per row.
+void draw_gauss_stream(uint64_t seed, int64_t first, int64_t count, double scale, double* d_out,
+                       cudaStream_t stream);
+
 // CountSketch / SJLT draws for the whole stream (sketch.cpp:119-124):
 // h[b * n + j] (int32) and sgn[b * n + j] = sign() * entry.
 void draw_count(uint64_t seed, int64_t n, int64_t rows_per_block, int blocks, double entry,

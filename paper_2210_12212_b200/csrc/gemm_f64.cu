@@ -1042,7 +1042,8 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   // Narrow products (N <= 64): one tile column, sized to N in steps of 8,
   // costed by the padded work on the busiest SM -- ceil(CTAs / 148) tiles of
   // BM x BN -- since such products never fill the GPU evenly.
-  const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0;
+  // (batched plain products only: the factorization's lower-only updates keep the general model)
+  const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0 && !g.lower_only && nb > 1;
   for (int t = 0; t < kNumTiles; ++t) {
     const bool narrow_tile = t >= 13;
     if (narrow) {

@@ -499,12 +499,15 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       // S slab budget: 1 GiB of doubles.
       const int64_t J = std::max<int64_t>(
           2, std::min<int64_t>(op.n_loc, ((int64_t{1} << 27) / std::max<int64_t>(m, 1)) & ~int64_t{1}));
-      DBuf<uint64_t> states(static_cast<size_t>(m) * 312, stream);
-      DBuf<int64_t> cursor(static_cast<size_t>(m), stream);
+      // One slab holding whole rows of an unsharded operator: S is the stream
+      // [0, m n) itself (row r = normals r n .. r n + n - 1, sketch.cpp:86-95).
+      const bool one_stream = op.row0 == 0 && op.n_loc == spec.n && J >= op.n_loc;
+      DBuf<uint64_t> states(one_stream ? 1 : static_cast<size_t>(m) * 312, stream);
+      DBuf<int64_t> cursor(one_stream ? 1 : static_cast<size_t>(m), stream);
       GaussRows g;
       g.d_states = states.get();
       g.d_cursor = cursor.get();
-      gauss_rows_init(spec.seed, m, op.row0, spec.n, g, stream);
+      if (!one_stream) gauss_rows_init(spec.seed, m, op.row0, spec.n, g, stream);
       DBuf<double> slab(static_cast<size_t>(m * J), stream);
       DBuf<double> slab_cm;
       if (op.sparse) {
@@ -514,7 +517,10 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
       }
       for (int64_t j0 = 0; j0 < op.n_loc; j0 += J) {
         const int64_t Jc = std::min(J, op.n_loc - j0);
-        gauss_rows_next(g, Jc, scale, slab.get(), Jc, stream);
+        if (one_stream)
+          draw_gauss_stream(spec.seed, 0, m * Jc, scale, slab.get(), stream);
+        else
+          gauss_rows_next(g, Jc, scale, slab.get(), Jc, stream);
         if (!op.sparse) {
           GemmArgs ga;
           ga.opa = Op::T;  // slab is row-major m x Jc == column-major Jc x m
