@@ -1042,12 +1042,16 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   // Narrow products (N <= 64): one tile column, sized to N in steps of 8,
   // costed by the padded work on the busiest SM -- ceil(CTAs / 148) tiles of
   // BM x BN -- since such products never fill the GPU evenly.
-  // (batched plain products only: the factorization's lower-only updates keep the general model)
-  const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0 && !g.lower_only && nb > 1;
+  // (the recursion's batched preconditioner products with m >= 512 only:
+  // measured -0.25 ms on C2's basis; on C1 (m = 256) and on the factor's
+  // products it was neutral to negative, profiles/r02_narrow_tiles.txt)
+  const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0 && !g.lower_only && nb > 1 &&
+                      g.epilogue != nullptr && g.m >= 512;
   for (int t = 0; t < kNumTiles; ++t) {
     const bool narrow_tile = t >= 13;
     if (narrow) {
-      if (kTiles[t].bn < g.n || (!narrow_tile && t != 4 && t != 2)) continue;  // 128 x 16 / 32 and the steps of 8
+      // 128 x 16 / 32, 64 x 32 / 48 / 64 and the 128-row steps of 8
+      if (kTiles[t].bn < g.n || (!narrow_tile && t != 4 && t != 2 && t != 3 && t != 11 && t != 1)) continue;
       if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;
       const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * nb * split;
       const double cost = static_cast<double>(ceil_div(ctas, 148)) * kTiles[t].bm * kTiles[t].bn / kEff[t];
