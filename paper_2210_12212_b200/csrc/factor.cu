@@ -310,8 +310,16 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // which corrupts results (concurrency finding).
   const cudaStream_t user = stream;
   cudaStream_t aux = nullptr, hi = nullptr;
-  RP_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-  RP_CUDA(cudaStreamCreateWithFlags(&hi, cudaStreamNonBlocking));
+  static const bool one_stream = [] {  // RP_FACTOR_ONE_STREAM=1: no lookahead streams (concurrency probe)
+    const char* e = std::getenv("RP_FACTOR_ONE_STREAM");
+    return e && e[0] == '1';
+  }();
+  if (one_stream) {
+    aux = hi = user;
+  } else {
+    RP_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    RP_CUDA(cudaStreamCreateWithFlags(&hi, cudaStreamNonBlocking));
+  }
   std::vector<cudaEvent_t> events;
   auto new_event = [&]() {
     cudaEvent_t e;
@@ -325,6 +333,10 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     RP_CUDA(cudaStreamWaitEvent(hi, start, 0));
   }
   stream = hi;
+  // One TMA grid at a time (concurrency finding): the critical
+  // chain's GEMMs (panel solve, next-column update) run on the cp.async
+  // kernel while the trailing updates on the aux stream keep the TMA kernel.
+  const bool chain_no_tma = !one_stream;
   auto syrk_update = [&](int64_t row0, int64_t m, int64_t ncols, int64_t k0, int kb, cudaStream_t st) {
     // C(row0.., row0..row0+ncols) -= A21(row0.., :) A21(row0..row0+ncols, :)^T, lower part
     GemmArgs g;
@@ -347,6 +359,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     g.batch = batch;
     g.lower_only = true;
     g.split_k = 1;
+    g.no_tma = chain_no_tma && st != aux;
     dgemm(g, st);
   };
   cudaEvent_t prev_rest = nullptr;  // trailing update of the previous panel (aux stream)
@@ -381,6 +394,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
       t.batch = batch;
       t.split_k = 1;
       t.force_tile = 6;  // 128 x 64
+      t.no_tma = chain_no_tma;
       dgemm(t, stream);
     }
     const int64_t r0 = k0 + kb;
@@ -408,10 +422,12 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   }
   stream = user;
   for (cudaEvent_t e : events) RP_CUDA(cudaEventDestroy(e));  // (released once complete)
-  release_workspace(aux);  // (the GEMMs above run unsplit; this only guards a recycled handle)
-  release_workspace(hi);
-  RP_CUDA(cudaStreamDestroy(aux));
-  RP_CUDA(cudaStreamDestroy(hi));
+  if (!one_stream) {
+    release_workspace(aux);  // (the GEMMs above run unsplit; this only guards a recycled handle)
+    release_workspace(hi);
+    RP_CUDA(cudaStreamDestroy(aux));
+    RP_CUDA(cudaStreamDestroy(hi));
+  }
   // 2) Triangular inverse in place.
   {
     // (the strict upper triangle is already zero: shifted_copies writes it so

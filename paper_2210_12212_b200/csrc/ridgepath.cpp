@@ -367,7 +367,10 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
-  bool gram_overlap_tma = true;   // option "gram_overlap_tma": 0 = cp.async kernel for the overlapped SYRK
+  // option "gram_overlap_tma": 1 = the overlapped SYRK on the TMA kernel.  Off: two grids issuing TMA
+  // copies at the same time corrupt tiles in some runs (concurrency finding), so every kernel
+  // that runs beside another stream's work is a cp.async one
+  bool gram_overlap_tma = false;
   int gram_overlap_split = 0;     // option "gram_overlap_split": split-K of the overlapped SYRK (0 = auto; probe)
   bool sketch_on_hi = true;       // option "sketch_on_hi": sketch on its own stream while the SYRK runs
   // option "stream_priorities" is rejected: compute preemption (which stream
