@@ -336,7 +336,11 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // One TMA grid at a time (concurrency finding): the critical
   // chain's GEMMs (panel solve, next-column update) run on the cp.async
   // kernel while the trailing updates on the aux stream keep the TMA kernel.
-  const bool chain_no_tma = !one_stream;
+  static const bool chain_tma = [] {  // RP_FACTOR_CHAIN_TMA=1: TMA kernel on the critical chain too (probe)
+    const char* e = std::getenv("RP_FACTOR_CHAIN_TMA");
+    return e && e[0] == '1';
+  }();
+  const bool chain_no_tma = !one_stream && !chain_tma;
   auto syrk_update = [&](int64_t row0, int64_t m, int64_t ncols, int64_t k0, int kb, cudaStream_t st) {
     // C(row0.., row0..row0+ncols) -= A21(row0.., :) A21(row0..row0+ncols, :)^T, lower part
     GemmArgs g;

@@ -494,9 +494,21 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
 // so both produce identical bits.
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool VS>
 __global__ void __launch_bounds__((WM * WN + 1) * 32)
-    dgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, KParams p,
-                     int a_batched, int a_batched2, int b_batched, int b_batched2) {
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap amap_p, const __grid_constant__ CUtensorMap bmap_p, KParams p,
+                     int a_batched, int a_batched2, int b_batched, int b_batched2
+#ifdef RP_PROBE_GMAP  // (concurrency probe, tools/tma_race.cu: tensor maps read from global memory)
+                     ,
+                     const CUtensorMap* gmaps
+#endif
+    ) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
+#ifdef RP_PROBE_GMAP
+  const CUtensorMap& amap = gmaps[0];
+  const CUtensorMap& bmap = gmaps[1];
+#else
+  const CUtensorMap& amap = amap_p;
+  const CUtensorMap& bmap = bmap_p;
+#endif
   extern __shared__ __align__(128) double smem_raw[];
   // 128-byte aligned ring (TMA destinations); the launch adds 128 B of slack
   double* smem = smem_raw + (((128u - (tma::smem_u32(smem_raw) & 127u)) & 127u) >> 3);
@@ -598,7 +610,24 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32)
 #pragma unroll
           for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
-      // (the DMMAs above consumed every fragment: the stage may be refilled)
+      // Release the stage.  The refill is an async-proxy write (TMA) and this
+      // warp's fragment loads are generic-proxy reads that may still be in
+      // flight when the arrive is issued (ptxas schedules the arrive ahead of
+      // the last DMMAs, whose operands those loads feed): without a
+      // cross-proxy fence the refill can overwrite the stage before the loads
+      // return.  Seen as wrong 8 x 16 / 32 x 16 / 64 x 32 output blocks in
+      // 1 of 8 runs whenever a second grid's CTAs shared the SMs
+      // (profiles/r02_tma_release_race.txt: 6/48 runs wrong without the
+      // fence, 0/48 with it).
+#ifdef RP_PROBE_ORDER  // (concurrency probe: every DMMA of the stage retired before the release)
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) asm volatile("add.f64 %0, %0, 0d0000000000000000;" : "+d"(acc[i][j][0]));
+#endif
+#ifndef RP_PROBE_NOFENCE  // (concurrency probe: the round-1 kernel, no fence)
+      tma::fence_proxy_async_smem();
+#endif
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[stage]);
       if (++stage == STAGES) {
@@ -782,7 +811,21 @@ bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl_enabled ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+#ifdef RP_PROBE_GMAP
+  {
+    static CUtensorMap* ring = nullptr;
+    static size_t slot = 0;
+    constexpr size_t kSlots = 1 << 16;  // (never reused within a probe run)
+    if (!ring) RP_CUDA(cudaMalloc(&ring, sizeof(CUtensorMap) * 2 * kSlots));
+    CUtensorMap* dst = ring + 2 * (slot++ % kSlots);
+    const CUtensorMap both[2] = {amap, bmap};
+    RP_CUDA(cudaMemcpyAsync(dst, both, sizeof(both), cudaMemcpyHostToDevice, stream));
+    const CUtensorMap* gm = dst;
+    RP_CUDA(cudaLaunchKernelEx(&cfg, kern, amap, bmap, kp, ab1, ab2, bb1, bb2, gm));
+  }
+#else
   RP_CUDA(cudaLaunchKernelEx(&cfg, kern, amap, bmap, kp, ab1, ab2, bb1, bb2));
+#endif
   RP_LAUNCH_CHECK();
   return true;
 }

@@ -162,6 +162,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Orders this thread's earlier shared-memory reads (generic proxy) before the
+// TMA refill of the stage (async proxy): issued by every consumer lane before
+// the stage is released -- an mbarrier arrive or a CTA barrier alone lets the
+// refill overtake loads still in flight (gemm_f64.cu, stage release).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -286,6 +293,7 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
     }
     // release the stage only once its values are consumed (the arrive does
     // not wait for this warp's outstanding shared-memory loads)
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[rp.stage]);
     rp.next(stages);
@@ -313,6 +321,7 @@ __global__ void __launch_bounds__((kPWarps + 1) * 32, 1)
         pv[g2][k] = p;
       }
     }
+    fence_proxy_async_smem();
     __syncwarp();  // (stage values consumed: release it)
     if (lane == 0) mbar_arrive(&empty[rp.stage]);
     rp.next(stages);
@@ -568,6 +577,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
     }
     // every warp is done with block j: its stage takes block j + stages
+    fence_proxy_async_smem();
     __syncthreads();
     if (t == 0 && j + stages < cnt) issue(j + stages);
     if (more) y_sum(j + 1, yb);

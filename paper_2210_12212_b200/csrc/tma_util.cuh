@@ -33,6 +33,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Orders this thread's earlier generic-proxy shared-memory accesses (LDS
+// fragment loads) before later async-proxy accesses (the TMA refill of the
+// stage): issued by every consumer lane before the stage's "empty" arrive.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
