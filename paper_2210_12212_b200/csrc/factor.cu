@@ -294,7 +294,7 @@ void shifted_copies(const double* g, int64_t n, const double* d_shifts, int64_t 
 }
 
 void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64_t batch, double* out, int64_t ldo,
-                         int64_t stride_o, cudaStream_t stream) {
+                         int64_t stride_o, cudaStream_t stream, bool chain_high_priority) {
   require(n >= 1 && batch >= 1, "spd_inverse: empty problem");
   DBuf<int> info(static_cast<size_t>(batch), stream);
   RP_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int) * batch, stream));
@@ -305,9 +305,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
   // (one CTA per matrix) overlap the big trailing GEMMs.  All GEMMs here run
   // unsplit, so they share no workspace.
   // The critical chain (diagonal kernels, panel solves, next-column updates)
-  // runs on its own stream.  Both streams keep the default priority: a
-  // high-priority chain would preempt trailing-update CTAs mid-TMA-pipeline,
-  // which corrupts results (concurrency finding).
+  // runs on its own stream, optionally at the highest stream priority.
   const cudaStream_t user = stream;
   cudaStream_t aux = nullptr, hi = nullptr;
   static const bool one_stream = [] {  // RP_FACTOR_ONE_STREAM=1: no lookahead streams (concurrency probe)
@@ -318,7 +316,9 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     aux = hi = user;
   } else {
     RP_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-    RP_CUDA(cudaStreamCreateWithFlags(&hi, cudaStreamNonBlocking));
+    int lo_p = 0, hi_p = 0;
+    if (chain_high_priority) RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+    RP_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, chain_high_priority ? hi_p : 0));
   }
   std::vector<cudaEvent_t> events;
   auto new_event = [&]() {
@@ -333,14 +333,14 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     RP_CUDA(cudaStreamWaitEvent(hi, start, 0));
   }
   stream = hi;
-  // One TMA grid at a time (concurrency finding): the critical
-  // chain's GEMMs (panel solve, next-column update) run on the cp.async
-  // kernel while the trailing updates on the aux stream keep the TMA kernel.
-  static const bool chain_tma = [] {  // RP_FACTOR_CHAIN_TMA=1: TMA kernel on the critical chain too (probe)
+  // (round 2 ran the chain's GEMMs on the cp.async kernel to keep one TMA
+  // grid on the GPU at a time; with the stage-release fence of gemm_f64.cu
+  // concurrent TMA grids are exact, profiles/r02_tma_release_race.txt)
+  static const bool chain_cp_async = [] {  // RP_FACTOR_CHAIN_TMA=0: cp.async kernel on the critical chain (A/B)
     const char* e = std::getenv("RP_FACTOR_CHAIN_TMA");
-    return e && e[0] == '1';
+    return e && e[0] == '0';
   }();
-  const bool chain_no_tma = !one_stream && !chain_tma;
+  const bool chain_no_tma = !one_stream && chain_cp_async;
   auto syrk_update = [&](int64_t row0, int64_t m, int64_t ncols, int64_t k0, int kb, cudaStream_t st) {
     // C(row0.., row0..row0+ncols) -= A21(row0.., :) A21(row0..row0+ncols, :)^T, lower part
     GemmArgs g;

@@ -17,8 +17,11 @@ namespace rpb {
 // lower triangle read, strict upper triangle must be zero) is overwritten
 // (scratch); out_b = H_b^{-1} (full symmetric).  Throws FactorFailure if some
 // H_b is not numerically positive definite.
+// chain_high_priority: the critical chain's stream (diagonal kernels, panel
+// solves) is created at the device's highest stream priority, so its CTAs
+// are placed ahead of the trailing updates' and of any overlapped work.
 void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64_t batch, double* out,
-                         int64_t ldo, int64_t stride_o, cudaStream_t stream);
+                         int64_t ldo, int64_t stride_o, cudaStream_t stream, bool chain_high_priority = false);
 
 // H_b = lower(G) + shift_b * I for b < batch (G shared, n x n), strict upper
 // triangle zero -- the input spd_inverse_batched expects.

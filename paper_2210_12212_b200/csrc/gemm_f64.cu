@@ -77,6 +77,7 @@ struct KParams {
   bool mirror;  // lower_only: also write the transposed element (C symmetric)
   bool tri_k;   // op(A)(i, k) == 0 for k < i: start the k loop at the tile's first row
   bool no_tma;  // use the cp.async kernel (GemmArgs::no_tma)
+  int occ_cap;  // host side only: GemmArgs::max_ctas_per_sm
   RecursionEpilogue epi;
 };
 
@@ -792,11 +793,15 @@ bool launch_tma_cfg(const KParams& kp, cudaStream_t stream) {
                                       kp.batch2, BN + 4, BK, &bb1, &bb2);
   if (!ok_b) return false;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VS>;
-  constexpr int smem = C::SMEM_BYTES + 128;
+  int smem = C::SMEM_BYTES + 128;
+  // (occupancy cap: a CTA that asks for more than 1/(cap + 1) of the SM's
+  // shared memory leaves room for at most `cap` of its kind)
+  constexpr int kSmSmem = 227 * 1024, kMaxDyn = kSmSmem - 4096;
+  if (kp.occ_cap > 0) smem = std::min(kMaxDyn, std::max(smem, kSmSmem / (kp.occ_cap + 1) + 1024));
   static std::atomic<bool> attr_set[kMaxDevices];  // per template instantiation and device
   const int dev = current_device();
   if (!attr_set[dev].load(std::memory_order_acquire)) {
-    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDyn));
     attr_set[dev].store(true, std::memory_order_release);
   }
   dim3 grid(static_cast<unsigned>(ceil_div(kp.m, BM)), static_cast<unsigned>(ceil_div(kp.n, BN)),
@@ -867,6 +872,9 @@ constexpr TileShape kTiles[] = {{128, 128}, {64, 64}, {128, 32}, {64, 32}, {128,
                                  {128, 64},  {64, 128}, {128, 64}, {64, 128}, {128, 64}, {64, 48}, {128, 48},
                                  // narrow N (the recursion's batched preconditioner GEMM, N = g + 1 <= 64):
                                  // 128-row tiles of 4 x 1 warps in steps of 8 columns
+                                 // (32-row tiles -- 1024 CTAs, 7 x 32 rows on the busiest SM instead of
+                                 // 2 x 128 -- were measured: no gain, each small tile re-streams the whole
+                                 // B operand; profiles/r02_gemm_tune_32row.txt)
                                  {128, 24},  {128, 40}, {128, 48}, {128, 56}, {128, 64}};
 constexpr int kNumTiles = 18;
 constexpr int kTileBK[kNumTiles] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16,
@@ -1095,6 +1103,7 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
     if (narrow) {
       // 128 x 16 / 32, 64 x 32 / 48 / 64 and the 128-row steps of 8
       if (kTiles[t].bn < g.n || (!narrow_tile && t != 4 && t != 2 && t != 3 && t != 11 && t != 1)) continue;
+      if (kEff[t] <= 0.0) continue;
       if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;
       const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * nb * split;
       const double cost = static_cast<double>(ceil_div(ctas, 148)) * kTiles[t].bm * kTiles[t].bn / kEff[t];
@@ -1186,6 +1195,7 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   kp.lower_only = g.lower_only;
   kp.tri_k = g.tri_k;
   kp.no_tma = g.no_tma;
+  kp.occ_cap = g.max_ctas_per_sm;
 
   const bool ak = g.opa == Op::T;  // A contiguous along k
   const bool bk = g.opb == Op::N;  // B contiguous along k

@@ -42,9 +42,13 @@ struct GemmArgs {
   // op(A)(i, k) == 0 for k < i (A^T of a lower-triangular matrix): each output
   // tile skips the k range below its first row.  Requires split_k == 1.
   bool tri_k = false;
-  // Use the cp.async kernel instead of the TMA one (A/B switch; the cp.async
-  // pipeline survives preemption by higher-priority work).
+  // Use the cp.async kernel instead of the TMA one (A/B switch).
   bool no_tma = false;
+  // At most this many CTAs of the launch per SM (0 = the kernel's natural
+  // occupancy): the TMA kernel pads its dynamic shared memory so that the
+  // rest of every SM stays free for another stream's kernels (the Gram SYRK
+  // overlapping the latency-bound Cholesky chain).
+  int max_ctas_per_sm = 0;
   // Deterministic split-K factor; 0 = heuristic.  With col_stable the
   // heuristic looks at (m, k) only, so column j of C does not depend on n.
   int split_k = 0;

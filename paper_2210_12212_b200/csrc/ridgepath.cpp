@@ -367,20 +367,20 @@ struct rp_ctx {
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
-  // option "gram_overlap_tma": 1 = the overlapped SYRK on the TMA kernel.  Off: two grids issuing TMA
-  // copies at the same time corrupt tiles in some runs (concurrency finding), so every kernel
-  // that runs beside another stream's work is a cp.async one
-  bool gram_overlap_tma = false;
+  // option "gram_overlap_tma": 1 = the overlapped SYRK on the TMA kernel (0: cp.async, A/B switch)
+  bool gram_overlap_tma = true;
   int gram_overlap_split = 0;     // option "gram_overlap_split": split-K of the overlapped SYRK (0 = auto; probe)
+  int gram_overlap_occ = 0;       // option "gram_overlap_occ": at most this many CTAs of that SYRK per SM (0 = no cap)
   bool sketch_on_hi = true;       // option "sketch_on_hi": sketch on its own stream while the SYRK runs
-  // option "stream_priorities" is rejected: compute preemption (which stream
-  // priorities trigger) of a CTA with TMA copies in flight corrupts results
-  // (concurrency finding; repro tools/tma_race.cu).  Every stream
-  // of the library runs at the default priority.
+  // option "stream_priorities": the sketch stream and the Cholesky chain's
+  // stream run at the highest stream priority, so their CTAs are placed
+  // ahead of the overlapped Gram SYRK's.  (Rounds 1-2 rejected priorities:
+  // the wrong results they exposed were the TMA GEMM's stage-release race,
+  // fixed in gemm_f64.cu -- DESIGN.md, concurrency finding.)
+  bool stream_priorities = true;  // (C2: 18.5 -> 17.9 ms; exact in every stress run)
   // option "gram_overlap": Gram SYRK on a side stream, overlapping the sketch
-  // and the precond build; bit-identical to the single-stream path as long as
-  // the streams share one priority (tools/race_probe.py; DESIGN.md,
-  // concurrency finding).
+  // and the precond build; bit-identical to the single-stream path
+  // (tools/race_stress.py, concurrency finding).
   bool gram_overlap = true;
   bool gram_after_sketch = false;  // option "gram_after_sketch": start that SYRK after the sketch instead of before
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
@@ -681,6 +681,7 @@ struct GramOp {
     if (st && ctx->gram_overlap_tile >= 0) g.force_tile = ctx->gram_overlap_tile;
     if (st && !ctx->gram_overlap_tma) g.no_tma = true;
     if (st && ctx->gram_overlap_split > 0) g.split_k = ctx->gram_overlap_split;
+    if (st && ctx->gram_overlap_occ > 0) g.max_ctas_per_sm = ctx->gram_overlap_occ;
     dgemm(g, s);
     allreduce(ctx, G.get(), op.d * op.d, s);
     matrix = true;
@@ -781,7 +782,7 @@ struct PrecondBatch {
       if (s1 > s0) {
         DBuf<double> h(static_cast<size_t>((s1 - s0) * nn * nn), s);
         shifted_copies(gram, nn, d_lambda0.get() + s0, s1 - s0, h.get(), s);
-        spd_inverse_batched(h.get(), nn, nn, nn * nn, s1 - s0, mine.get(), nn, nn * nn, s);
+        spd_inverse_batched(h.get(), nn, nn, nn * nn, s1 - s0, mine.get(), nn, nn * nn, s, ctx->stream_priorities);
       }
       inv_owned.alloc(static_cast<size_t>(ctx->world * lb * nn * nn), s);
       allgather(ctx, mine.get(), lb * nn * nn, inv_owned.get());
@@ -792,7 +793,7 @@ struct PrecondBatch {
     shifted_copies(gram, nn, d_lambda0.get(), L, h.get(), s);
     inv_owned.alloc(static_cast<size_t>(L * nn * nn), s);
     inv = inv_owned.get();
-    spd_inverse_batched(h.get(), nn, nn, nn * nn, L, inv_owned.get(), nn, nn * nn, s);
+    spd_inverse_batched(h.get(), nn, nn, nn * nn, L, inv_owned.get(), nn, nn * nn, s, ctx->stream_priorities);
   }
 
   // A view of shifts [l0, l1) (no copy of the factors).
@@ -1367,7 +1368,9 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     //    preconditioner -- runs on a second stream of the context.
     if (gram_done && ctx->sketch_on_hi) {
       if (!ctx->hi) {
-        RP_CUDA(cudaStreamCreateWithFlags(&ctx->hi, cudaStreamNonBlocking));
+        int lo_p = 0, hi_p = 0;
+        if (ctx->stream_priorities) RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+        RP_CUDA(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, ctx->stream_priorities ? hi_p : 0));
       }
       cudaEvent_t fork;
       RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1889,9 +1892,13 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "feature_shard") {
       ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {
-      require(value == 0,
-              "stream_priorities: rejected -- preempting a CTA with TMA copies in flight corrupts results "
-              "(DESIGN.md, concurrency finding)");
+      if (ctx->stream_priorities != (value != 0) && ctx->hi) {  // (recreated at the new priority on next use)
+        RP_CUDA(cudaStreamSynchronize(ctx->hi));
+        release_workspace(ctx->hi);
+        RP_CUDA(cudaStreamDestroy(ctx->hi));
+        ctx->hi = nullptr;
+      }
+      ctx->stream_priorities = value != 0;
     } else if (k == "sketch_on_hi") {
       ctx->sketch_on_hi = value != 0;
     } else if (k == "gram_overlap_tma") {
@@ -1899,6 +1906,9 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "gram_overlap_tile") {
       require(value >= -1 && value < 13, "gram_overlap_tile must be in [-1, 12]");
       ctx->gram_overlap_tile = static_cast<int>(value);
+    } else if (k == "gram_overlap_occ") {
+      require(value >= 0 && value <= 4, "gram_overlap_occ must be in [0, 4]");
+      ctx->gram_overlap_occ = static_cast<int>(value);
     } else if (k == "gram_after_sketch") {
       ctx->gram_after_sketch = value != 0;
     } else if (k == "gram_overlap") {

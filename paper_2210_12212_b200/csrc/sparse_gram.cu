@@ -150,7 +150,9 @@ __global__ void __launch_bounds__(256) pass2_kernel(const int64_t* __restrict__ 
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int c = lane + 32 * q;
-      acc[q] = (!first && c < cc) ? zr[c] : 0.0;
+      // (Z only streams through: read once and written once per panel -- evict-first
+      // loads / stores keep it from displacing the gathered Yp and W rows in L2)
+      acc[q] = (!first && c < cc) ? __ldcs(zr + c) : 0.0;
     }
     for (int64_t base = e0; base < e1; base += 32) {
       const int cnt = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const int64_t* __restrict__ 
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int c = lane + 32 * q;
-      if (c < cc) zr[c] = acc[q];
+      if (c < cc) __stcs(zr + c, acc[q]);
     }
   }
 }
@@ -261,6 +263,8 @@ void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* c
       run_chunk<1>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
     } else if (cc <= 64) {
       run_chunk<2>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+    } else if (cc <= 96) {
+      run_chunk<3>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
     } else {
       run_chunk<4>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
     }

@@ -1,9 +1,10 @@
 """Regression for the concurrency finding: on the full C2 workload
 the overlapped Gram SYRK (TMA kernel on a side stream, next to the sketch and
 the preconditioner build) must give the same bits as the single-stream path.
-With a low-priority side stream next to a high-priority sketch stream it did
-not (x(lambda) off by 1e-2 in most runs), so the default keeps every stream at
-one priority; this test runs the default schedule several times."""
+Before the stage-release fence of the TMA GEMM (gemm_f64.cu) it did not
+whenever another grid's CTAs shared the SMs: x(lambda) off by 1e-2 in most
+runs with a prioritized sketch stream, in 45% of runs with the SYRK started
+after the sketch.  Those schedules are run here on purpose."""
 import numpy as np
 import pytest
 
@@ -38,5 +39,12 @@ def test_overlapped_gram_bitwise_c2_full(rp):
         return out
 
     ref = run({"gram_overlap": 0}, 1)[0]
-    for x in run({}, 4):  # default: overlapped TMA SYRK, single priority
+    for x in run({}, 4):  # default: overlapped TMA SYRK
         assert np.array_equal(x, ref)
+    # the schedules that exposed the race: prioritized sketch / Cholesky-chain
+    # streams beside the SYRK; SYRK launched after the sketch, beside the
+    # factorization's own TMA GEMMs
+    for opts in ({"stream_priorities": 1}, {"gram_after_sketch": 1}, {"gram_after_sketch": 1, "stream_priorities": 1},
+                 {"gram_overlap_occ": 1, "gram_overlap_tile": 1, "stream_priorities": 1}):
+        for x in run(opts, 6):
+            assert np.array_equal(x, ref), opts

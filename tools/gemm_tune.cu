@@ -10,6 +10,21 @@
 
 using namespace rpb;
 
+// (operands in [-0.5, 0.5): every tile must reproduce the auto tile's bits -- same k order per element)
+__global__ void tune_fill(double* x, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    unsigned long long z = (i + 1) * 0x9E3779B97F4A7C15ull + seed;
+    z ^= z >> 29, z *= 0xBF58476D1CE4E5B9ull, z ^= z >> 32;
+    x[i] = static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5;
+  }
+}
+__global__ void tune_diff(const double* x, const double* y, size_t n, unsigned long long* bad) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    if (__double_as_longlong(x[i]) != __double_as_longlong(y[i])) atomicAdd(bad, 1ull);
+}
+
 struct Shape {
   const char* name;
   Op opa, opb;
@@ -33,6 +48,10 @@ int main(int argc, char** argv) {
       {"P  g=47  32x(1024x48x1024)", Op::N, Op::N, 1024, 48, 1024, 32, false, true},
       {"P  g=55  32x(1024x56x1024)", Op::N, Op::N, 1024, 56, 1024, 32, false, true},
       {"P  g=63  32x(1024x64x1024)", Op::N, Op::N, 1024, 64, 1024, 32, false, true},
+      // quantization / overhead probes of the recursion's P product: 16 x batch CTAs of 64 x 64 on 296 slots
+      {"P  N=64 batch 37 (2 full waves)", Op::N, Op::N, 1024, 64, 1024, 37, false, true},
+      {"P  N=64 batch 74 (4 full waves)", Op::N, Op::N, 1024, 64, 1024, 74, false, true},
+      {"P  N=64 batch 32, K = 4096", Op::N, Op::N, 1024, 64, 4096, 32, false, true},
       {"SYRK A^T A (1024,65536)", Op::T, Op::N, 1024, 1024, 65536, 1, true, false},
       {"square 4096^3", Op::N, Op::N, 4096, 4096, 4096, 1, false, false},
       {"sketch S^T A 2048x1024x65536", Op::T, Op::N, 2048, 1024, 65536, 1, false, false},
@@ -42,12 +61,15 @@ int main(int argc, char** argv) {
   size_t maxe = 0;
   for (auto& sh : shapes)
     maxe = std::max(maxe, (size_t)std::max({sh.m * sh.k * sh.batch, sh.k * sh.n * sh.batch, sh.m * sh.n * sh.batch}));
-  double *a, *b, *c;
+  double *a, *b, *c, *cref;
+  unsigned long long* bad;
   cudaMalloc(&a, maxe * 8);
   cudaMalloc(&b, maxe * 8);
   cudaMalloc(&c, maxe * 8);
-  cudaMemset(a, 0, maxe * 8);
-  cudaMemset(b, 0, maxe * 8);
+  cudaMalloc(&cref, maxe * 8);
+  cudaMalloc(&bad, 8);
+  tune_fill<<<148 * 8, 256>>>(a, maxe, 1);
+  tune_fill<<<148 * 8, 256>>>(b, maxe, 2);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -85,9 +107,20 @@ int main(int argc, char** argv) {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       double fl = 2.0 * sh.m * sh.n * sh.k * sh.batch * (sh.lower ? 0.5 : 1.0);
-      printf(" %s%6.1f", tile < 0 ? "auto:" : "", fl / (ms / iters * 1e-3) / 1e12);
+      // bits against the auto tile (lower_only shapes leave the upper triangle untouched: same in both)
+      const size_t ce = static_cast<size_t>(sh.m * sh.n * sh.batch);
+      unsigned long long hb = 0;
+      if (tile < 0) {
+        cudaMemcpyAsync(cref, c, ce * 8, cudaMemcpyDeviceToDevice, s);
+      } else {
+        cudaMemsetAsync(bad, 0, 8, s);
+        tune_diff<<<148 * 4, 256, 0, s>>>(c, cref, ce, bad);
+        cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, s);
+      }
+      cudaStreamSynchronize(s);
+      printf(" %s%6.1f%s", tile < 0 ? "auto:" : "", fl / (ms / iters * 1e-3) / 1e12, hb ? "!" : "");
     }
-    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64, 64x128w4, 128x64w4, 64x128k32, 128x64k32, 64x48, 128x48]\n");
+    printf("   TF/s [auto, 128x128, 64x64, 128x32, 64x32, 128x16, 64x128, 128x64, 64x128w4, 128x64w4, 64x128k32, 128x64k32, 64x48, 128x48, 128x{24,40,48,56,64}, 32x{16..64 step 8} 4x1 warps, 32x{32,48,64} 2x2 warps]; ! = bits differ from auto\n");
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
