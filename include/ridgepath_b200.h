@@ -28,8 +28,8 @@
  * one context must come from one host thread.  Distinct contexts hold
  * independent state and may be driven from different threads: calls are
  * synchronous and a per-device lock serializes the calls of contexts that
- * share a GPU (a TMA GEMM running next to higher-priority work was observed
- * to give wrong results, concurrency finding).
+ * share a GPU (so each call's phase timings are its own; correctness does not
+ * depend on it -- DESIGN.md, concurrency finding).
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H
@@ -151,7 +151,10 @@ RP_API const char* rp_last_error(const rp_ctx* ctx);
  * for the context's own stream. */
 RP_API rp_status rp_set_stream(rp_ctx* ctx, void* stream);
 RP_API rp_status rp_synchronize(rp_ctx* ctx);
-/* Options: "gram_mode" (-1 auto, 0 pass, 1 matrix); "profile" (0/1). */
+/* Options: "gram_mode" (-1 auto, 0 pass, 1 matrix); "profile" (0/1);
+ * "stream_priorities" (default 1: sketch and Cholesky-chain streams at the
+ * highest stream priority); "gram_overlap" (default 1: Gram matrix SYRK on a
+ * side stream); tuning knobs listed in DESIGN.md. */
 RP_API rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value);
 RP_API int64_t rp_launch_count(void);
 

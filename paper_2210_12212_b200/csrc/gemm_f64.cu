@@ -286,8 +286,11 @@ __device__ __forceinline__ void gemm_epilogue(const KParams& p, double (&acc)[C:
   // C = reduced values of warp-column w (in smem) -> consumer.  Loads are
   // issued U elements at a time before any store, so the L2 latency of the
   // read-modify-write consumers overlaps.
-  constexpr int U = 4;
   constexpr int PER = BM * C::TN;
+  // (a thread owns PER / THREADS elements of a warp-column: 8 in the 64 x 32 tile, 40-64 in the
+  // 128-row narrow tiles -- batches of 4 cost those up to 16 serialized L2 round trips per CTA)
+  constexpr int EPT = PER / C::THREADS;
+  constexpr int U = EPT >= 16 ? 16 : (EPT >= 8 ? 8 : 4);
   __shared__ ColInfo cinfo[C::TN];
   auto finish = [&](int w) {
     const int64_t col0 = n0 + w * C::TN;
@@ -298,13 +301,34 @@ __device__ __forceinline__ void gemm_epilogue(const KParams& p, double (&acc)[C:
     if (!active) {
       if (p.epi.kind == 0 && p.mirror) __syncthreads();
     } else if (p.epi.kind == 0) {
-      for (int idx = tid; idx < PER; idx += C::THREADS) {
-        const int rr = idx % BM, cc = idx / BM;
-        const int64_t row = m0 + rr, col = col0 + cc;
-        if (row < p.m && col < p.n && !(p.lower_only && row < col)) {
-          double* dst = Cb + row + col * p.ldc;
-          const double v = smem[cc * SLD + rr];
-          *dst = (p.beta == 0.0) ? p.alpha * v : p.alpha * v + p.beta * (*dst);
+      if (p.beta == 0.0) {
+        for (int idx = tid; idx < PER; idx += C::THREADS) {
+          const int rr = idx % BM, cc = idx / BM;
+          const int64_t row = m0 + rr, col = col0 + cc;
+          if (row < p.m && col < p.n && !(p.lower_only && row < col)) Cb[row + col * p.ldc] = p.alpha * smem[cc * SLD + rr];
+        }
+      } else {
+        // C <- alpha AB + beta C: the old values are fetched UB at a time before
+        // any store -- one element per iteration serialized a full L2 / HBM
+        // round trip per element (16 per thread and warp-column: the rank-64
+        // trailing updates of the Cholesky ran at 8 TF/s on it)
+        constexpr int UB = 8;
+        for (int base = tid; base < PER; base += UB * C::THREADS) {
+          double old[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+            const int64_t row = m0 + rr, col = col0 + cc;
+            old[u] = 0.0;
+            if (idx < PER && row < p.m && col < p.n && !(p.lower_only && row < col)) old[u] = __ldcg(Cb + row + col * p.ldc);
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int idx = base + u * C::THREADS, rr = idx % BM, cc = idx / BM;
+            const int64_t row = m0 + rr, col = col0 + cc;
+            if (idx < PER && row < p.m && col < p.n && !(p.lower_only && row < col))
+              Cb[row + col * p.ldc] = p.alpha * smem[cc * SLD + rr] + p.beta * old[u];
+          }
         }
       }
       if (p.mirror) {
@@ -1010,8 +1034,82 @@ void dgemm(const GemmArgs& g, cudaStream_t stream) {
   g_prof->recs.push_back(r);
 }
 
+// ---- joint (tile, split) plan of long-K products ---------------------------------
+// Products whose 128 x 128 tiles do not fill the GPU twice and whose reduction
+// order is free (not col_stable) -- the Gram-matrix SYRKs over the operator's
+// rows -- pick tile and split together from a time model:
+//   waves x per-CTA time + the partial-sum round trip,
+// per-CTA time = 2 bm bn (k / split + K0) flop at the SM's DMMA rate shared by
+// the tile's resident CTAs; K0 = 400 k-values of prologue + epilogue per CTA
+// (fitted: the 64 x 64 tile runs K = 1024 at 24.4 and K = 4096 at 31.1 TF/s);
+// lower_only counts only the tiles that run.  (Round 2: the split came from a
+// 128-tile wave count and the tile from an all-tiles count, which gave C3's
+// 2048 x 2048 x 1M SYRK 1056 CTAs of 64 x 32 x 1M -- 2.4 waves, 25 TF/s.)
+constexpr int kOccT[kNumTiles] = {1, 2, 2, 3, 3, 1, 1, 2, 2, 2, 2, 3, 2, 2, 2, 2, 2, 2};
+constexpr double kEffT[kNumTiles] = {0.97, 1.0, 0.99, 0.98, 0.94, 0.94, 0.98, 0.0, 0.0, 0.99, 0.99, 1.25, 0.0,
+                                 1.0, 1.0, 1.0, 1.0, 1.0};
+// CTAs of one batch entry and one split: all tiles, or (lower_only) the tiles
+// that reach the diagonal -- the kernel returns at once when m0 + BM <= n0.
+int64_t plan_ctas(const GemmArgs& g, int tile) {
+  const int64_t bm = kTiles[tile].bm, bn = kTiles[tile].bn;
+  const int64_t tm = ceil_div(g.m, bm), tn = ceil_div(g.n, bn);
+  if (!g.lower_only) return tm * tn;
+  int64_t c = 0;
+  for (int64_t j = 0; j < tn; ++j) {
+    const int64_t first = std::max<int64_t>(0, (j * bn - bm) / bm + 1);  // smallest i with i bm + bm > j bn
+    c += std::max<int64_t>(0, tm - first);
+  }
+  return c;
+}
+double plan_seconds(const GemmArgs& g, int tile, int split) {
+  const int64_t nb = g.batch * g.batch2;
+  const int64_t kc = ceil_div(ceil_div(g.k, split), 16) * 16;
+  const int64_t ctas = plan_ctas(g, tile) * nb * split;
+  const double waves = static_cast<double>(ceil_div(ctas, int64_t{148} * kOccT[tile]));
+  const double sm_rate = 35.0e12 / 148.0 * kEffT[tile];
+  const double t_cta = 2.0 * kTiles[tile].bm * kTiles[tile].bn * static_cast<double>(kc + 400) * kOccT[tile] / sm_rate;
+  const double mn = (g.lower_only ? 0.5 : 1.0) * static_cast<double>(g.m) * static_cast<double>(g.n);
+  const double t_red = split > 1 ? 4.0e-12 * mn * static_cast<double>(nb) * split + 5.0e-6 : 0.0;
+  return waves * t_cta + t_red;
+}
+bool plan_applies(const GemmArgs& g) {
+  if (g.col_stable || g.split_k > 0 || g.force_tile >= 0 || g.tri_k || g.epilogue || g.partials) return false;
+  if (g.k < 8192) return false;
+  const int64_t tm = ceil_div(g.m, 128), tn = ceil_div(g.n, 128);
+  int64_t tiles = tm * tn;
+  if (g.lower_only) {
+    tiles = 0;
+    for (int64_t i = 0; i < tm; ++i) tiles += std::min<int64_t>(tn, i + 1);
+  }
+  return tiles * g.batch * g.batch2 < 2 * 148;
+}
+void plan_long_k(const GemmArgs& g, int* tile_out, int* split_out) {
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(64, g.k / 512));
+  double best = 1e300;
+  *tile_out = 0;
+  *split_out = 1;
+  for (int t = 0; t < kNumTiles; ++t) {
+    if (kEffT[t] <= 0.0 || t >= 13 || kTileBK[t] > 16 || kTiles[t].bn == 16 || kTiles[t].bn == 48) continue;
+    for (int64_t s2 = 1; s2 <= cap; ++s2) {
+      const double sec = plan_seconds(g, t, static_cast<int>(s2));
+      if (sec < best * 0.999) {
+        best = sec;
+        *tile_out = t;
+        *split_out = static_cast<int>(s2);
+      }
+    }
+  }
+}
+
+
 // Split-K factor of a product (see dgemm_split in gemm_f64.h).
 int choose_split(const GemmArgs& g) {
+  if (plan_applies(g)) {
+    int t = 0, s2 = 1;
+    plan_long_k(g, &t, &s2);
+    const int64_t kc = std::max<int64_t>(16, ceil_div(ceil_div(g.k, s2), 16) * 16);
+    return static_cast<int>(std::max<int64_t>(1, ceil_div(g.k, kc)));
+  }
   const int64_t nb = g.batch * g.batch2;
   // Split-K.  With col_stable the factor depends on (m, k) only, never on n
   // (column determinism); otherwise it is picked for full waves over the
@@ -1090,6 +1188,11 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   const int64_t nb = g.batch * g.batch2;
   int tile = 0;
   double best = 1e300;
+  if (!vs && plan_applies(g)) {  // (long-K product: tile and split were chosen together)
+    int s2 = 1;
+    plan_long_k(g, &tile, &s2);
+    return tile;
+  }
   // Narrow products (N <= 64): one tile column, sized to N in steps of 8,
   // costed by the padded work on the busiest SM -- ceil(CTAs / 148) tiles of
   // BM x BN -- since such products never fill the GPU evenly.
@@ -1098,15 +1201,26 @@ int choose_tile(const GemmArgs& g, int split, int64_t k_chunk, bool vs) {
   // products it was neutral to negative, profiles/r02_narrow_tiles.txt)
   const bool narrow = g_narrow_tiles && g.n <= 64 && !vs && g.force_tile < 0 && !g.lower_only && nb > 1 &&
                       g.epilogue != nullptr && g.m >= 512;
+  static const int pgemm_tile = [] {  // RP_PGEMM_TILE=t: that tile for every such product (tuning probe)
+    const char* e = std::getenv("RP_PGEMM_TILE");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (narrow && pgemm_tile >= 0 && pgemm_tile < kNumTiles) return pgemm_tile;
   for (int t = 0; t < kNumTiles; ++t) {
     const bool narrow_tile = t >= 13;
     if (narrow) {
       // 128 x 16 / 32, 64 x 32 / 48 / 64 and the 128-row steps of 8
-      if (kTiles[t].bn < g.n || (!narrow_tile && t != 4 && t != 2 && t != 3 && t != 11 && t != 1)) continue;
+      // (the 64 x 32 tile may take two column tiles: 1024 short CTAs overlap one another's
+      // prologue and epilogue -- N = 57..64 in 145 us against 168 for one 64-wide column of
+      // tiles, profiles/r02_pgemm_tile_sweep.txt)
+      const bool two_cols = t == 3 && g.n > kTiles[t].bn && g.n <= 2 * kTiles[t].bn;
+      if ((kTiles[t].bn < g.n && !two_cols) || (!narrow_tile && t != 4 && t != 2 && t != 3 && t != 11 && t != 1))
+        continue;
       if (kEff[t] <= 0.0) continue;
       if (kTileBK[t] > 16 && k_chunk % kTileBK[t] != 0) continue;
-      const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * nb * split;
-      const double cost = static_cast<double>(ceil_div(ctas, 148)) * kTiles[t].bm * kTiles[t].bn / kEff[t];
+      const int64_t ctas = ceil_div(g.m, kTiles[t].bm) * ceil_div(g.n, kTiles[t].bn) * nb * split;
+      const double eff = t == 11 ? 1.0 : kEff[t];  // (64 x 48: 127 us at N = 33..40 where 128 x 40 takes 108)
+      const double cost = static_cast<double>(ceil_div(ctas, 148)) * kTiles[t].bm * kTiles[t].bn / eff;
       if (cost < best * 0.999) {
         best = cost;
         tile = t;

@@ -30,6 +30,7 @@ struct Shape {
   Op opa, opb;
   int64_t m, n, k, batch;
   bool lower, col_stable;
+  int split = 0;  // > 0: forced (the recursion's P product runs unsplit, fused epilogue)
 };
 
 int main(int argc, char** argv) {
@@ -40,19 +41,20 @@ int main(int argc, char** argv) {
       {"GW g=8   (1024x256x1024)", Op::N, Op::N, 1024, 256, 1024, 1, false, true},
       {"GW g=32  (1024x1024x1024)", Op::N, Op::N, 1024, 1024, 1024, 1, false, true},
       {"GW g=63  (1024x2016x1024)", Op::N, Op::N, 1024, 2016, 1024, 1, false, true},
-      {"P  g=1   32x(1024x2x1024)", Op::N, Op::N, 1024, 2, 1024, 32, false, true},
-      {"P  g=15  32x(1024x16x1024)", Op::N, Op::N, 1024, 16, 1024, 32, false, true},
-      {"P  g=31  32x(1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 32, false, true},
-      {"P  g=35  32x(1024x36x1024)", Op::N, Op::N, 1024, 36, 1024, 32, false, true},
-      {"P  g=41  32x(1024x42x1024)", Op::N, Op::N, 1024, 42, 1024, 32, false, true},
-      {"P  g=47  32x(1024x48x1024)", Op::N, Op::N, 1024, 48, 1024, 32, false, true},
-      {"P  g=55  32x(1024x56x1024)", Op::N, Op::N, 1024, 56, 1024, 32, false, true},
-      {"P  g=63  32x(1024x64x1024)", Op::N, Op::N, 1024, 64, 1024, 32, false, true},
+      {"P  g=1   32x(1024x2x1024)", Op::N, Op::N, 1024, 2, 1024, 32, false, true, 1},
+      {"P  g=15  32x(1024x16x1024)", Op::N, Op::N, 1024, 16, 1024, 32, false, true, 1},
+      {"P  g=31  32x(1024x32x1024)", Op::N, Op::N, 1024, 32, 1024, 32, false, true, 1},
+      {"P  g=35  32x(1024x36x1024)", Op::N, Op::N, 1024, 36, 1024, 32, false, true, 1},
+      {"P  g=41  32x(1024x42x1024)", Op::N, Op::N, 1024, 42, 1024, 32, false, true, 1},
+      {"P  g=47  32x(1024x48x1024)", Op::N, Op::N, 1024, 48, 1024, 32, false, true, 1},
+      {"P  g=55  32x(1024x56x1024)", Op::N, Op::N, 1024, 56, 1024, 32, false, true, 1},
+      {"P  g=63  32x(1024x64x1024)", Op::N, Op::N, 1024, 64, 1024, 32, false, true, 1},
       // quantization / overhead probes of the recursion's P product: 16 x batch CTAs of 64 x 64 on 296 slots
-      {"P  N=64 batch 37 (2 full waves)", Op::N, Op::N, 1024, 64, 1024, 37, false, true},
-      {"P  N=64 batch 74 (4 full waves)", Op::N, Op::N, 1024, 64, 1024, 74, false, true},
-      {"P  N=64 batch 32, K = 4096", Op::N, Op::N, 1024, 64, 4096, 32, false, true},
+      {"P  N=64 batch 37 (2 full waves)", Op::N, Op::N, 1024, 64, 1024, 37, false, true, 1},
+      {"P  N=64 batch 74 (4 full waves)", Op::N, Op::N, 1024, 64, 1024, 74, false, true, 1},
+      {"P  N=64 batch 32, K = 4096", Op::N, Op::N, 1024, 64, 4096, 32, false, true, 1},
       {"SYRK A^T A (1024,65536)", Op::T, Op::N, 1024, 1024, 65536, 1, true, false},
+      {"SYRK A^T A (2048,262144) [C3/4]", Op::T, Op::N, 2048, 2048, 262144, 1, true, false},
       {"square 4096^3", Op::N, Op::N, 4096, 4096, 4096, 1, false, false},
       {"sketch S^T A 2048x1024x65536", Op::T, Op::N, 2048, 1024, 65536, 1, false, false},
   };
@@ -97,6 +99,7 @@ int main(int argc, char** argv) {
       g.batch = sh.batch;
       g.lower_only = sh.lower;
       g.col_stable = sh.col_stable;
+      g.split_k = sh.split;
       g.force_tile = tile;
       for (int w = 0; w < 3; ++w) dgemm(g, s);
       cudaEventRecord(e0, s);
