@@ -475,8 +475,9 @@ def run_ours(args):
     # again with every GEMM bracketed by CUDA events on the step's stream
     # (the side-stream Gram overlap is switched off there, so each launch is
     # timed alone).
-    ctx.set_option("profile", 1)
     ctx.set_option("gram_overlap", 0)
+    arm.step()  # (untimed: the serialized schedule's first step sizes the main stream's split-K workspace)
+    ctx.set_option("profile", 1)
     prof = [arm.step() for _ in range(max(1, min(args.steps, 2)))]
     ctx.set_option("gram_overlap", 1)
     ctx.set_option("profile", 0)

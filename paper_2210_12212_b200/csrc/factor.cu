@@ -341,8 +341,10 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     return e && e[0] == '0';
   }();
   const bool chain_no_tma = !one_stream && chain_cp_async;
-  auto syrk_update = [&](int64_t row0, int64_t m, int64_t ncols, int64_t k0, int kb, cudaStream_t st) {
-    // C(row0.., row0..row0+ncols) -= A21(row0.., :) A21(row0..row0+ncols, :)^T, lower part
+  // C(rowc.., colc..colc+ncols) -= A21(rowc.., :) A21(colc..colc+ncols, :)^T over m rows; `lower`: a block
+  // with rowc == colc, only its part on and below the diagonal
+  auto panel_update = [&](int64_t rowc, int64_t colc, int64_t m, int64_t ncols, bool lower, int64_t k0, int kb,
+                          cudaStream_t st) {
     GemmArgs g;
     g.opa = Op::N;
     g.opb = Op::T;
@@ -351,22 +353,23 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     g.k = kb;
     g.alpha = -1.0;
     g.beta = 1.0;
-    g.a = h + row0 + k0 * ld;
+    g.a = h + rowc + k0 * ld;
     g.lda = ld;
     g.stride_a = stride;
-    g.b = g.a;
+    g.b = h + colc + k0 * ld;
     g.ldb = ld;
     g.stride_b = stride;
-    g.c = h + row0 + row0 * ld;
+    g.c = h + rowc + colc * ld;
     g.ldc = ld;
     g.stride_c = stride;
     g.batch = batch;
-    g.lower_only = true;
+    g.lower_only = lower;
     g.split_k = 1;
     g.no_tma = chain_no_tma && st != aux;
     dgemm(g, st);
   };
   cudaEvent_t prev_rest = nullptr;  // trailing update of the previous panel (aux stream)
+  cudaEvent_t prev_col = nullptr;   // previous panel's update of this block column below its diagonal block (aux)
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(std::min<int64_t>(NB, n - k0));
     if (blocked_diag())
@@ -376,6 +379,8 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     RP_LAUNCH_CHECK();
     const int64_t rows = n - k0 - kb;
     if (rows <= 0) break;
+    if (prev_col) RP_CUDA(cudaStreamWaitEvent(stream, prev_col, 0));  // (the rows the panel solve reads)
+    prev_col = nullptr;
     {
       // Panel: A21 <- A21 * L11^{-T}.  In place is safe: N = kb <= 64 fits one
       // 128x64 tile, so each CTA owns whole rows and reads its full A tile
@@ -404,18 +409,23 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
     const int64_t r0 = k0 + kb;
     const int64_t nxt = std::min<int64_t>(NB, rows), rest = rows - nxt;
     cudaEvent_t rest_done = nullptr;
-    if (rest > 0) {  // columns beyond the next block: aux stream
+    if (rest > 0) {
+      // aux stream: first the next block column below its diagonal block (the
+      // next panel solve's input), then the columns beyond it
       cudaEvent_t panel_done = new_event();
       RP_CUDA(cudaEventRecord(panel_done, stream));
       RP_CUDA(cudaStreamWaitEvent(aux, panel_done, 0));
-      syrk_update(r0 + nxt, rest, rest, k0, kb, aux);
+      panel_update(r0 + nxt, r0, rest, nxt, false, k0, kb, aux);
+      prev_col = new_event();
+      RP_CUDA(cudaEventRecord(prev_col, aux));
+      panel_update(r0 + nxt, r0 + nxt, rest, rest, true, k0, kb, aux);
       rest_done = new_event();
       RP_CUDA(cudaEventRecord(rest_done, aux));
     }
-    // the next block column (all rows below the diagonal) on the main stream;
-    // it also needs the previous panel's update of those columns
+    // chain: only the next diagonal block (the next potrf_diag's input); it
+    // also needs the previous panel's update of that block (aux)
     if (prev_rest) RP_CUDA(cudaStreamWaitEvent(stream, prev_rest, 0));
-    syrk_update(r0, rows, nxt, k0, kb, stream);
+    panel_update(r0, r0, nxt, nxt, true, k0, kb, stream);
     prev_rest = rest_done;
   }
   if (prev_rest) RP_CUDA(cudaStreamWaitEvent(stream, prev_rest, 0));
@@ -467,6 +477,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
         g1.batch = npairs;
         g1.batch2 = batch;
         g1.split_k = 1;
+        g1.tri_b = true;  // L11^{-1} is lower triangular: column j only needs k >= j
         dgemm(g1, stream);
         // X21 = -L22^{-1} * T  -> written over L21
         GemmArgs g2;
@@ -489,6 +500,7 @@ void spd_inverse_batched(double* h, int64_t n, int64_t ld, int64_t stride, int64
         g2.batch = npairs;
         g2.batch2 = batch;
         g2.split_k = 1;
+        g2.tri_a_lower = true;  // L22^{-1} is lower triangular: row i only needs k <= i
         dgemm(g2, stream);
       };
       combine(0, pairs_full, s);

@@ -76,6 +76,8 @@ struct KParams {
   bool lower_only;
   bool mirror;  // lower_only: also write the transposed element (C symmetric)
   bool tri_k;   // op(A)(i, k) == 0 for k < i: start the k loop at the tile's first row
+  bool tri_b;   // op(B)(k, j) == 0 for k < j: start the k loop at the tile's first column
+  bool tri_a_lower;  // op(A)(i, k) == 0 for k > i: end the k loop at the tile's last row
   bool no_tma;  // use the cp.async kernel (GemmArgs::no_tma)
   int occ_cap;  // host side only: GemmArgs::max_ctas_per_sm
   RecursionEpilogue epi;
@@ -287,10 +289,7 @@ __device__ __forceinline__ void gemm_epilogue(const KParams& p, double (&acc)[C:
   // issued U elements at a time before any store, so the L2 latency of the
   // read-modify-write consumers overlaps.
   constexpr int PER = BM * C::TN;
-  // (a thread owns PER / THREADS elements of a warp-column: 8 in the 64 x 32 tile, 40-64 in the
-  // 128-row narrow tiles -- batches of 4 cost those up to 16 serialized L2 round trips per CTA)
-  constexpr int EPT = PER / C::THREADS;
-  constexpr int U = EPT >= 16 ? 16 : (EPT >= 8 ? 8 : 4);
+  constexpr int U = 4;  // (batches of 8 / 16 were measured: no gain on C2's basis, and the 64 x 64 tile spills)
   __shared__ ColInfo cinfo[C::TN];
   auto finish = [&](int w) {
     const int64_t col0 = n0 + w * C::TN;
@@ -444,8 +443,10 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(KParams p) {
   const double* A = p.a + b1 * p.stride_a + b2 * p.stride_a2;
   const double* B = p.b + b1 * p.stride_b + b2 * p.stride_b2;
   int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
-  const int64_t kend = min(p.k, kbeg + p.k_chunk);
+  int64_t kend = min(p.k, kbeg + p.k_chunk);
   if (p.tri_k) kbeg = max(kbeg, m0 & ~static_cast<int64_t>(BK - 1));
+  if (p.tri_b) kbeg = max(kbeg, n0 & ~static_cast<int64_t>(BK - 1));
+  if (p.tri_a_lower) kend = min(kend, m0 + BM);  // (BM is a multiple of BK)
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
   double acc[C::FM][C::FN][2];
@@ -556,8 +557,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32)
   const int sidx = static_cast<int>(z % p.split);
   const int64_t b1 = bidx % p.batch, b2 = bidx / p.batch;
   int64_t kbeg = static_cast<int64_t>(sidx) * p.k_chunk;
-  const int64_t kend = min(p.k, kbeg + p.k_chunk);
+  int64_t kend = min(p.k, kbeg + p.k_chunk);
   if (p.tri_k) kbeg = max(kbeg, m0 & ~static_cast<int64_t>(BK - 1));
+  if (p.tri_b) kbeg = max(kbeg, n0 & ~static_cast<int64_t>(BK - 1));
+  if (p.tri_a_lower) kend = min(kend, m0 + BM);  // (BM is a multiple of BK)
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
   if (tid == 0) {
@@ -1073,7 +1076,7 @@ double plan_seconds(const GemmArgs& g, int tile, int split) {
   return waves * t_cta + t_red;
 }
 bool plan_applies(const GemmArgs& g) {
-  if (g.col_stable || g.split_k > 0 || g.force_tile >= 0 || g.tri_k || g.epilogue || g.partials) return false;
+  if (g.col_stable || g.split_k > 0 || g.force_tile >= 0 || g.tri_k || g.tri_b || g.tri_a_lower || g.epilogue || g.partials) return false;
   if (g.k < 8192) return false;
   const int64_t tm = ceil_div(g.m, 128), tn = ceil_div(g.n, 128);
   int64_t tiles = tm * tn;
@@ -1308,6 +1311,10 @@ void dgemm_impl(const GemmArgs& g, cudaStream_t stream) {
   kp.stride_c2 = g.stride_c2;
   kp.lower_only = g.lower_only;
   kp.tri_k = g.tri_k;
+  kp.tri_b = g.tri_b;
+  kp.tri_a_lower = g.tri_a_lower;
+  require(!(g.tri_k || g.tri_b || g.tri_a_lower) || (g.split_k == 1 && !g.col_stable),
+          "dgemm: triangular k ranges need an unsplit product");
   kp.no_tma = g.no_tma;
   kp.occ_cap = g.max_ctas_per_sm;
 

@@ -42,6 +42,12 @@ struct GemmArgs {
   // op(A)(i, k) == 0 for k < i (A^T of a lower-triangular matrix): each output
   // tile skips the k range below its first row.  Requires split_k == 1.
   bool tri_k = false;
+  // op(B)(k, j) == 0 for k < j (B lower triangular as a k x n matrix): each
+  // output tile starts its k range at its first column.  Requires split_k == 1.
+  bool tri_b = false;
+  // op(A)(i, k) == 0 for k > i (A lower triangular as an m x k matrix): each
+  // output tile ends its k range at its last row.  Requires split_k == 1.
+  bool tri_a_lower = false;
   // Use the cp.async kernel instead of the TMA one (A/B switch).
   bool no_tma = false;
   // At most this many CTAs of the launch per SM (0 = the kernel's natural
