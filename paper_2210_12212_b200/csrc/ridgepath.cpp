@@ -382,7 +382,7 @@ struct rp_ctx {
   // and the precond build; bit-identical to the single-stream path
   // (tools/race_stress.py, concurrency finding).
   bool gram_overlap = true;
-  bool gram_after_sketch = false;  // option "gram_after_sketch": start that SYRK after the sketch instead of before
+  int gram_after_sketch = 0;  // option "gram_after_sketch": start that SYRK after the sketch (1) or after the linear term too (2)
   int64_t upload_chunk_bytes = 32 << 20;  // option "upload_chunk_bytes": column chunk of RP_HOST_STREAM uploads
   std::vector<double> prof_seconds, prof_flops, prof_bytes;  // per-GEMM profile of the last profiled path
   int64_t csr_panel_rows = 65536;    // option "csr_panel_rows": row panel of the sparse Gram passes
@@ -1384,7 +1384,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
       sketch_apply(spec, op, sa.get(), s);
     }
     allreduce(ctx, sa.get(), spec.m * dim);
-    if (side_gram && ctx->gram_after_sketch) launch_side_gram();
+    if (side_gram && ctx->gram_after_sketch == 1) launch_side_gram();
     RP_CUDA(cudaEventRecord(ev.ev[1], s));
     // 3) Linear term: c = M^T b (primal) or c = b (dual).
     if (!dual) {
@@ -1392,6 +1392,7 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     } else {
       copy_cols(b.ptr, dim, K, dim, cbuf.get(), dim, s);
     }
+    if (side_gram && ctx->gram_after_sketch == 2) launch_side_gram();
     RP_CUDA(cudaEventRecord(ev.ev[5], s));
   }
   if (use_matrix && !gram.matrix) gram.build_matrix();  // (gram_overlap off)
@@ -1910,7 +1911,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       require(value >= 0 && value <= 4, "gram_overlap_occ must be in [0, 4]");
       ctx->gram_overlap_occ = static_cast<int>(value);
     } else if (k == "gram_after_sketch") {
-      ctx->gram_after_sketch = value != 0;
+      require(value >= 0 && value <= 2, "gram_after_sketch must be 0, 1 or 2");
+      ctx->gram_after_sketch = static_cast<int>(value);
     } else if (k == "gram_overlap") {
       ctx->gram_overlap = value != 0;
     } else if (k == "upload_chunk_bytes") {

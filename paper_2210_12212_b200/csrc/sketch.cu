@@ -515,12 +515,43 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
         zero_fill<<<grid_for(m * d), 256, 0, stream>>>(d_sa, m, d, m);
         RP_LAUNCH_CHECK();
       }
-      for (int64_t j0 = 0; j0 < op.n_loc; j0 += J) {
+      // Several slabs of a dense operator: slab j + 1 is drawn on a second
+      // stream (FP64 SIMT + integer work) while the DMMA GEMM consumes slab j;
+      // two slab buffers, events both ways.  (C3: 32 slabs, 1.8 ms of normals
+      // beside each 16 ms GEMM.)
+      const bool two_buf = !op.sparse && !one_stream && op.n_loc > J;
+      DBuf<double> slab_b;
+      cudaStream_t gs = stream;
+      std::vector<cudaEvent_t> evs;
+      auto new_event = [&]() {
+        cudaEvent_t e;
+        RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        return e;
+      };
+      cudaEvent_t gemm_done[2] = {nullptr, nullptr};
+      if (two_buf) {
+        slab_b.alloc(static_cast<size_t>(m * J), stream);
+        RP_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+        cudaEvent_t start = new_event();  // (the row states and both buffers exist in `stream` order)
+        RP_CUDA(cudaEventRecord(start, stream));
+        RP_CUDA(cudaStreamWaitEvent(gs, start, 0));
+      }
+      int64_t slab_index = 0;
+      for (int64_t j0 = 0; j0 < op.n_loc; j0 += J, ++slab_index) {
         const int64_t Jc = std::min(J, op.n_loc - j0);
-        if (one_stream)
-          draw_gauss_stream(spec.seed, 0, m * Jc, scale, slab.get(), stream);
-        else
-          gauss_rows_next(g, Jc, scale, slab.get(), Jc, stream);
+        double* const buf = (two_buf && (slab_index & 1)) ? slab_b.get() : slab.get();
+        if (one_stream) {
+          draw_gauss_stream(spec.seed, 0, m * Jc, scale, buf, stream);
+        } else {
+          if (two_buf && gemm_done[slab_index & 1]) RP_CUDA(cudaStreamWaitEvent(gs, gemm_done[slab_index & 1], 0));
+          gauss_rows_next(g, Jc, scale, buf, Jc, gs);
+          if (two_buf) {
+            cudaEvent_t drawn = new_event();
+            RP_CUDA(cudaEventRecord(drawn, gs));
+            RP_CUDA(cudaStreamWaitEvent(stream, drawn, 0));
+          }
+        }
         if (!op.sparse) {
           GemmArgs ga;
           ga.opa = Op::T;  // slab is row-major m x Jc == column-major Jc x m
@@ -528,7 +559,7 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
           ga.m = m;
           ga.n = d;
           ga.k = Jc;
-          ga.a = slab.get();
+          ga.a = buf;
           ga.lda = Jc;
           ga.b = op.trans ? op.a + j0 * op.ld : op.a + j0;
           ga.ldb = op.ld;
@@ -536,6 +567,10 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
           ga.ldc = m;
           ga.beta = j0 == 0 ? 0.0 : 1.0;
           dgemm(ga, stream);
+          if (two_buf) {
+            gemm_done[slab_index & 1] = new_event();
+            RP_CUDA(cudaEventRecord(gemm_done[slab_index & 1], stream));
+          }
         } else {
           dim3 tg(static_cast<unsigned>(ceil_div(Jc, 32)), static_cast<unsigned>(ceil_div(m, 32)));
           transpose_rm_to_cm<<<tg, dim3(32, 8), 0, stream>>>(slab.get(), m, Jc, slab_cm.get());
@@ -548,6 +583,8 @@ void sketch_apply(const SketchSpecC& spec, const OpView& op, double* d_sa, cudaS
           }
         }
       }
+      for (cudaEvent_t e : evs) RP_CUDA(cudaEventDestroy(e));  // (released once complete)
+      if (two_buf) RP_CUDA(cudaStreamDestroy(gs));  // (every draw was awaited by its GEMM on `stream`)
       return;
     }
     case kCountSketch:
