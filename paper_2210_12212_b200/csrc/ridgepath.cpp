@@ -352,6 +352,11 @@ struct rp_ctx {
   cudaStream_t copy = nullptr;  // upload stream of RP_HOST_STREAM operators (created on first use)
   cudaStream_t side = nullptr;  // side stream: the Gram matrix overlapping the sketch and the preconditioner build
   cudaStream_t hi = nullptr;    // second stream: the sketch while the Gram matrix is in flight
+  cudaStream_t basis2 = nullptr;  // second stream of the two-group basis recursion (option "basis_streams")
+  // option "basis_streams": 1 = one recursion over all intervals, 2 = two interval groups on two streams,
+  // interleaved generation by generation (exact; measured: no gain -- C2 -0.1 ms, C4 7.73 vs 7.72 s, the
+  // sparse Gram passes and the other group's GEMMs each fill every SM and take turns instead of overlapping)
+  int basis_streams = 1;
   rpb::OperatorStore op;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -394,6 +399,7 @@ struct rp_ctx {
   // intervals (all-gather of the inverses); 0 = every rank applies it whole
   bool feature_shard = true;
   bool csr_l2_persist = false;  // option "csr_l2_persist": sparse Gram running sums as an L2-persisting window
+  int csr_blocks_per_sm = 0;  // option "csr_blocks_per_sm": cap of the sparse passes' 256-thread blocks per SM (0 = none)
   std::string err;
 };
 
@@ -612,7 +618,7 @@ struct GramOp {
       const PanelView pv = one_panel ? single_panel(op.n_loc, op.d, op.csc_off, op.csc_row, op.csc_val)
                                      : view_of(panel_csc(ctx, op));
       sparse_gram(op.csr_off, op.csr_col, op.csr_val, pv, W, op.d, cols, Y, op.d, ctx->csr_chunk, s,
-                  ctx->csr_l2_persist);
+                  ctx->csr_l2_persist, ctx->csr_blocks_per_sm);
       allreduce(ctx, Y, op.d * cols);
       return;
     }
@@ -1448,17 +1454,56 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   // 5) Bases for all owned intervals at once; diverged intervals are retried
   //    at tau/2 (path_solver.cpp:132-140).
   BasisRun run2;
-  // the first attempt's bases: one run over all owned intervals (part p of
-  // `runs` covers own positions [pbeg[p], pend[p]); a two-stream split of
-  // the intervals was measured at -0.1 ms on C2 and found run-to-run
-  // nondeterministic on C3, so it is not used)
+  // the first attempt's bases: one run over all owned intervals, or two runs
+  // over the two halves on two streams (part p of `runs` covers own positions
+  // [pbeg[p], pend[p]); in Gram-matrix mode the split was measured at -0.1 ms
+  // on C2, so there it is opt-in; its round-2 run-to-run differences on C3
+  // were the TMA stage-release race, fixed since)
   std::vector<BasisRun> runs(1);
   std::vector<int64_t> pbeg{0}, pend{Lo};
   std::vector<int64_t> retry;             // positions in `own`
   std::vector<int> retry_slot(static_cast<size_t>(Lo), -1);
   int failed = 0;
   if (Lo > 0) {
-    run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, runs[0]);
+    // Option "basis_streams" = 2: two interval groups on two streams
+    // (BasisStepper), interleaved generation by generation: exact (every
+    // group runs the one-stream arithmetic on its own intervals).
+    const bool two_ok = Lo >= 2 && !has_comm(ctx) && (gram.matrix || op.sparse);
+    const bool two = two_ok && ctx->basis_streams == 2;
+    if (!two) {
+      run_basis(ctx, gram, P, cbuf.get(), K, taus, ks, runs[0]);
+    } else {
+      if (!ctx->basis2) RP_CUDA(cudaStreamCreateWithFlags(&ctx->basis2, cudaStreamNonBlocking));
+      // (the lazily built panel structure of the sparse Gram passes: once, here, before the second stream reads it)
+      if (!gram.matrix && op.sparse) (void)GramOp::panel_csc(ctx, op);
+      const int64_t h = (Lo + 1) / 2;
+      runs.resize(2);
+      pbeg = {0, h};
+      pend = {h, Lo};
+      const PrecondBatch PA = P.slice(ctx, 0, h), PB = P.slice(ctx, h, Lo);
+      cudaEvent_t fork;
+      RP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      RP_CUDA(cudaEventRecord(fork, s));
+      RP_CUDA(cudaStreamWaitEvent(ctx->basis2, fork, 0));
+      {
+        BasisStepper A(ctx, gram, PA, runs[0], s), B(ctx, gram, PB, runs[1], ctx->basis2);
+        A.begin(cbuf.get(), K, std::vector<double>(taus.begin(), taus.begin() + h),
+                std::vector<int>(ks.begin(), ks.begin() + h));
+        B.begin(cbuf.get(), K, std::vector<double>(taus.begin() + h, taus.end()),
+                std::vector<int>(ks.begin() + h, ks.end()));
+        for (int64_t g = 1; g < std::max(A.kmax, B.kmax); ++g) {
+          A.step(g);
+          B.step(g);
+        }
+        A.finish();
+        B.finish();
+        RP_CUDA(cudaEventRecord(fork, ctx->basis2));  // (the steppers' buffers are freed on their streams)
+      }
+      RP_CUDA(cudaStreamWaitEvent(s, fork, 0));
+      RP_CUDA(cudaStreamSynchronize(s));
+      RP_CUDA(cudaStreamSynchronize(ctx->basis2));
+      RP_CUDA(cudaEventDestroy(fork));
+    }
     for (size_t q = 0; q < runs.size(); ++q)
       for (int64_t i = pbeg[q]; i < pend[q]; ++i)
         if (runs[q].diverged[static_cast<size_t>(i - pbeg[q])]) retry.push_back(i);
@@ -1845,6 +1890,11 @@ void rp_destroy(rp_ctx* ctx) {
       cudaStreamSynchronize(ctx->hi);
       cudaStreamDestroy(ctx->hi);
     }
+    if (ctx->basis2) {
+      release_workspace(ctx->basis2);
+      cudaStreamSynchronize(ctx->basis2);
+      cudaStreamDestroy(ctx->basis2);
+    }
     if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
     if (ctx->own) {
@@ -1888,8 +1938,14 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "gram_overlap_split") {
       require(value >= 0 && value <= 64, "gram_overlap_split must be in [0, 64]");
       ctx->gram_overlap_split = static_cast<int>(value);
+    } else if (k == "csr_blocks_per_sm") {
+      require(value >= 0 && value <= 8, "csr_blocks_per_sm must be in [0, 8]");
+      ctx->csr_blocks_per_sm = static_cast<int>(value);
     } else if (k == "csr_l2_persist") {
       ctx->csr_l2_persist = value != 0;
+    } else if (k == "basis_streams") {
+      require(value == 1 || value == 2, "basis_streams must be 1 or 2");
+      ctx->basis_streams = static_cast<int>(value);
     } else if (k == "feature_shard") {
       ctx->feature_shard = value != 0;
     } else if (k == "stream_priorities") {

@@ -182,16 +182,24 @@ __global__ void __launch_bounds__(256) pass2_kernel(const int64_t* __restrict__ 
   }
 }
 
+// blocks_per_sm > 0: the passes run as that many 256-thread blocks per SM, leaving the rest of every SM to
+// another stream's kernels (the two-stream basis recursion: these gather-bound passes beside the other
+// interval group's tensor-bound GEMMs).
 template <int CPL>
 void run_chunk(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
-               const double* wr, int cc, double* yp, double* z, cudaStream_t s) {
+               const double* wr, int cc, double* yp, double* z, cudaStream_t s, int blocks_per_sm) {
+  // (a grid of 148 x blocks_per_sm blocks lands that many blocks on every SM; the passes walk their rows /
+  // columns with grid-stride loops.  Registers and shared memory stay free for the other stream's CTAs.)
+  const int pad = 0;
+  const unsigned cap = blocks_per_sm > 0 ? 148u * static_cast<unsigned>(blocks_per_sm) : 148u * 32u;
   for (int64_t p = 0; p < pc.panels; ++p) {
     const int64_t row0 = p * pc.panel_rows;
     const int64_t rows = std::min(pc.panel_rows, pc.n - row0);
-    pass1_kernel<CPL><<<grid_for(rows * 32), 256, 0, s>>>(csr_off, csr_col, csr_val, row0, rows, wr, cc, yp);
+    pass1_kernel<CPL><<<std::min(grid_for(rows * 32), cap), 256, pad, s>>>(csr_off, csr_col, csr_val, row0, rows, wr,
+                                                                          cc, yp);
     RP_LAUNCH_CHECK();
-    pass2_kernel<CPL><<<grid_for(pc.d * 32), 256, 0, s>>>(pc.off + p * pc.d, pc.row, pc.val, pc.d,
-                                                          row0, yp, cc, z, p == 0);
+    pass2_kernel<CPL><<<std::min(grid_for(pc.d * 32), cap), 256, pad, s>>>(pc.off + p * pc.d, pc.row, pc.val, pc.d,
+                                                                          row0, yp, cc, z, p == 0);
     RP_LAUNCH_CHECK();
   }
 }
@@ -222,7 +230,7 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
 
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s,
-                 bool l2_persist) {
+                 bool l2_persist, int blocks_per_sm) {
   if (cols <= 0 || pc.d <= 0) return;
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, 128));
   const int64_t cmax = std::min(chunk, cols);
@@ -260,13 +268,13 @@ void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* c
     if (pc.n == 0) {
       fill(z.get(), pc.d * cc, 0.0, s);
     } else if (cc <= 32) {
-      run_chunk<1>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+      run_chunk<1>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s, blocks_per_sm);
     } else if (cc <= 64) {
-      run_chunk<2>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+      run_chunk<2>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s, blocks_per_sm);
     } else if (cc <= 96) {
-      run_chunk<3>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+      run_chunk<3>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s, blocks_per_sm);
     } else {
-      run_chunk<4>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s);
+      run_chunk<4>(csr_off, csr_col, csr_val, pc, wr.get(), cc, yp.get(), z.get(), s, blocks_per_sm);
     }
     transpose(z.get(), cc, pc.d, cc, Y + c0 * ldy, ldy, s);  // back to column-major
   }

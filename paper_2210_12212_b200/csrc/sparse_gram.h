@@ -61,6 +61,6 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
 // Y_p gathers do not evict them.
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s,
-                 bool l2_persist = false);
+                 bool l2_persist = false, int blocks_per_sm = 0);
 
 }  // namespace rpb

@@ -28,3 +28,9 @@ RP_GRAM_W_ONLY=8 timeout 900 ncu --set full --clock-control none --import-source
     python tools/gram_pass_bench.py > gpurun_out/r02_ncu_gram_w8.log 2>&1
 echo "gram rc=$?"
 fi
+# Summaries on the box; the reports themselves (tens of MB each) stay behind unless KEEP_REP=1.
+for r in r02_gemm_c2 r02_gram_w1 r02_gram_w8; do
+  [ -f gpurun_out/$r.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$r.ncu-rep > gpurun_out/${r}_summary.json 2>/dev/null
+  [ -z "$KEEP_REP" ] && rm -f gpurun_out/$r.ncu-rep
+done
+du -sh gpurun_out
