@@ -82,6 +82,9 @@ __global__ void __launch_bounds__(256) atv_partial_kernel(const double* __restri
 __global__ void __launch_bounds__(256) sum_chunks_tree_kernel(const double* __restrict__ part, int64_t chunks,
                                                               int64_t total, double* __restrict__ x) {
   __shared__ double red[16][17];
+  // (launched programmatically after the pass that writes `part`: resident early, waits here for that grid;
+  // a no-op under a plain launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int o = threadIdx.x & 15, g = threadIdx.x >> 4;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * 16 + o;
   double s = 0.0;
@@ -483,6 +486,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   double* ypart = ring + stages * STAGE;  // [2][kGWarps][64]
   __shared__ __align__(8) uint64_t full[kPMaxStages];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  // (the partial-sum kernel behind this pass is launched programmatically: its blocks may take the SMs'
+  // free slots early; they wait for this grid's completion before reading the partials)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t nb = (n + kGRows - 1) / kGRows;
   const int64_t b0 = (static_cast<int64_t>(blockIdx.x) * nb) / gridDim.x;
   const int64_t cnt = (static_cast<int64_t>(blockIdx.x + 1) * nb) / gridDim.x - b0;
@@ -740,7 +746,22 @@ bool gram_dmma_launch_nt(const double* a, int64_t lda, int64_t n, int64_t d, con
   ensure_dynamic_smem(gram_dmma_kernel<NT, NW>, smem);
   gram_dmma_kernel<NT, NW><<<grid, NW * 32, smem, s>>>(map, n, d, static_cast<int>(k), w, ws.get(), stages);
   RP_LAUNCH_CHECK();
-  sum_chunks_tree_kernel<<<static_cast<unsigned>(ceil_div(d * k, 16)), 256, 0, s>>>(ws.get(), grid, d * k, z);
+  {
+    // the CTA-partial sum starts its blocks while the pass drains (programmatic dependent launch)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(ceil_div(d * k, 16)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const double* part = ws.get();
+    const int64_t chunks = grid, total = d * k;
+    RP_CUDA(cudaLaunchKernelEx(&cfg, sum_chunks_tree_kernel, part, chunks, total, z));
+  }
   RP_LAUNCH_CHECK();
   return true;
 }
