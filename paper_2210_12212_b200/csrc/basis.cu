@@ -97,6 +97,38 @@ __global__ void compose_kernel(BasisDims d, const double* __restrict__ tilde, co
   }
 }
 
+// One thread per (interval l, grid slot c): the column of powers, in j order.
+__global__ void compose_coeffs_kernel(BasisDims d, const double* __restrict__ tau, const int* __restrict__ kb,
+                                      const double* __restrict__ lambda, const int* __restrict__ off,
+                                      const int* __restrict__ cnt, int64_t tmax, double* __restrict__ coef) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= d.L * tmax) return;
+  const int64_t l = idx / tmax, c = idx - l * tmax;
+  double* col = coef + (l * tmax + c) * d.kmax;
+  const bool live = c < cnt[l];
+  const double ta = tau[l];
+  const double tt = live ? __dmul_rn(ta, lambda[off[l] + c]) : 0.0;
+  const int k = kb[l];
+  double pw = ta;
+  for (int j = 0; j < d.kmax; ++j) {
+    col[j] = (live && j < k) ? pw : 0.0;
+    pw = __dmul_rn(pw, tt);
+  }
+}
+
+// Grid: x = dim chunks, y = padded column (l, c, r); dead slots return at once.
+__global__ void compose_gather_kernel(BasisDims d, const double* __restrict__ xpad, const int* __restrict__ off,
+                                      const int* __restrict__ cnt, int64_t tmax, double* __restrict__ x, int64_t col0) {
+  const int64_t col = blockIdx.y + col0;  // (l*tmax + c)*K + r
+  const int64_t r = col % d.K, lc = col / d.K, l = lc / tmax, c = lc - l * tmax;
+  if (c >= cnt[l]) return;
+  const double* src = xpad + col * d.dim;
+  double* dst = x + ((off[l] + c) * d.K + r) * d.dim;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d.dim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
 __global__ void woodbury_tail_kernel(int64_t dim, int64_t cols, int64_t L, const double* __restrict__ args,
                                      int64_t s_args, const double* __restrict__ t3, int64_t s_t3,
                                      const double* __restrict__ lambda0, double* __restrict__ out, int64_t s_out) {
@@ -285,6 +317,21 @@ void compose(const BasisDims& d, const double* tilde, const double* d_tau, const
   if (T <= 0) return;
   for_col_chunks(d.dim, d.K * T, [&](dim3 grid, int64_t c0) {
     compose_kernel<<<grid, 256, 0, stream>>>(d, tilde, d_tau, d_k, d_lambda, d_interval, T, x, c0);
+  });
+}
+
+void compose_coeffs(const BasisDims& d, const double* d_tau, const int* d_k, const double* d_lambda, const int* d_off,
+                    const int* d_cnt, int64_t tmax, double* coef, cudaStream_t stream) {
+  if (d.L <= 0 || tmax <= 0) return;
+  compose_coeffs_kernel<<<grid_for(d.L * tmax), 256, 0, stream>>>(d, d_tau, d_k, d_lambda, d_off, d_cnt, tmax, coef);
+  RP_LAUNCH_CHECK();
+}
+
+void compose_gather(const BasisDims& d, const double* xpad, const int* d_off, const int* d_cnt, int64_t tmax, double* x,
+                    cudaStream_t stream) {
+  if (d.L <= 0 || tmax <= 0) return;
+  for_col_chunks(d.dim, d.L * tmax * d.K, [&](dim3 grid, int64_t c0) {
+    compose_gather_kernel<<<grid, 256, 0, stream>>>(d, xpad, d_off, d_cnt, tmax, x, c0);
   });
 }
 

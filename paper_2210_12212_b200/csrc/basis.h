@@ -51,6 +51,17 @@ void update_gen(const BasisDims& d, int64_t g, const Partials& applied, const in
 void compose(const BasisDims& d, const double* tilde, const double* d_tau, const int* d_k, const double* d_lambda,
              const int* d_interval, int64_t T, double* x, cudaStream_t stream);
 
+// Composition as a product (north_star 6): for interval l with cnt[l] grid
+// points starting at position off[l] of d_lambda, the k x tmax coefficient
+// block  coef[l][j + c*kmax] = tau_l (tau_l lambda_{off[l]+c})^j  (j < k_l,
+// c < cnt[l]; zero elsewhere), so that  x(lambda) = U_l coef[l]  with U_l the
+// interval's dim x kmax basis.  compose_gather copies the cnt[l]*K columns of
+// each interval's padded dim x (tmax*K) result block to x[:, (off[l]+c)*K + r].
+void compose_coeffs(const BasisDims& d, const double* d_tau, const int* d_k, const double* d_lambda, const int* d_off,
+                    const int* d_cnt, int64_t tmax, double* coef, cudaStream_t stream);
+void compose_gather(const BasisDims& d, const double* xpad, const int* d_off, const int* d_cnt, int64_t tmax, double* x,
+                    cudaStream_t stream);
+
 // out_l = (args_l - t3_l) / lambda0_l for l < L (Woodbury preconditioner tail);
 // each operand is dim x cols contiguous per interval at its own interval
 // stride (s_args = 0 broadcasts one input).

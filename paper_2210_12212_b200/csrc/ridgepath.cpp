@@ -371,6 +371,7 @@ struct rp_ctx {
   double last_device_seconds = 0.0;  // profile: device time of the last product call
   bool fuse_update = true;           // option "fuse_update": recursion update in the P GEMM epilogue
   bool stable_columns = true;        // option "stable_columns": column-stable GEMMs inside the path
+  bool compose_gemm = true;          // option "compose_gemm": x(lambda) as a DMMA GEMM (0: Horner kernel, the reference's order)
   int gram_overlap_tile = -1;  // option "gram_overlap_tile": GEMM tile of the overlapped Gram SYRK (-1 = auto)
   // option "gram_overlap_tma": 1 = the overlapped SYRK on the TMA kernel (0: cp.async, A/B switch)
   bool gram_overlap_tma = true;
@@ -1235,6 +1236,60 @@ struct NvtxPhases {
   }
 };
 
+// Composition of T grid points (sorted by interval: itv ascending) into
+// x[:, t*K + r].  Default: one FP64 DMMA GEMM batched over (interval, right-hand
+// side) -- x(lambda) = U_l (dim x kmax) times the interval's kmax x tmax block of
+// coefficients tau_l (tau_l lambda)^j, padded to the largest interval and
+// gathered (north_star 6).  Option "compose_gemm" = 0: the reference's Horner
+// order, one thread per entry (compose_horner, path_solver.cpp:64-74).
+void compose_points(rp_ctx* ctx, const BasisRun& R, const std::vector<int>& itv, const double* d_lam, const int* d_itv,
+                    int64_t Tn, double* x) {
+  cudaStream_t s = ctx->stream;
+  const BasisDims& d = R.dims;
+  bool sorted = true;
+  for (size_t i = 1; i < itv.size(); ++i) sorted = sorted && itv[i - 1] <= itv[i];
+  if (!ctx->compose_gemm || !sorted || d.kmax < 2) {
+    compose(d, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam, d_itv, Tn, x, s);
+    return;
+  }
+  std::vector<int> off(static_cast<size_t>(d.L), 0), cnt(static_cast<size_t>(d.L), 0);
+  for (int64_t t = 0; t < Tn; ++t) {
+    if (cnt[itv[t]] == 0) off[itv[t]] = static_cast<int>(t);
+    ++cnt[itv[t]];
+  }
+  int64_t tmax = 1;
+  for (int c : cnt) tmax = std::max<int64_t>(tmax, c);
+  tmax = (tmax + 7) & ~int64_t{7};  // (whole 8-column DMMA fragments; keeps the operand strides even)
+  DBuf<int> d_off(static_cast<size_t>(d.L), s), d_cnt(static_cast<size_t>(d.L), s);
+  RP_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int) * d.L, cudaMemcpyHostToDevice, s));
+  RP_CUDA(cudaMemcpyAsync(d_cnt.get(), cnt.data(), sizeof(int) * d.L, cudaMemcpyHostToDevice, s));
+  DBuf<double> coef(static_cast<size_t>(d.L * tmax * d.kmax), s);
+  DBuf<double> xpad(static_cast<size_t>(d.L * tmax * d.K * d.dim), s);
+  compose_coeffs(d, R.d_tau.get(), R.d_k.get(), d_lam, d_off.get(), d_cnt.get(), tmax, coef.get(), s);
+  GemmArgs g;  // batch = interval l, batch2 = right-hand side r
+  g.m = d.dim;
+  g.n = tmax;
+  g.k = d.kmax;
+  g.a = R.tilde.get();           // U_{l,r}: column j at ((j*NB + l*K + r) * dim)
+  g.lda = d.nb() * d.dim;
+  g.stride_a = d.K * d.dim;
+  g.stride_a2 = d.dim;
+  g.b = coef.get();              // kmax x tmax per interval, shared by the right-hand sides
+  g.ldb = d.kmax;
+  g.stride_b = d.kmax * tmax;
+  g.stride_b2 = 0;
+  g.c = xpad.get();              // column (l*tmax + c)*K + r
+  g.ldc = d.K * d.dim;
+  g.stride_c = tmax * d.K * d.dim;
+  g.stride_c2 = d.dim;
+  g.batch = d.L;
+  g.batch2 = d.K;
+  g.split_k = 1;
+  dgemm(g, s);
+  compose_gather(d, xpad.get(), d_off.get(), d_cnt.get(), tmax, x, s);
+  RP_CUDA(cudaStreamSynchronize(s));  // (off / cnt are host vectors of this frame)
+}
+
 // ---- run_path (path_solver.cpp:147-190) ------------------------------------------
 
 struct Events {
@@ -1569,11 +1624,10 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // grid points of one batch are contiguous in t when no interval is skipped
     const bool contiguous = tidx.back() - tidx.front() + 1 == Tn;
     if (contiguous) {
-      compose(R.dims, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam.get(), d_itv.get(), Tn,
-              xs.get() + tidx.front() * dim * K, s);
+      compose_points(ctx, R, itv, d_lam.get(), d_itv.get(), Tn, xs.get() + tidx.front() * dim * K);
     } else {
       DBuf<double> tmp(static_cast<size_t>(dim * K * Tn), s);
-      compose(R.dims, R.tilde.get(), R.d_tau.get(), R.d_k.get(), d_lam.get(), d_itv.get(), Tn, tmp.get(), s);
+      compose_points(ctx, R, itv, d_lam.get(), d_itv.get(), Tn, tmp.get());
       for (int64_t i = 0; i < Tn; ++i)
         copy_cols(tmp.get() + i * dim * K, dim, K, dim, xs.get() + tidx[i] * dim * K, dim, s);
     }
@@ -1930,6 +1984,8 @@ rp_status rp_set_option(rp_ctx* ctx, const char* key, int64_t value) {
       ctx->profile = value != 0;
     } else if (k == "fuse_update") {
       ctx->fuse_update = value != 0;
+    } else if (k == "compose_gemm") {
+      ctx->compose_gemm = value != 0;
     } else if (k == "stable_columns") {
       ctx->stable_columns = value != 0;
     } else if (k == "csr_panel_rows") {

@@ -432,3 +432,27 @@ def test_virtual_split_bitwise(name, scale, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         xs.append(np.load(out))
     assert np.array_equal(xs[0], xs[1])
+
+
+def test_compose_gemm_matches_horner(rp, ctx, oracle):
+    """x(lambda) composed as a batched DMMA GEMM (interval basis times the
+    interval's coefficient block tau (tau lambda)^j, the default) against the
+    reference's Horner order (option compose_gemm = 0; compose_horner,
+    path_solver.cpp:64-74): same sums in another order -- 1e-12 -- for a
+    matrix right-hand side, a grid that leaves intervals empty and a
+    one-point grid."""
+    w = workloads.c1(scale=0.25)
+    (oa, ocfg, ospec, orho), (ga, gcfg, gspec, grho) = _mirror(rp, oracle, w)
+    B = np.asfortranarray(np.column_stack([w.b[:, 0], 2 * w.b[:, 0] + 1, w.b[:, 0] ** 2]))
+    full = list(gcfg.lambdas)
+    for grid in (full, full[:3] + full[-2:], [full[len(full) // 2]]):
+        cfg = rp.PathConfig(gcfg.lambda_min, gcfg.lambda_max, grid, gcfg.epsilon, gcfg.num_intervals)
+        out = []
+        for flag in (1, 0):
+            ctx.set_option("compose_gemm", flag)
+            out.append(rp.ihs_bin_path_matrix(ga, B, cfg, gspec, grho, ctx=ctx))
+        ctx.set_option("compose_gemm", 1)
+        assert len(out[0].points) == len(grid)
+        for pg, ph in zip(out[0].points, out[1].points):
+            assert pg.lam == ph.lam
+            assert oracle.rel_error(pg.solution, ph.solution) < 1e-12
