@@ -26,10 +26,10 @@
  *
  * Threading: a context is single-owner (like SeededRng); calls on
  * one context must come from one host thread.  Distinct contexts hold
- * independent state and may be driven from different threads: calls are
- * synchronous and a per-device lock serializes the calls of contexts that
- * share a GPU (so each call's phase timings are its own; correctness does not
- * depend on it -- DESIGN.md, concurrency finding).
+ * independent state and may be driven from different threads concurrently;
+ * calls are synchronous.  (RP_DEVICE_LOCK=1 in the environment serializes
+ * the calls of contexts that share a GPU, e.g. to keep one call's phase
+ * timings free of another's work.)
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H

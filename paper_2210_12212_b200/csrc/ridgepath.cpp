@@ -1687,11 +1687,12 @@ namespace {
 
 thread_local std::string g_err_noctx;
 
-// One lock per device, held for the whole of every context call: calls are
-// synchronous, so contexts sharing a GPU in one process never overlap their
-// device work (a second line of defence next to the single stream priority:
-// the TMA pipelines must not be preempted, concurrency finding).
-// Recursive: a call may use another entry point.
+// Optional lock per device (RP_DEVICE_LOCK=1), held for the whole of every
+// context call, so that contexts sharing a GPU in one process never overlap
+// their device work.  Rounds 1-2 needed it (concurrent grids exposed the TMA
+// GEMM's stage-release race, concurrency finding); since the fix
+// contexts driven from different threads run concurrently and the lock is
+// off by default.  Recursive: a call may use another entry point.
 std::recursive_mutex& device_mutex(int dev) {
   static std::recursive_mutex m[64];
   return m[static_cast<unsigned>(dev) % 64];
@@ -1702,12 +1703,12 @@ rp_status guarded(rp_ctx* ctx, F&& f) {
   try {
     std::optional<DeviceGuard> guard;
     std::unique_lock<std::recursive_mutex> lock;
-    static const bool no_lock = [] {  // RP_NO_DEVICE_LOCK=1: probe only (tools/concurrency_probe.py)
-      const char* e = std::getenv("RP_NO_DEVICE_LOCK");
+    static const bool use_lock = [] {  // RP_DEVICE_LOCK=1: serialize the calls of contexts that share a GPU
+      const char* e = std::getenv("RP_DEVICE_LOCK");
       return e && e[0] == '1';
     }();
     if (ctx) {
-      if (!no_lock) lock = std::unique_lock<std::recursive_mutex>(device_mutex(ctx->device));
+      if (use_lock) lock = std::unique_lock<std::recursive_mutex>(device_mutex(ctx->device));
       guard.emplace(ctx->device);
     }
     f();
