@@ -19,6 +19,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <limits>
 #include <chrono>
 #include <string_view>
 #include <cerrno>
@@ -1766,7 +1767,10 @@ void set_csr_impl(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, 
   require(n_local >= 0 && d >= 0 && n_global >= n_local, "csr: negative dimensions");
   require(d < (int64_t{1} << 31) && n_local < (int64_t{1} << 31), "csr: dimensions exceed int32 indices");
   cudaStream_t s = ctx->stream;
-  // Bring the arrays to the host for validation and the CSC build.
+  // Row offsets are validated on the host (n + 1 values); the entries never
+  // visit the host: invariants, int32 columns and the CSC mirror (a stable
+  // radix sort by column keeps the rows of a column ascending, as the
+  // reference's counting pass does) are built on the device.
   std::vector<int64_t> off(static_cast<size_t>(n_local + 1));
   if (where == RP_DEVICE) {
     RP_CUDA(cudaMemcpy(off.data(), offsets, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
@@ -1774,65 +1778,58 @@ void set_csr_impl(rp_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local, 
     std::memcpy(off.data(), offsets, sizeof(int64_t) * (n_local + 1));
   }
   require(off.front() == 0, "csr: row_offsets must start at 0");
+  for (int64_t i = 0; i < n_local; ++i) require(off[i] <= off[i + 1], "csr: row_offsets must be monotone");
   const int64_t nnz = off.back();
-  std::vector<int64_t> c64(static_cast<size_t>(nnz));
-  std::vector<double> v(static_cast<size_t>(nnz));
-  if (where == RP_DEVICE) {
-    RP_CUDA(cudaMemcpy(c64.data(), cols, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-    RP_CUDA(cudaMemcpy(v.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
-  } else {
-    std::memcpy(c64.data(), cols, sizeof(int64_t) * nnz);
-    std::memcpy(v.data(), vals, sizeof(double) * nnz);
-  }
-  // CsrMatrix invariants (matrix.cpp:22-50).
-  std::vector<int32_t> c32(static_cast<size_t>(nnz));
-  std::vector<int64_t> ccount(static_cast<size_t>(d) + 1, 0);
-  for (int64_t i = 0; i < n_local; ++i) {
-    require(off[i] <= off[i + 1], "csr: row_offsets must be monotone");
-    for (int64_t p = off[i]; p < off[i + 1]; ++p) {
-      require(c64[p] >= 0 && c64[p] < d, "csr: column index out of range");
-      if (p > off[i]) require(c64[p - 1] < c64[p], "csr: column indices must be strictly increasing within a row");
-      require(std::isfinite(v[p]), "csr: non-finite value");
-      c32[p] = static_cast<int32_t>(c64[p]);
-      ccount[c64[p] + 1]++;
-    }
-  }
-  std::partial_sum(ccount.begin(), ccount.end(), ccount.begin());
-  std::vector<int32_t> crow(static_cast<size_t>(nnz));
-  std::vector<double> cval(static_cast<size_t>(nnz));
-  {
-    std::vector<int64_t> pos(ccount.begin(), ccount.end() - 1);
-    for (int64_t i = 0; i < n_local; ++i)
-      for (int64_t p = off[i]; p < off[i + 1]; ++p) {
-        const int64_t q = pos[c64[p]]++;
-        crow[q] = static_cast<int32_t>(i);
-        cval[q] = v[p];
-      }
-  }
-  OperatorStore& o = ctx->op;
-  wait_upload(ctx);
-  o = OperatorStore();
+  require(nnz < (int64_t{1} << 31), "csr: more than 2^31 entries");
+  OperatorStore o;  // (built aside: a rejected matrix leaves the context's operator as it was)
   o.sparse = true;
-  o.n = shard == 2 ? n_global : n_global;
+  o.n = n_global;
   o.d = d;
   o.shard = shard;
   o.off0 = row0;
   o.n_local = n_local;
   o.nnz = nnz;
   o.csr_off.alloc(off.size(), s);
-  o.csr_col.alloc(std::max<size_t>(c32.size(), 1), s);
-  o.csr_val.alloc(std::max<size_t>(v.size(), 1), s);
-  o.csc_off.alloc(ccount.size(), s);
-  o.csc_row.alloc(std::max<size_t>(crow.size(), 1), s);
-  o.csc_val.alloc(std::max<size_t>(cval.size(), 1), s);
+  o.csr_col.alloc(static_cast<size_t>(std::max<int64_t>(nnz, 1)), s);
+  o.csr_val.alloc(static_cast<size_t>(std::max<int64_t>(nnz, 1)), s);
   RP_CUDA(cudaMemcpyAsync(o.csr_off.get(), off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(o.csr_col.get(), c32.data(), sizeof(int32_t) * c32.size(), cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(o.csr_val.get(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(o.csc_off.get(), ccount.data(), sizeof(int64_t) * ccount.size(), cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(o.csc_row.get(), crow.data(), sizeof(int32_t) * crow.size(), cudaMemcpyHostToDevice, s));
-  RP_CUDA(cudaMemcpyAsync(o.csc_val.get(), cval.data(), sizeof(double) * cval.size(), cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    DBuf<int64_t> c64;
+    const int64_t* d_c64 = cols;
+    if (where != RP_DEVICE) {
+      c64.alloc(static_cast<size_t>(nnz), s);
+      RP_CUDA(cudaMemcpyAsync(c64.get(), cols, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+      d_c64 = c64.get();
+    }
+    RP_CUDA(cudaMemcpyAsync(o.csr_val.get(), vals, sizeof(double) * nnz,
+                            where == RP_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    DBuf<long long> flag(1, s);
+    const long long none = std::numeric_limits<long long>::max();
+    RP_CUDA(cudaMemcpyAsync(flag.get(), &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    csr_validate_convert(o.csr_off.get(), d_c64, o.csr_val.get(), n_local, d, o.csr_col.get(), flag.get(), s);
+    long long seen = none;
+    RP_CUDA(cudaMemcpyAsync(&seen, flag.get(), sizeof(seen), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (seen != none) {
+      switch (static_cast<int>(seen & 3)) {
+        case 1: throw InvalidArgument("csr: column index out of range");
+        case 2: throw InvalidArgument("csr: column indices must be strictly increasing within a row");
+        default: throw InvalidArgument("csr: non-finite value");
+      }
+    }
+  }
+  {
+    PanelCsc mirror;  // one panel over all rows = the CSC of the shard
+    build_panel_csc(o.csr_off.get(), o.csr_col.get(), o.csr_val.get(), n_local, d, nnz, std::max<int64_t>(n_local, 1),
+                    mirror, s);
+    o.csc_off = std::move(mirror.off);
+    o.csc_row = std::move(mirror.row);
+    o.csc_val = std::move(mirror.val);
+  }
   RP_CUDA(cudaStreamSynchronize(s));
   o.set = true;
+  wait_upload(ctx);
+  ctx->op = std::move(o);
 }
 
 void set_dense_impl(rp_ctx* ctx, int64_t n, int64_t d, int shard, int64_t off0, int64_t n_local, const double* a,

@@ -88,6 +88,28 @@ void build_impl(const int64_t* csr_off, const int32_t* csr_col, const double* cs
   RP_LAUNCH_CHECK();
 }
 
+// ---- ingest ---------------------------------------------------------------------
+
+__global__ void csr_validate_kernel(const int64_t* __restrict__ off, const int64_t* __restrict__ col,
+                                    const double* __restrict__ val, int64_t n, int64_t d, int32_t* __restrict__ c32,
+                                    long long* __restrict__ flag) {
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const int64_t p0 = off[r], p1 = off[r + 1];
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      const int64_t c = col[p];
+      int code = 0;
+      if (c < 0 || c >= d) code = 1;
+      else if (p > p0 && !(col[p - 1] < c)) code = 2;
+      else if (!isfinite(val[p])) code = 3;
+      if (code) atomicMin(flag, static_cast<long long>(4 * p + code));
+      c32[p] = static_cast<int32_t>(c);
+    }
+  }
+}
+
 // ---- the two passes ---------------------------------------------------------------
 
 // Yp (rows x cc, row-major) = M[row0 : row0 + rows] * Wr (d x cc, row-major).
@@ -205,6 +227,13 @@ void run_chunk(const int64_t* csr_off, const int32_t* csr_col, const double* csr
 }
 
 }  // namespace
+
+void csr_validate_convert(const int64_t* d_off, const int64_t* d_col64, const double* d_val, int64_t n, int64_t d,
+                          int32_t* d_col32, long long* d_flag, cudaStream_t s) {
+  if (n <= 0) return;
+  csr_validate_kernel<<<grid_for(n * 32), 256, 0, s>>>(d_off, d_col64, d_val, n, d, d_col32, d_flag);
+  RP_LAUNCH_CHECK();
+}
 
 void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, int64_t n, int64_t d,
                      int64_t nnz, int64_t panel_rows, PanelCsc& out, cudaStream_t s) {

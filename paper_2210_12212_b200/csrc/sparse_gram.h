@@ -59,6 +59,14 @@ void build_panel_csc(const int64_t* csr_off, const int32_t* csr_col, const doubl
 // l2_persist: mark the running sums Z (d x chunk) as persisting in L2 for the
 // duration of the product (stream access-policy window), so the panels'
 // Y_p gathers do not evict them.
+// CsrMatrix invariants on the device (matrix.cpp:22-50): column indices in
+// [0, d), strictly increasing within a row, finite values; writes the int32
+// column indices.  *d_flag (initialized to INT64_MAX by the caller) receives
+// min over violating entries p of 4 p + code (1 = range, 2 = order, 3 = value):
+// the violation a row-major scan meets first.
+void csr_validate_convert(const int64_t* d_off, const int64_t* d_col64, const double* d_val, int64_t n, int64_t d,
+                          int32_t* d_col32, long long* d_flag, cudaStream_t s);
+
 void sparse_gram(const int64_t* csr_off, const int32_t* csr_col, const double* csr_val, const PanelView& pc,
                  const double* W, int64_t ldw, int64_t cols, double* Y, int64_t ldy, int64_t chunk, cudaStream_t s,
                  bool l2_persist = false, int blocks_per_sm = 0);

@@ -182,3 +182,41 @@ def test_csr_panel_gram_empty_matrix(rp, ctx, oracle):
     oc, gc = _csr(rp, oracle, dense)
     got = rp.gram_apply(gc, np.ones((9, 3)), ctx=ctx)
     assert np.array_equal(got, np.zeros((9, 3)))
+
+
+def test_csr_invariants_checked_on_device(rp, ctx, oracle):
+    """CsrMatrix invariants (matrix.cpp:22-50) are checked where the entries
+    live: same messages as the reference's constructor, the violation a
+    row-major scan meets first is the one reported, and a rejected matrix
+    leaves the context's operator untouched."""
+    off = np.array([0, 2, 3, 5], dtype=np.int64)
+    col = np.array([0, 2, 1, 0, 3], dtype=np.int64)
+    val = np.array([1.0, -2.0, 3.0, 0.5, 4.0])
+    good = rp.Csr(3, 4, off, col, val)
+    dense = np.zeros((3, 4))
+    for r in range(3):
+        for p in range(off[r], off[r + 1]):
+            dense[r, col[p]] = val[p]
+    x = np.arange(1.0, 5.0)
+    assert np.array_equal(np.asarray(rp.apply(good, x, ctx=ctx)).reshape(-1), dense @ x)
+    y = np.array([1.0, -1.0, 2.0])
+    got_t = rp.apply_transpose(good, y, ctx=ctx)
+    assert np.array_equal(np.asarray(got_t).reshape(-1), dense.T @ y)  # (the device-built CSC mirror)
+    bad_cases = [
+        (off, np.array([0, 4, 1, 0, 3], dtype=np.int64), val, "column index out of range"),
+        (off, np.array([0, -1, 1, 0, 3], dtype=np.int64), val, "column index out of range"),
+        (off, np.array([2, 0, 1, 0, 3], dtype=np.int64), val, "strictly increasing"),
+        (off, np.array([0, 0, 1, 0, 3], dtype=np.int64), val, "strictly increasing"),
+        (off, col, np.array([1.0, -2.0, np.nan, 0.5, 4.0]), "non-finite"),
+        (off, col, np.array([1.0, -2.0, 3.0, 0.5, np.inf]), "non-finite"),
+        (np.array([0, 2, 1, 5], dtype=np.int64), col, val, "monotone"),
+        (np.array([1, 2, 3, 5], dtype=np.int64), col, val, "start at 0"),
+        # two violations: the earlier entry (order, entry 1) wins over the later one (range, entry 4)
+        (off, np.array([2, 0, 1, 0, 9], dtype=np.int64), val, "strictly increasing"),
+    ]
+    for o2, c2, v2, needle in bad_cases:
+        with pytest.raises(ValueError, match=needle):
+            rp.apply(rp.Csr(3, 4, o2, c2, v2), x, ctx=ctx)
+    # an empty matrix and an empty row are fine
+    empty = rp.Csr(2, 4, np.zeros(3, dtype=np.int64), np.zeros(0, dtype=np.int64), np.zeros(0))
+    assert np.array_equal(np.asarray(rp.apply(empty, x, ctx=ctx)).reshape(-1), np.zeros(2))
