@@ -1326,9 +1326,18 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   require(K >= 1, "path: empty right-hand side");
   // A dense primal operator still landing in chunks (RP_HOST_STREAM) is
   // consumed chunk by chunk below; every other case waits for the upload.
+  // (a Gaussian sketch is streamed when its local S, m x n_loc doubles, can stay resident: it is drawn
+  // once and applied to each column block as that lands)
+  bool gauss_resident = false;
+  if (spec.kind == kGaussian && ctx->op.set && !ctx->op.sparse) {
+    size_t free_b = 0, total_b = 0;
+    RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double need = 8.0 * static_cast<double>(spec.m) * static_cast<double>(ctx->op.shard == 1 ? ctx->op.n_local : ctx->op.n);
+    gauss_resident = need <= 0.45 * static_cast<double>(free_b);
+  }
   const bool stream_in = !dual && ctx->op.set && !ctx->op.sparse && ctx->op.shard != 2 &&
                          ctx->op.up.chunks() > 1 && ctx->op.up.next < ctx->op.up.chunks() &&
-                         spec.kind != kGaussian;
+                         (spec.kind != kGaussian || gauss_resident);
   const OpView op = stream_in ? ctx->op.primal() : (dual ? op_dual(ctx) : op_primal(ctx));
   // ihs_bin_path: spec.n == A.rows; dual_path: spec.n == A.cols (path_solver.cpp:294, 333-334)
   require(spec.n == op.n_global, dual ? "dual_path: spec.n must equal A.cols (the dual operator is A^T)"
@@ -1378,16 +1387,24 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
     // sketch its columns, form rows c0..c1 of c = A^T b and block row
     // G[c0:c1, 0:c1] of the Gram matrix (lower part; mirrored at the end).
     const Upload& up = ctx->op.up;
-    DBuf<double> ctmp(static_cast<size_t>(std::min<int64_t>(up.chunk, dim) * K), s);
+    // upload chunks consumed per step: one, or -- Gaussian sketch, whose block product streams all of S --
+    // as many as make the block at least 128 columns wide
+    const int64_t nchunks = static_cast<int64_t>(up.ev.size());
+    const int64_t group = spec.kind == kGaussian ? std::max<int64_t>(1, ceil_div(128, std::max<int64_t>(up.chunk, 1))) : 1;
+    DBuf<double> ctmp(static_cast<size_t>(std::min<int64_t>(up.chunk * group, dim) * K), s);
     if (use_matrix) gram.begin_matrix();
     Upload& upm = ctx->op.up;
-    const bool planned = spec.kind == kCountSketch || spec.kind == kSjlt || spec.kind == kSrht;
-    SketchPlan plan;  // draws / SRHT tables once, applied per column block
-    if (planned) sketch_plan(spec, op, plan, s);
-    for (size_t j = 0; j < up.ev.size(); ++j) {
-      const int64_t c0 = static_cast<int64_t>(j) * up.chunk, cc = std::min(up.chunk, dim - c0);
-      upm.enqueue(static_cast<int64_t>(j) + kUploadDepth);
-      RP_CUDA(cudaStreamWaitEvent(s, up.ev[j], 0));
+    const bool planned = spec.kind == kCountSketch || spec.kind == kSjlt || spec.kind == kSrht || spec.kind == kGaussian;
+    SketchPlan plan;  // draws / SRHT tables / Gaussian S once, applied per column block
+    if (planned) {
+      upm.enqueue(kUploadDepth * group);  // (the first blocks travel while the plan is drawn)
+      sketch_plan(spec, op, plan, s);
+    }
+    for (int64_t j = 0; j < nchunks; j += group) {
+      const int64_t j1 = std::min(nchunks, j + group);
+      const int64_t c0 = j * up.chunk, cc = std::min(up.chunk * (j1 - j), dim - c0);
+      upm.enqueue(j1 + kUploadDepth * group);
+      RP_CUDA(cudaStreamWaitEvent(s, up.ev[static_cast<size_t>(j1 - 1)], 0));  // (copy-stream order: the block is whole)
       OpView sub = op;
       sub.a = op.a + c0 * op.ld;
       sub.d = cc;

@@ -612,7 +612,27 @@ void sketch_plan(const SketchSpecC& spec, const OpView& op, SketchPlan& plan, cu
     draw_count(spec.seed, spec.n, plan.rpb, plan.blocks, entry, plan.h.get(), plan.sg.get(), stream);
     return;
   }
-  require(spec.kind == kSrht, "sketch plan: only CountSketch / SJLT / SRHT are planned");
+  if (spec.kind == kGaussian) {
+    require(!op.sparse, "sketch plan: the Gaussian plan needs a dense operator");
+    const double scale = 1.0 / std::sqrt(static_cast<double>(m));
+    plan.gauss_rows = op.n_loc;
+    plan.gauss_s.alloc(static_cast<size_t>(m * op.n_loc), stream);
+    if (op.row0 == 0 && op.n_loc == spec.n) {
+      // unsharded: S is the normal stream [0, m n) itself (sketch.cpp:86-95)
+      draw_gauss_stream(spec.seed, 0, m * op.n_loc, scale, plan.gauss_s.get(), stream);
+    } else {
+      DBuf<uint64_t> states(static_cast<size_t>(m) * 312, stream);
+      DBuf<int64_t> cursor(static_cast<size_t>(m), stream);
+      GaussRows g;
+      g.d_states = states.get();
+      g.d_cursor = cursor.get();
+      gauss_rows_init(spec.seed, m, op.row0, spec.n, g, stream);
+      gauss_rows_next(g, op.n_loc, scale, plan.gauss_s.get(), op.n_loc, stream);
+      RP_CUDA(cudaStreamSynchronize(stream));  // (states / cursor are released with this frame)
+    }
+    return;
+  }
+  require(spec.kind == kSrht, "sketch plan: only Gaussian / CountSketch / SJLT / SRHT are planned");
   int64_t npad = 1;
   int P = 0;
   while (npad < spec.n) {
@@ -692,6 +712,23 @@ void sketch_apply_planned(const SketchPlan& plan, const OpView& op, double* d_sa
           plan.sg.get(), d_sa, m);
     }
     RP_LAUNCH_CHECK();
+    return;
+  }
+  if (spec.kind == kGaussian) {
+    require(!op.sparse && op.n_loc == plan.gauss_rows, "sketch plan: operator changed");
+    GemmArgs ga;  // SA[:, block] = S_local (m x n_loc) * M_local[:, block]
+    ga.opa = Op::T;
+    ga.opb = op.trans ? Op::T : Op::N;
+    ga.m = m;
+    ga.n = d;
+    ga.k = op.n_loc;
+    ga.a = plan.gauss_s.get();
+    ga.lda = op.n_loc;
+    ga.b = op.a;
+    ga.ldb = op.ld;
+    ga.c = d_sa;
+    ga.ldc = m;
+    dgemm(ga, stream);
     return;
   }
   const int64_t npad = plan.npad;

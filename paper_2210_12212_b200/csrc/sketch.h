@@ -51,6 +51,11 @@ struct SketchPlan {
   std::vector<int32_t> meta;
   DBuf<int64_t> d_tpos;
   DBuf<int32_t> d_meta;
+  // Gaussian (dense operators): the local columns of S, drawn once -- row r of
+  // S at gauss_s + r * n_loc (column-major n_loc x m) -- so that column blocks
+  // of the operator can be sketched as they arrive (streamed uploads).
+  DBuf<double> gauss_s;
+  int64_t gauss_rows = 0;
 };
 void sketch_plan(const SketchSpecC& spec, const OpView& op, SketchPlan& plan, cudaStream_t stream);
 void sketch_apply_planned(const SketchPlan& plan, const OpView& op, double* d_sa, cudaStream_t stream);

@@ -26,11 +26,11 @@ def _run(rp, ctx, a, b, cfg, spec, rho, stream):
 
 
 @pytest.mark.parametrize("kind,K,mode", [("srht", 1, -1), ("srht", 2, 0), ("countsketch", 1, 1), ("sjlt", 1, -1),
-                                         ("identity", 1, 1)])
+                                         ("identity", 1, 1), ("gaussian", 1, -1), ("gaussian", 2, 1)])
 def test_streamed_upload_matches_resident_path(rp, ctx, oracle, kind, K, mode):
     w = workloads.c2(scale=1 / 16)
     n, d = w.a.shape
-    m = n if kind == "identity" else 16 * d
+    m = n if kind == "identity" else (4 * d if kind == "gaussian" else 16 * d)  # (Gaussian: S stays resident)
     s = 4 if kind == "sjlt" else 1
     b = np.asfortranarray(np.concatenate([w.b] + [w.b * (k + 2) - 0.5 for k in range(K - 1)], axis=1))
     grid = rp.log_grid(w.lambda_min, w.lambda_max, 40)
@@ -125,3 +125,25 @@ def test_streamed_upload_pageable_and_column_shard(rp, ctx, oracle):
         assert np.array_equal(outs[0], outs[1])
     finally:
         ctx.set_option("upload_chunk_bytes", 32 << 20)
+
+
+def test_streamed_gaussian_blocks_of_several_chunks(rp, ctx, oracle):
+    """Gaussian sketch through the streamed upload: S is drawn once and applied
+    to blocks of several upload chunks (at least 128 columns wide); d = 300 with
+    50-column chunks gives blocks of 150 columns.  Against the oracle."""
+    rng = np.random.default_rng(11)
+    n, d, m = 2048, 300, 600
+    a = np.asfortranarray(rng.standard_normal((n, d)) / np.sqrt(np.arange(1, d + 1)))
+    b = np.asfortranarray((a @ rng.standard_normal(d) + 0.1 * rng.standard_normal(n)).reshape(n, 1))
+    grid = rp.log_grid(1e-2, 1e1, 12)
+    rho = workloads.mp_envelope(d, m)
+    cfg = rp.PathConfig(1e-2, 1e1, grid, 1e-6)
+    ctx.set_option("upload_chunk_bytes", n * 8 * 50)
+    try:
+        xs, keep = _run(rp, ctx, a, b, cfg, rp.SketchSpec("gaussian", m, n, 1, 5), rp.RhoBounds.manual(*rho), True)
+    finally:
+        ctx.set_option("upload_chunk_bytes", 32 << 20)
+    ref = oracle.ihs_bin_path(a, b, oracle.PathConfig(1e-2, 1e1, grid, 1e-6, None),
+                              oracle.SketchSpec("gaussian", m, n, 1, 5), oracle.RhoBounds.manual(*rho))
+    worst = max(oracle.rel_error(xs[t, 0], p.solution[:, 0]) for t, p in enumerate(ref.points))
+    assert worst < 1e-8
