@@ -1329,7 +1329,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   // (a Gaussian sketch is streamed when its local S, m x n_loc doubles, can stay resident: it is drawn
   // once and applied to each column block as that lands)
   bool gauss_resident = false;
-  if (spec.kind == kGaussian && ctx->op.set && !ctx->op.sparse) {
+  if (spec.kind == kGaussian && !dual && ctx->op.set && !ctx->op.sparse && ctx->op.shard != 2 &&
+      ctx->op.up.chunks() > 1 && ctx->op.up.next < ctx->op.up.chunks()) {  // (only when an upload is streaming)
     size_t free_b = 0, total_b = 0;
     RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double need = 8.0 * static_cast<double>(spec.m) * static_cast<double>(ctx->op.shard == 1 ? ctx->op.n_local : ctx->op.n);
