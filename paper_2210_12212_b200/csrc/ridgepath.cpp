@@ -274,6 +274,7 @@ struct Upload {
 constexpr int64_t kUploadDepth = 2;  // chunks kept in flight ahead of the consumer
 
 struct OperatorStore {
+  double free_after_alloc = 0.0;  // free device bytes when a streamed upload's buffer was allocated
   bool set = false;
   bool sparse = false;
   int shard = 0;  // 0 none, 1 rows, 2 cols
@@ -1331,10 +1332,8 @@ void run_path(rp_ctx* ctx, bool dual, const double* b_in, int64_t K, const PathC
   bool gauss_resident = false;
   if (spec.kind == kGaussian && !dual && ctx->op.set && !ctx->op.sparse && ctx->op.shard != 2 &&
       ctx->op.up.chunks() > 1 && ctx->op.up.next < ctx->op.up.chunks()) {  // (only when an upload is streaming)
-    size_t free_b = 0, total_b = 0;
-    RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double need = 8.0 * static_cast<double>(spec.m) * static_cast<double>(ctx->op.shard == 1 ? ctx->op.n_local : ctx->op.n);
-    gauss_resident = need <= 0.45 * static_cast<double>(free_b);
+    gauss_resident = need <= 0.45 * ctx->op.free_after_alloc;
   }
   const bool stream_in = !dual && ctx->op.set && !ctx->op.sparse && ctx->op.shard != 2 &&
                          ctx->op.up.chunks() > 1 && ctx->op.up.next < ctx->op.up.chunks() &&
@@ -1872,6 +1871,14 @@ void set_dense_impl(rp_ctx* ctx, int64_t n, int64_t d, int shard, int64_t off0, 
   } else if (where == RP_HOST_STREAM) {
     // Column chunks of ~upload_chunk_bytes (32 MiB) on the copy stream, one event each.
     o.owned.alloc(static_cast<size_t>(std::max<int64_t>(rows * cols, 1)), s);
+    {
+      // free device memory once the operator's buffer exists (asked here, before the copies start: the query
+      // takes ~10 ms beside a running upload); the streamed Gaussian sketch budgets its resident S with it
+      size_t free_b = 0, total_b = 0;
+      RP_CUDA(cudaStreamSynchronize(s));
+      RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      o.free_after_alloc = static_cast<double>(free_b);
+    }
     if (!ctx->copy) RP_CUDA(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
     cudaEvent_t alloc_done;
     RP_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
