@@ -118,6 +118,10 @@ template <int CPL>
 __global__ void __launch_bounds__(256) pass1_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                                                     const double* __restrict__ val, int64_t row0, int64_t rows,
                                                     const double* __restrict__ wr, int cc, double* __restrict__ yp) {
+  // (the passes of a chunk are chained by programmatic dependent launch: the next pass's blocks take the
+  // slots this one's tail frees, and wait here until the previous grid -- whose Yp / Z they touch -- is done)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -162,6 +166,8 @@ __global__ void __launch_bounds__(256) pass2_kernel(const int64_t* __restrict__ 
                                                     const double* __restrict__ pval, int64_t d, int64_t row0,
                                                     const double* __restrict__ yp, int cc, double* __restrict__ z,
                                                     int first) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -217,11 +223,23 @@ void run_chunk(const int64_t* csr_off, const int32_t* csr_col, const double* csr
   for (int64_t p = 0; p < pc.panels; ++p) {
     const int64_t row0 = p * pc.panel_rows;
     const int64_t rows = std::min(pc.panel_rows, pc.n - row0);
-    pass1_kernel<CPL><<<std::min(grid_for(rows * 32), cap), 256, pad, s>>>(csr_off, csr_col, csr_val, row0, rows, wr,
-                                                                          cc, yp);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = pad;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(std::min(grid_for(rows * 32), cap));
+    RP_CUDA(cudaLaunchKernelEx(&cfg, pass1_kernel<CPL>, csr_off, csr_col, csr_val, row0, rows, wr, cc, yp));
     RP_LAUNCH_CHECK();
-    pass2_kernel<CPL><<<std::min(grid_for(pc.d * 32), cap), 256, pad, s>>>(pc.off + p * pc.d, pc.row, pc.val, pc.d,
-                                                                          row0, yp, cc, z, p == 0);
+    cfg.gridDim = dim3(std::min(grid_for(pc.d * 32), cap));
+    const int64_t* poff = pc.off + p * pc.d;
+    const int first = p == 0 ? 1 : 0;
+    RP_CUDA(cudaLaunchKernelEx(&cfg, pass2_kernel<CPL>, poff, pc.row, pc.val, pc.d, row0,
+                               static_cast<const double*>(yp), cc, z, first));
     RP_LAUNCH_CHECK();
   }
 }
